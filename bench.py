@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Benchmark of the batched explicit Schur-complement assembly (arXiv 2509.21037 hot path) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2] [--impl ours|reference]
+
+One step = one sc_assemble_batch over the config's whole batch of subdomains (X init + stepped
+supernodal TRSM + block-sparse SYRK), with the L values resident in HBM.  Multi-GPU (torchrun):
+one process per GPU, each rank assembles its own cluster of subdomains (weak scaling, P:276-283:
+"each process handles a single cluster"); no collective on the assembly path; time = max over
+ranks of the CUDA-event time.  `--impl reference` times the CPU oracle (oracle/) on the host cores
+on a bounded sample of the same workload (rank 0 only).  Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PAPER_A100_MS = {  # PAPER.md Fig. 8 "sep", optimized GPU, per subdomain (context only, A100)
+    "cfg1": 0.0470,  # 2D n=81
+    "cfg2": 0.5441,  # 2D n=4,225
+    "cfg3": 2.008,   # 3D n=4,913
+}
+METRIC = "SC assembly subdomains/s + FP64 GFLOP/s at 1/2/4/8 B200; amortization iters"
+CFG_DESC = {
+    "cfg1": "2D heat 4x4=16 subdomains of 8x8 Q1 (81 DOF)",
+    "cfg2": "2D heat 1024 subdomains of 64x64 Q1 (4225 DOF)",
+    "cfg3": "3D heat 512 subdomains of 16^3 Q1 hex (4913 DOF)",
+    "cfg4": "3D elasticity 512 subdomains of 12^3 Q1 hex (6591 DOF)",
+    "cfg5": "3D elasticity 64 subdomains of 24^3 Q1 hex (46875 DOF)",
+}
+
+
+def load_peaks():
+    peaks = {}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        peaks.update(json.load(open(p)))
+    # FP64 DMMA peak measured on this pool's B200 by tools/fp64_peak.cu (profiles/fp64_peak_r01.txt)
+    peaks.setdefault("fp64_tflops", 37.108)
+    peaks.setdefault("fp64_tflops_source", "measured: tools/fp64_peak.cu DMMA.8x8x4 loop, profiles/fp64_peak_r01.txt")
+    if "hbm_gbs" not in peaks:
+        peaks["hbm_gbs"] = 6650.0
+        peaks["hbm_source"] = "fallback (B200_PROFILING.md)"
+    return peaks
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, nm in enumerate(names):
+                if len(r) > 3 + k and "Active" in r[3 + k] and "Not" not in r[3 + k]:
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]), "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def cpu_oracle_sample(problem, budget_s: float, threads: int):
+    """Oracle (as it stands) over subdomains of the workload, one subdomain per host thread, until
+    `budget_s` elapses; returns (subdomains/s, subdomains done, wall seconds)."""
+    import oracle
+    from concurrent.futures import ThreadPoolExecutor
+    subs = problem.subdomains
+    done, t0 = 0, time.perf_counter()
+    with ThreadPoolExecutor(max_workers=threads) as ex:
+        while True:
+            batch = [subs[(done + k) % len(subs)] for k in range(threads)]
+            list(ex.map(oracle.subdomain_F, batch))
+            done += len(batch)
+            if time.perf_counter() - t0 >= budget_s:
+                break
+    wall = time.perf_counter() - t0
+    return done / wall, done, wall
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from synth import config_problem
+    P = config_problem(args.config)
+    threads = len(os.sched_getaffinity(0))
+    per_step = []
+    total_done, total_wall = 0, 0.0
+    for k in range(args.warmup + args.steps):
+        v, done, wall = cpu_oracle_sample(P, args.ref_budget, threads)
+        if k >= args.warmup:
+            per_step.append(wall / done)
+            total_done += done
+            total_wall += wall
+    value = total_done / total_wall
+    useful = None
+    sample = (f"{args.steps} steps x >= {args.ref_budget:.0f}s of oracle work each, one subdomain per thread "
+              f"({total_done} subdomains of {args.config}), extrapolated as subdomains/s")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "subdomains/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * len(P.subdomains) / value,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": CFG_DESC[args.config], "subdomains": len(P.subdomains)},
+            "cpu_baseline": {"value": value, "unit": "subdomains/s", "cores": threads, "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "subdomains/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="cfg2", choices=list(CFG_DESC))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--skip", default="exact", choices=["none", "envelope", "exact"])
+    ap.add_argument("--tile", type=int, default=0)
+    ap.add_argument("--panel", type=int, default=0)
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
+    ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2509_21037_b200 import SCPlan
+    from synth import config_problem
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = load_peaks()
+
+    # each rank: its own cluster (replica of the config batch with its own coefficients)
+    t_plan0 = time.perf_counter()
+    P = config_problem(args.config, seed=rank)
+    skip = {"none": 0, "envelope": 1, "exact": 2}[args.skip]
+    plan = SCPlan(P.subdomains, n_lambda=P.n_lambda, skip=skip, tile_cols=args.tile, panel_cols=args.panel,
+                  device=local)
+    t_plan = time.perf_counter() - t_plan0
+    st = plan.stats()
+    Ls = [torch.from_numpy(np.ascontiguousarray(sd.L_values)).cuda() for sd in P.subdomains]
+    nsub = len(P.subdomains)
+    stream = torch.cuda.current_stream()
+    useful = st["flops_trsm_useful"] + st["flops_syrk_useful"]
+
+    # warm-up
+    for _ in range(args.warmup):
+        plan.assemble(Ls)
+    torch.cuda.synchronize()
+    plan.check()
+
+    # timed region: K steps, per-kernel events recorded inside sc_assemble_batch on `stream`
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for k in range(args.steps):
+            plan.set_timing_events(*evs[k])
+            plan.assemble(Ls)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    plan.set_timing_events(None, None, None)
+    if world > 1:
+        dist.barrier()
+    ms_total = start.elapsed_time(stop)
+    ms_trsm = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    ms_syrk = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    plan.check()
+    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_step = t.item() / args.steps
+    value = world * nsub / (ms_step / 1e3)
+
+    # e2e through the public API with HOST inputs: pinned L values -> H2D inside the call ->
+    # assemble -> one explicit apply q = F lambda (solution stage) -> D2H of q
+    e2e = None
+    if not args.no_e2e:
+        hostL = [torch.from_numpy(np.ascontiguousarray(sd.L_values)).pin_memory() for sd in P.subdomains]
+        lam_h = torch.from_numpy(np.random.default_rng(rank).standard_normal(P.n_lambda)).pin_memory()
+        lam_d = torch.empty(P.n_lambda, dtype=torch.float64, device="cuda")
+        q_d = torch.empty_like(lam_d)
+        q_h = torch.empty(P.n_lambda, dtype=torch.float64).pin_memory()
+        for _ in range(args.warmup):
+            plan.assemble_host(hostL)
+            lam_d.copy_(lam_h, non_blocking=True)
+            plan.apply_global(lam_d, q_d)
+            q_h.copy_(q_d, non_blocking=True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            plan.assemble_host(hostL)
+            lam_d.copy_(lam_h, non_blocking=True)
+            plan.apply_global(lam_d, q_d)
+            q_h.copy_(q_d, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = int(sum(8 * sd.L_values.size for sd in P.subdomains) + 8 * P.n_lambda)
+        e2e = {"value": world * nsub / (te.item() / 1e3), "unit": "subdomains/s", "ms_per_step": te.item(),
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * P.n_lambda,
+               "includes": "pinned H2D of all L values + assemble + 1 sc_apply (+all-reduce) + D2H of q"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (useful FP64 flops per launch / live event time)
+    dom = "trsm" if ms_trsm >= ms_syrk else "syrk"
+    dom_ms = ms_trsm if dom == "trsm" else ms_syrk
+    dom_flops = st["flops_trsm_useful"] if dom == "trsm" else st["flops_syrk_useful"]
+    achieved = dom_flops / (dom_ms / 1e3) / 1e12
+    prof_traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
+    if os.path.exists(tp):
+        prof_traffic = json.load(open(tp)).get(dom)
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                "frac": achieved / peaks["fp64_tflops"], "traffic": prof_traffic, "kernel": f"{dom}",
+                "dtype": "f64 (DMMA m8n8k4)", "peak_source": peaks["fp64_tflops_source"],
+                "algorithmic": "useful (etree-exact) FP64 flops of the phase per launch",
+                "share_of_step": dom_ms / ms_step}
+    cpu = None
+    if not args.no_cpu_baseline:
+        threads = len(os.sched_getaffinity(0))
+        v, done, wall = cpu_oracle_sample(P, args.cpu_budget, threads)
+        cpu = {"value": v, "unit": "subdomains/s", "cores": threads, "kind": "oracle",
+               "sample": f"{done} subdomains of {args.config} ({wall:.1f}s, one subdomain per host thread)"}
+    clocks = clk.summary()
+    line = {
+        "metric": METRIC, "value": value, "unit": "subdomains/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": CFG_DESC[args.config], "name": args.config, "subdomains_per_gpu": nsub,
+                   "skip": args.skip, "tile_cols": st["tile_cols"], "panel_cols": st["panel_cols"],
+                   "parallelism": f"subdomain-sharded x{world} (no collective in assembly)",
+                   "l2": f"inputs larger than L2: L values {st['bytes_L_values'] / 1e9:.2f} GB, "
+                         f"X {st['bytes_X'] / 1e9:.2f} GB, F {8 * sum(m * m for m in plan.m) / 1e9:.2f} GB per GPU"},
+        "gflops_useful": world * useful / (ms_step / 1e3) / 1e9,
+        "gflops_executed": world * (st["flops_trsm_executed"] + st["flops_syrk_executed"]) / (ms_step / 1e3) / 1e9,
+        "fp64_frac_useful": useful / (ms_step / 1e3) / 1e12 / peaks["fp64_tflops"],
+        "phase_ms": {"trsm": ms_trsm, "syrk": ms_syrk},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": args.steps * plan.launches_per_assemble,
+        "clocks": clocks, "plan_s": t_plan,
+        "paper_context": {"a100_sep_opt_ms_per_subdomain": PAPER_A100_MS.get(args.config),
+                          "note": "PAPER.md Fig. 8, A100, triangles/tets; context only"},
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

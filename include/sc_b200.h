@@ -1,0 +1,170 @@
+/* sc_b200.h — C ABI of the B200-native batched Schur-complement (FETI dual operator) assembly.
+ *
+ * What it computes (eq. localdualoperator, eq. localdualoperatorwithU):
+ *     F_i = B~_i K_{i,reg}^{-1} B~_i^T = (L_i^{-1} B~_i^T)^T (L_i^{-1} B~_i^T) = X_i^T X_i
+ * for a batch of subdomains i, from the precomputed sparse Cholesky factor L_i of the permuted
+ * regularised stiffness (P K_reg P^T = L L^T) and the sparse gluing matrix B~_i^T (§3:
+ * "The input for the algorithm is the matrix B~_i^T together with the factor L_i").  The columns of
+ * B~^T are permuted to the stepped shape; X = L^{-1} B~^T is a forward-substitution TRSM
+ * that preserves the zeros above the column pivots (§3.2) and is blocked by supernodal
+ * factor panels with pruned sub-diagonal rows (factor splitting + pruning); F = X^T X is
+ * a SYRK restricted to the structurally non-zero rows of each output tile (§3.3).  F is
+ * kept in stepped order; the permutation back to the original multiplier order is folded
+ * into sc_apply's gather/scatter and into sc_get_F.
+ *
+ * Three solver stages: sc_plan_create = "initialization" (symbolic, host, once per
+ * pattern); sc_assemble_batch = "preprocessing" (numeric, device, whenever L values change);
+ * sc_apply = "solution" (one application q = sum_i scatter(F_i gather(lambda)) per iteration,
+ * eq. dualop_apply_expl).
+ *
+ * Conventions
+ *   - All integers are 0-based.  Matrices in CSC: colptr[ncols+1], rowidx[nnz].
+ *   - Device pointers are CUDA device memory of the plan's device (e.g. torch tensor data_ptr()).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream); all device work
+ *     of a call is enqueued on it and the call returns without synchronising unless stated.
+ *   - No C++ exception crosses this boundary.  A non-OK status leaves a thread-local message
+ *     readable with sc_last_error().
+ *   - Errors detected on the device (a non-positive or non-finite L diagonal met by the TRSM)
+ *     are sticky per plan: they are reported by the next synchronising call (sc_check,
+ *     sc_get_F, sc_get_X) as SC_ERR_ZERO_PIVOT; F of the flagged subdomain is undefined.
+ */
+#ifndef SC_B200_H
+#define SC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct sc_plan_s* sc_plan_t;
+
+typedef enum {
+  SC_OK = 0,
+  SC_ERR_INVALID_ARG = 1, /* NULL pointer, negative size, inconsistent sizes, bad option value   */
+  SC_ERR_PATTERN = 2,     /* L not lower / rows unsorted / diagonal not first / not a Cholesky
+                             fill pattern (not closed under its elimination tree); B~^T row out of
+                             range; perm not a bijection                                          */
+  SC_ERR_ZERO_PIVOT = 3,  /* L_kk <= 0 or non-finite (found on the device, sticky)               */
+  SC_ERR_OOM = 4,         /* device allocation failed                                             */
+  SC_ERR_CUDA = 5,        /* any other CUDA error                                                 */
+  SC_ERR_STATE = 6        /* call not valid in this plan state (e.g. host-only plan, no F yet)    */
+} sc_status;
+
+/* One subdomain as the caller describes it.  sc_plan_create copies what it needs; the caller may
+   free these arrays after it returns. */
+typedef struct {
+  int32_t n;                 /* DOFs of the subdomain (order of L)                                 */
+  int32_t m;                 /* local multipliers = columns of B~^T (0 allowed: empty F)           */
+  const int64_t* L_colptr;   /* n+1; CSC of L, lower triangle incl. diagonal, diagonal FIRST in
+                                each column, row indices strictly ascending                        */
+  const int32_t* L_rowidx;   /* nnz(L) = L_colptr[n]                                               */
+  const int32_t* perm;       /* n; perm[new] = old: L factors P K_reg P^T.  NULL = identity        */
+  const int32_t* Bt_colptr;  /* m+1; CSC of B~^T (n x m)                                           */
+  const int32_t* Bt_rowidx;  /* nnz(B~^T); rows in the ORIGINAL DOF numbering (before perm)         */
+  const double* Bt_values;   /* nnz(B~^T); typically +-1 (signed Boolean), any value works  */
+  const int64_t* lambda_map; /* m; local multiplier -> global multiplier id in [0, n_lambda_global).
+                                May be NULL if sc_apply is never called                            */
+} sc_subdomain_desc;
+
+enum { SC_SKIP_NONE = 0,      /* no B~ sparsity: every column solved from row 0 ("original" [PDSEC],
+                                 P:412-428), supernodal factor sparsity still used                 */
+       SC_SKIP_ENVELOPE = 1,  /* the paper's stepped envelope: rows >= the tile's highest pivot,
+                                 SYRK k from the highest pivot                  */
+       SC_SKIP_EXACT = 2 };   /* elimination-tree reach of each tile's pivots (default; beyond the
+                                 paper's envelope, exact structural zeros of L^{-1} B~^T)          */
+
+typedef struct {
+  int32_t precision;         /* 64 (FP64).  Other values -> SC_ERR_INVALID_ARG in this version     */
+  int32_t skip;              /* SC_SKIP_*                                                          */
+  int32_t tile_cols;         /* T: RHS column-tile width, 16, 32 or 64; 0 = automatic              */
+  int32_t panel_cols;        /* max factor panel width (factor-splitting block), <= 64; 0 = 64      */
+  int64_t n_lambda_global;   /* length of the global dual vector used by sc_apply                   */
+  int32_t device;            /* CUDA device ordinal; -1 = host-only plan (symbolic + stats only)    */
+  int32_t reserved[7];       /* must be zero                                                        */
+} sc_options;
+
+/* Work and size counters (SURVEY.md Appendix A definitions).  flops: 2 per multiply-add, 1 per
+   division.  "useful" = etree-exact structural non-zero work (independent of skip mode and tile
+   size); "envelope" = the paper's stepped envelope at block size 1; "dense" = original dense
+   algorithm (m n^2 TRSM, n m (m+1) SYRK); "sparse_orig" = original sparse-factor TRSM m(2nnz(L)-n);
+   "executed" = what this plan's kernels compute. */
+typedef struct {
+  int32_t nsub, n_classes, tile_cols, panel_cols;
+  int64_t sum_n, sum_m, max_m, sum_nnz_L;
+  int64_t trsm_tasks, trsm_steps, syrk_tasks, syrk_segments;
+  double flops_trsm_useful, flops_syrk_useful;
+  double flops_trsm_envelope, flops_syrk_envelope;
+  double flops_trsm_dense, flops_syrk_dense, flops_trsm_sparse_orig;
+  double flops_trsm_executed, flops_syrk_executed;
+  double bytes_L_values;     /* 8 nnz(L), summed                                                   */
+  double bytes_F_lower;      /* 8 m(m+1)/2, summed                                                 */
+  double bytes_X;            /* X workspace (tile-exact strips)                                    */
+  double device_bytes;       /* everything the plan allocated on the device                        */
+  double bytes_apply;        /* algorithmic bytes of one sc_apply (F lower read once + vectors)    */
+} sc_stats;
+
+/* Fill `opt` with defaults: precision 64, skip EXACT, tile/panel auto, device 0. */
+void sc_options_default(sc_options* opt);
+
+/* Initialization stage: validate patterns, build the symbolic plan (stepped order, elimination tree,
+   supernodes, per-tile reach and panel lists, SYRK segment lists), deduplicate subdomains with
+   identical patterns into classes, and (device >= 0) upload it and allocate the X workspace and the
+   persistent F storage.  On success *out owns everything; release it with sc_plan_destroy. */
+sc_status sc_plan_create(const sc_subdomain_desc* sd, int32_t nsub, const sc_options* opt, sc_plan_t* out);
+
+/* Preprocessing stage: assemble every F_i of the plan from the L values.
+   L_values: HOST array of nsub DEVICE pointers; L_values[i] points to nnz(L_i) doubles in the CSC
+   order of sd[i].L_colptr/L_rowidx.  They must stay valid until the work on `stream` completes.
+   Enqueues the TRSM and SYRK kernels; does not synchronise. */
+sc_status sc_assemble_batch(sc_plan_t p, const double* const* L_values, void* stream);
+
+/* Same as sc_assemble_batch but the L values live in HOST memory (ideally pinned): the call copies
+   them to a plan-owned device staging buffer on `stream` (host->device inside the call, the
+   paper's "copies factor L_i to the GPU") and then assembles.  Does not synchronise. */
+sc_status sc_assemble_batch_host(sc_plan_t p, const double* const* L_values_host, void* stream);
+
+/* Solution stage: q[g] = sum_i sum_{a: lambda_map_i(a) = g} (F_i lambda_i)(a), lambda_i(a) =
+   lambda[lambda_map_i(a)]  (eq. dualop_apply_expl per subdomain, summed additively).
+   lambda, q: DEVICE arrays of n_lambda_global doubles.  q is overwritten with this plan's partial
+   sum; multi-GPU callers all-reduce q over ranks (torch.distributed / NCCL).  Deterministic. */
+sc_status sc_apply(sc_plan_t p, const double* lambda, double* q, void* stream);
+
+/* Synchronise the plan's last stream and report a sticky device error (SC_ERR_ZERO_PIVOT). */
+sc_status sc_check(sc_plan_t p);
+
+/* Export F_i as a full symmetric m_i x m_i matrix in the ORIGINAL local multiplier order
+   (F(a,b) at F[b*ld + a], column-major), into HOST memory.  Synchronises. */
+sc_status sc_get_F(sc_plan_t p, int32_t i, double* F, int64_t ld);
+
+/* Debug hook for the X-phase pins: X_i = L_i^{-1} P B~_i^T(:, sigma) as a dense n_i x m_i HOST
+   matrix (column-major, ld = n_i; rows in the permuted order, columns in stepped order); entries
+   outside the plan's strips are written as exact zeros.  Valid after sc_assemble_batch.  Also
+   returns the stepped order: sigma[a] = original local column of stepped column a (may be NULL). */
+sc_status sc_get_X(sc_plan_t p, int32_t i, double* X, int32_t* sigma);
+
+/* Host-side structure query (works for host-only plans): the permuted rows held by the X strip of
+   stepped column `a` of subdomain i, ascending, in rows[0..*nrows) (capacity n_i). */
+sc_status sc_plan_strip_rows(sc_plan_t p, int32_t i, int32_t a, int32_t* rows, int32_t* nrows);
+
+sc_status sc_plan_stats(sc_plan_t p, sc_stats* out);
+
+/* Measurement hook: when set (non-NULL), every following sc_assemble_batch records the three
+   cudaEvent_t handles (passed as void*) on its stream: ev0 before the TRSM kernel, ev1 between the
+   TRSM and the SYRK kernel, ev2 after the SYRK kernel.  Pass NULLs to disable. */
+sc_status sc_set_timing_events(sc_plan_t p, void* ev0, void* ev1, void* ev2);
+
+/* Number of kernel launches one sc_assemble_batch / sc_apply enqueues. */
+int32_t sc_launches_per_assemble(sc_plan_t p);
+int32_t sc_launches_per_apply(sc_plan_t p);
+
+/* Frees F storage, workspace and device copies (synchronises the device first). */
+void sc_plan_destroy(sc_plan_t p);
+
+/* Thread-local message for the last non-OK status on this thread ("" if none). */
+const char* sc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SC_B200_H */

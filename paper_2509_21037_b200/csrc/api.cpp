@@ -1,0 +1,194 @@
+// api.cpp — the C ABI (include/sc_b200.h).  Marshalling and validation only; every arithmetic
+// step of the path runs in kernels.cu.
+#include <algorithm>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "sc_internal.h"
+
+struct sc_plan_s {
+  sc::Plan P;
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+sc_status fail(sc_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+}  // namespace
+
+extern "C" {
+
+void sc_options_default(sc_options* opt) {
+  if (!opt) return;
+  std::memset(opt, 0, sizeof(*opt));
+  opt->precision = 64;
+  opt->skip = SC_SKIP_EXACT;
+  opt->tile_cols = 0;
+  opt->panel_cols = 0;
+  opt->n_lambda_global = 0;
+  opt->device = 0;
+}
+
+sc_status sc_plan_create(const sc_subdomain_desc* sd, int32_t nsub, const sc_options* opt, sc_plan_t* out) {
+  if (!out || !opt) return fail(SC_ERR_INVALID_ARG, "sc_plan_create: NULL opt or out");
+  *out = nullptr;
+  sc_plan_s* h = new (std::nothrow) sc_plan_s();
+  if (!h) return fail(SC_ERR_OOM, "host allocation failed");
+  std::string err;
+  sc_status st;
+  try {
+    st = sc::build_plan(sd, nsub, *opt, h->P, err);
+    if (st == SC_OK && opt->device >= 0) st = sc::upload_plan(h->P, err);
+  } catch (const std::bad_alloc&) {
+    st = SC_ERR_OOM;
+    err = "host allocation failed";
+  } catch (...) {
+    st = SC_ERR_INVALID_ARG;
+    err = "unexpected exception in sc_plan_create";
+  }
+  if (st != SC_OK) {
+    sc::free_plan_device(h->P);
+    delete h;
+    return fail(st, err);
+  }
+  *out = h;
+  g_last_error.clear();
+  return SC_OK;
+}
+
+sc_status sc_assemble_batch(sc_plan_t p, const double* const* L_values, void* stream) {
+  if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
+  if (!L_values && p->P.nsub > 0) return fail(SC_ERR_INVALID_ARG, "NULL L_values");
+  std::string err;
+  sc_status st = sc::launch_assemble(p->P, L_values, stream, err);
+  return st == SC_OK ? SC_OK : fail(st, err);
+}
+
+sc_status sc_assemble_batch_host(sc_plan_t p, const double* const* L_values_host, void* stream) {
+  if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
+  if (!L_values_host && p->P.nsub > 0) return fail(SC_ERR_INVALID_ARG, "NULL L_values_host");
+  std::string err;
+  std::vector<const double*> dptrs;
+  sc_status st = sc::stage_host_L(p->P, L_values_host, stream, dptrs, err);
+  if (st == SC_OK) st = sc::launch_assemble(p->P, dptrs.data(), stream, err);
+  return st == SC_OK ? SC_OK : fail(st, err);
+}
+
+sc_status sc_apply(sc_plan_t p, const double* lambda, double* q, void* stream) {
+  if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
+  if ((!lambda || !q) && p->P.n_lambda > 0) return fail(SC_ERR_INVALID_ARG, "NULL lambda or q");
+  std::string err;
+  sc_status st = sc::launch_apply(p->P, lambda, q, stream, err);
+  return st == SC_OK ? SC_OK : fail(st, err);
+}
+
+sc_status sc_check(sc_plan_t p) {
+  if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  if (!p->P.on_device) return SC_OK;
+  std::string err;
+  sc_status st = sc::device_check(p->P, err);
+  return st == SC_OK ? SC_OK : fail(st, err);
+}
+
+sc_status sc_get_F(sc_plan_t p, int32_t i, double* F, int64_t ld) {
+  if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
+  if (i < 0 || i >= p->P.nsub) return fail(SC_ERR_INVALID_ARG, "subdomain index out of range");
+  const sc::ClassPlan& C = p->P.classes[(size_t)p->P.sub_cls[(size_t)i]];
+  const int64_t m = C.m;
+  if (m == 0) return SC_OK;
+  if (!F || ld < m) return fail(SC_ERR_INVALID_ARG, "NULL F or ld < m");
+  std::string err;
+  std::vector<double> Fl;
+  sc_status st = sc::copy_F_lower(p->P, i, Fl, err);
+  if (st != SC_OK) return fail(st, err);
+  // F(sigma(a), sigma(b)) = F'(max(a,b), min(a,b))  (permute back; symmetrise)
+  for (int64_t b = 0; b < m; b++)
+    for (int64_t a = 0; a < m; a++) {
+      const int64_t hi = std::max(a, b), lo = std::min(a, b);
+      F[(int64_t)C.sigma[(size_t)b] * ld + C.sigma[(size_t)a]] = Fl[(size_t)(lo * m + hi)];
+    }
+  return SC_OK;
+}
+
+sc_status sc_get_X(sc_plan_t p, int32_t i, double* X, int32_t* sigma) {
+  if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  if (i < 0 || i >= p->P.nsub) return fail(SC_ERR_INVALID_ARG, "subdomain index out of range");
+  const sc::ClassPlan& C = p->P.classes[(size_t)p->P.sub_cls[(size_t)i]];
+  if (sigma) std::copy(C.sigma.begin(), C.sigma.end(), sigma);
+  if (!X) return SC_OK;
+  if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
+  std::string err;
+  std::vector<double> strips;
+  sc_status st = sc::copy_X_strips(p->P, i, strips, err);
+  if (st != SC_OK) return fail(st, err);
+  const int64_t n = C.n, T = p->P.T;
+  std::fill(X, X + n * (int64_t)C.m, 0.0);
+  for (const sc::Tile& t : C.tiles) {
+    for (int32_t q = t.reach_begin; q < t.reach_end; q++) {
+      // reach indices were globalised in build_plan: map back to the class-local array
+      const sc::Reach& R = C.reach[(size_t)(q - C.tiles[0].reach_begin)];
+      for (int32_t r = R.e; r < R.c1; r++)
+        for (int32_t j = 0; j < t.width; j++)
+          X[(int64_t)(t.col0 + j) * n + r] = strips[(size_t)(t.x_off + (int64_t)(R.off + r - R.e) * T + j)];
+    }
+  }
+  return SC_OK;
+}
+
+sc_status sc_plan_strip_rows(sc_plan_t p, int32_t i, int32_t a, int32_t* rows, int32_t* nrows) {
+  if (!p || !rows || !nrows) return fail(SC_ERR_INVALID_ARG, "NULL argument");
+  if (i < 0 || i >= p->P.nsub) return fail(SC_ERR_INVALID_ARG, "subdomain index out of range");
+  const sc::ClassPlan& C = p->P.classes[(size_t)p->P.sub_cls[(size_t)i]];
+  if (a < 0 || a >= C.m) return fail(SC_ERR_INVALID_ARG, "column out of range");
+  const sc::Tile& t = C.tiles[(size_t)(a / p->P.T)];
+  int32_t k = 0;
+  for (int32_t q = t.reach_begin; q < t.reach_end; q++) {
+    const sc::Reach& R = C.reach[(size_t)(q - C.tiles[0].reach_begin)];
+    for (int32_t r = R.e; r < R.c1; r++) rows[k++] = r;
+  }
+  *nrows = k;
+  return SC_OK;
+}
+
+sc_status sc_plan_stats(sc_plan_t p, sc_stats* out) {
+  if (!p || !out) return fail(SC_ERR_INVALID_ARG, "NULL argument");
+  *out = p->P.stats;
+  return SC_OK;
+}
+
+sc_status sc_set_timing_events(sc_plan_t p, void* ev0, void* ev1, void* ev2) {
+  if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  p->P.tev[0] = ev0;
+  p->P.tev[1] = ev1;
+  p->P.tev[2] = ev2;
+  return SC_OK;
+}
+
+int32_t sc_launches_per_assemble(sc_plan_t p) {
+  if (!p) return 0;
+  return (p->P.trsm_tasks.empty() ? 0 : 1) + (p->P.syrk_tasks.empty() ? 0 : 1);
+}
+
+int32_t sc_launches_per_apply(sc_plan_t p) {
+  if (!p) return 0;
+  return (p->P.apply_tasks.empty() ? 0 : 1) + (p->P.n_lambda > 0 ? 1 : 0);
+}
+
+void sc_plan_destroy(sc_plan_t p) {
+  if (!p) return;
+  sc::free_plan_device(p->P);
+  delete p;
+}
+
+const char* sc_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,243 @@
+"""Thin Python binding of the C ABI in include/sc_b200.h (argument marshalling only).
+
+Every step of the hot path runs in libsc_b200.so (sm_100a kernels); this module only converts numpy
+arrays / torch tensors into the pointers and sizes the ABI takes.  There is no CPU fallback: if the
+library is missing or a call fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsc_b200.so")
+
+SC_OK, SC_ERR_INVALID_ARG, SC_ERR_PATTERN, SC_ERR_ZERO_PIVOT, SC_ERR_OOM, SC_ERR_CUDA, SC_ERR_STATE = range(7)
+SKIP_NONE, SKIP_ENVELOPE, SKIP_EXACT = 0, 1, 2
+_STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARG", 2: "SC_ERR_PATTERN", 3: "SC_ERR_ZERO_PIVOT", 4: "SC_ERR_OOM",
+           5: "SC_ERR_CUDA", 6: "SC_ERR_STATE"}
+
+_P = ctypes.c_void_p
+
+
+class ScError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class SubdomainDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("m", ctypes.c_int32), ("L_colptr", _P), ("L_rowidx", _P), ("perm", _P),
+                ("Bt_colptr", _P), ("Bt_rowidx", _P), ("Bt_values", _P), ("lambda_map", _P)]
+
+
+class Options(ctypes.Structure):
+    _fields_ = [("precision", ctypes.c_int32), ("skip", ctypes.c_int32), ("tile_cols", ctypes.c_int32),
+                ("panel_cols", ctypes.c_int32), ("n_lambda_global", ctypes.c_int64), ("device", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 7)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_int32) for k in ("nsub", "n_classes", "tile_cols", "panel_cols")] + \
+               [(k, ctypes.c_int64) for k in ("sum_n", "sum_m", "max_m", "sum_nnz_L", "trsm_tasks", "trsm_steps",
+                                              "syrk_tasks", "syrk_segments")] + \
+               [(k, ctypes.c_double) for k in ("flops_trsm_useful", "flops_syrk_useful", "flops_trsm_envelope",
+                                               "flops_syrk_envelope", "flops_trsm_dense", "flops_syrk_dense",
+                                               "flops_trsm_sparse_orig", "flops_trsm_executed",
+                                               "flops_syrk_executed", "bytes_L_values", "bytes_F_lower", "bytes_X",
+                                               "device_bytes", "bytes_apply")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_lib = None
+
+EXPORTS = ["sc_options_default", "sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply",
+           "sc_check", "sc_get_F", "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_set_timing_events", "sc_launches_per_assemble",
+           "sc_launches_per_apply", "sc_plan_destroy", "sc_last_error"]
+
+
+def lib():
+    """Load libsc_b200.so (raises if it was not built: no fallback path exists)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    L.sc_options_default.argtypes = [ctypes.POINTER(Options)]
+    L.sc_options_default.restype = None
+    L.sc_plan_create.argtypes = [ctypes.POINTER(SubdomainDesc), ctypes.c_int32, ctypes.POINTER(Options), ctypes.POINTER(_P)]
+    L.sc_assemble_batch.argtypes = [_P, ctypes.POINTER(_P), _P]
+    L.sc_assemble_batch_host.argtypes = [_P, ctypes.POINTER(_P), _P]
+    L.sc_apply.argtypes = [_P, _P, _P, _P]
+    L.sc_check.argtypes = [_P]
+    L.sc_get_F.argtypes = [_P, ctypes.c_int32, _P, ctypes.c_int64]
+    L.sc_get_X.argtypes = [_P, ctypes.c_int32, _P, _P]
+    L.sc_plan_strip_rows.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _P, _P]
+    L.sc_plan_stats.argtypes = [_P, ctypes.POINTER(Stats)]
+    L.sc_set_timing_events.argtypes = [_P, _P, _P, _P]
+    L.sc_launches_per_assemble.argtypes = [_P]
+    L.sc_launches_per_assemble.restype = ctypes.c_int32
+    L.sc_launches_per_apply.argtypes = [_P]
+    L.sc_launches_per_apply.restype = ctypes.c_int32
+    L.sc_plan_destroy.argtypes = [_P]
+    L.sc_plan_destroy.restype = None
+    L.sc_last_error.argtypes = []
+    L.sc_last_error.restype = ctypes.c_char_p
+    for f in ("sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply", "sc_check", "sc_get_F",
+              "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_set_timing_events"):
+        getattr(L, f).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status != SC_OK:
+        raise ScError(status, lib().sc_last_error().decode())
+
+
+def _ptr(a: Optional[np.ndarray]):
+    return None if a is None else a.ctypes.data
+
+
+def _stream_handle(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+class SCPlan:
+    """sc_plan_create + the three stages.  `subdomains`: objects with n, m, L_colptr, L_rowidx, perm,
+    Bt_colptr, Bt_rowidx, Bt_values, lambda_map (numpy arrays, e.g. synth.Subdomain)."""
+
+    def __init__(self, subdomains: Sequence, *, n_lambda: int = 0, skip: int = SKIP_EXACT, tile_cols: int = 0,
+                 panel_cols: int = 0, device: int = 0):
+        L = lib()
+        keep: List[np.ndarray] = []
+
+        def arr(x, dt):
+            if x is None:
+                return None
+            a = np.ascontiguousarray(x, dtype=dt)
+            keep.append(a)
+            return a
+
+        descs = (SubdomainDesc * max(len(subdomains), 1))()
+        self.n = []
+        self.m = []
+        self.nnz = []
+        for i, sd in enumerate(subdomains):
+            d = descs[i]
+            d.n, d.m = int(sd.n), int(sd.m)
+            d.L_colptr = _ptr(arr(sd.L_colptr, np.int64))
+            d.L_rowidx = _ptr(arr(sd.L_rowidx, np.int32))
+            d.perm = _ptr(arr(getattr(sd, "perm", None), np.int32))
+            d.Bt_colptr = _ptr(arr(sd.Bt_colptr, np.int32))
+            d.Bt_rowidx = _ptr(arr(sd.Bt_rowidx, np.int32))
+            d.Bt_values = _ptr(arr(sd.Bt_values, np.float64))
+            d.lambda_map = _ptr(arr(getattr(sd, "lambda_map", None), np.int64))
+            self.n.append(d.n)
+            self.m.append(d.m)
+            self.nnz.append(int(sd.L_colptr[-1]))
+        opt = Options()
+        L.sc_options_default(ctypes.byref(opt))
+        opt.skip, opt.tile_cols, opt.panel_cols = skip, tile_cols, panel_cols
+        opt.n_lambda_global, opt.device = int(n_lambda), int(device)
+        self.device = device
+        self.n_lambda = int(n_lambda)
+        h = _P()
+        _check(L.sc_plan_create(descs, len(subdomains), ctypes.byref(opt), ctypes.byref(h)))
+        self._h = h
+        self.nsub = len(subdomains)
+
+    # -- preprocessing
+    def assemble(self, L_values: Sequence, stream=None):
+        """L_values: per subdomain a CUDA float64 tensor (or raw device pointer int) of nnz(L) values."""
+        ptrs = (_P * max(self.nsub, 1))()
+        for i, t in enumerate(L_values):
+            ptrs[i] = t if isinstance(t, int) else t.data_ptr()
+        _check(lib().sc_assemble_batch(self._h, ptrs, _stream_handle(stream)))
+
+    def assemble_host(self, L_values: Sequence[np.ndarray], stream=None):
+        """L values in host memory (pinned torch tensors or numpy arrays); copied H2D inside the call."""
+        ptrs = (_P * max(self.nsub, 1))()
+        for i, t in enumerate(L_values):
+            ptrs[i] = t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+        _check(lib().sc_assemble_batch_host(self._h, ptrs, _stream_handle(stream)))
+
+    # -- solution
+    def apply(self, lam, q, stream=None):
+        """q <- sum_i scatter(F_i gather(lam)) over this plan's subdomains (device tensors, float64)."""
+        _check(lib().sc_apply(self._h, lam.data_ptr(), q.data_ptr(), _stream_handle(stream)))
+
+    def apply_global(self, lam, q, group=None, stream=None):
+        """sc_apply then all-reduce(sum) of q over the ranks of `group` (NCCL over NVLink)."""
+        import torch.distributed as dist
+        self.apply(lam, q, stream)
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            dist.all_reduce(q, op=dist.ReduceOp.SUM, group=group)
+
+    # -- queries
+    def check(self):
+        _check(lib().sc_check(self._h))
+
+    def get_F(self, i: int) -> np.ndarray:
+        m = self.m[i]
+        F = np.zeros((m, m), dtype=np.float64, order="F")
+        _check(lib().sc_get_F(self._h, i, F.ctypes.data, m))
+        return np.asfortranarray(F)
+
+    def get_X(self, i: int):
+        n, m = self.n[i], self.m[i]
+        X = np.zeros((n, m), dtype=np.float64, order="F")
+        sigma = np.zeros(max(m, 1), dtype=np.int32)
+        _check(lib().sc_get_X(self._h, i, X.ctypes.data, sigma.ctypes.data))
+        return X, sigma[:m]
+
+    def sigma(self, i: int) -> np.ndarray:
+        sigma = np.zeros(max(self.m[i], 1), dtype=np.int32)
+        _check(lib().sc_get_X(self._h, i, None, sigma.ctypes.data))
+        return sigma[:self.m[i]]
+
+    def strip_rows(self, i: int, a: int) -> np.ndarray:
+        rows = np.zeros(max(self.n[i], 1), dtype=np.int32)
+        k = ctypes.c_int32(0)
+        _check(lib().sc_plan_strip_rows(self._h, i, a, rows.ctypes.data, ctypes.addressof(k)))
+        return rows[:k.value]
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib().sc_plan_stats(self._h, ctypes.byref(s)))
+        return s.as_dict()
+
+    def set_timing_events(self, ev0=None, ev1=None, ev2=None):
+        """torch.cuda.Event objects recorded around the TRSM and SYRK kernels of each assemble."""
+        h = [None if e is None else e.cuda_event for e in (ev0, ev1, ev2)]
+        _check(lib().sc_set_timing_events(self._h, *h))
+
+    @property
+    def launches_per_assemble(self) -> int:
+        return lib().sc_launches_per_assemble(self._h)
+
+    @property
+    def launches_per_apply(self) -> int:
+        return lib().sc_launches_per_apply(self._h)
+
+    def destroy(self):
+        if getattr(self, "_h", None):
+            lib().sc_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
