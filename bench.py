@@ -205,6 +205,9 @@ def main():
 
     # timed region: K steps, per-kernel events recorded inside sc_assemble_batch on `stream`
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for row in evs:  # torch creates the CUDA event lazily on first record
+        for e in row:
+            e.record(stream)
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()

@@ -14,6 +14,7 @@ from paper_2509_21037_b200 import SCPlan, ScError, SKIP_ENVELOPE, SKIP_EXACT, SK
 from paper_2509_21037_b200 import sc as scmod
 from synth import config_problem, make_problem
 from synth.mesh import Subdomain, custom_problem
+from helpers import copy_sd as _copy_sd
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -139,12 +140,6 @@ def test_pattern_classes_dedup():
     assert s["n_classes"] == 9  # 3 x 3 boundary classes of a 4x4 decomposition
 
 
-def _copy_sd(sd, **over):
-    d = dict(n=sd.n, m=sd.m, L_colptr=sd.L_colptr.copy(), L_rowidx=sd.L_rowidx.copy(), perm=sd.perm.copy(),
-             Bt_colptr=sd.Bt_colptr.copy(), Bt_rowidx=sd.Bt_rowidx.copy(), Bt_values=sd.Bt_values.copy(),
-             lambda_map=sd.lambda_map.copy())
-    d.update(over)
-    return type("SD", (), d)
 
 
 def test_invalid_inputs_rejected():
