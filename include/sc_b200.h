@@ -77,7 +77,8 @@ enum { SC_SKIP_NONE = 0,      /* no B~ sparsity: every column solved from row 0 
 typedef struct {
   int32_t precision;         /* 64 (FP64).  Other values -> SC_ERR_INVALID_ARG in this version     */
   int32_t skip;              /* SC_SKIP_*                                                          */
-  int32_t tile_cols;         /* T: RHS column-tile width, 16, 32 or 64; 0 = automatic              */
+  int32_t tile_cols;         /* T: RHS column-tile width 8, 16, 32 or 64; 0 = automatic (widest whose
+                                X strip fits in shared memory)                                      */
   int32_t panel_cols;        /* max factor panel width (factor-splitting block), <= 64; 0 = 64      */
   int64_t n_lambda_global;   /* length of the global dual vector used by sc_apply                   */
   int32_t device;            /* CUDA device ordinal; -1 = host-only plan (symbolic + stats only)    */
@@ -102,6 +103,9 @@ typedef struct {
   double bytes_X;            /* X workspace (tile-exact strips)                                    */
   double device_bytes;       /* everything the plan allocated on the device                        */
   double bytes_apply;        /* algorithmic bytes of one sc_apply (F lower read once + vectors)    */
+  double bytes_panels;       /* panel buffers (inverted diagonal blocks + pruned row chunks)        */
+  int64_t panels;            /* factor panels, summed over subdomains                               */
+  int32_t group_cols, pad0;  /* SYRK output tile width G                                            */
 } sc_stats;
 
 /* Fill `opt` with defaults: precision 64, skip EXACT, tile/panel auto, device 0. */
@@ -148,6 +152,10 @@ sc_status sc_get_X(sc_plan_t p, int32_t i, double* X, int32_t* sigma);
 sc_status sc_plan_strip_rows(sc_plan_t p, int32_t i, int32_t a, int32_t* rows, int32_t* nrows);
 
 sc_status sc_plan_stats(sc_plan_t p, sc_stats* out);
+
+/* Per-subdomain cost estimate (executed FP64 flops of prep + TRSM + SYRK) into costs[0..nsub), for
+   size-balanced assignment of subdomains to GPUs (works for host-only plans). */
+sc_status sc_plan_subdomain_costs(sc_plan_t p, double* costs);
 
 /* Measurement hook: when set (non-NULL), every following sc_assemble_batch records the three
    cudaEvent_t handles (passed as void*) on its stream: ev0 before the TRSM kernel, ev1 between the

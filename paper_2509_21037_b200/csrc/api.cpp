@@ -130,17 +130,19 @@ sc_status sc_get_X(sc_plan_t p, int32_t i, double* X, int32_t* sigma) {
   std::vector<double> strips;
   sc_status st = sc::copy_X_strips(p->P, i, strips, err);
   if (st != SC_OK) return fail(st, err);
-  const int64_t n = C.n, T = p->P.T;
+  const int64_t n = C.n;
+  const int32_t cls = p->P.sub_cls[(size_t)i];
+  const int32_t panel0 = p->P.cls_panel_begin[(size_t)cls];
+  const int32_t greach0 = C.groups.empty() ? 0 : C.groups[0].reach_begin;  // globalised indices
   std::fill(X, X + n * (int64_t)C.m, 0.0);
-  for (const sc::Tile& t : C.tiles) {
-    for (int32_t q = t.reach_begin; q < t.reach_end; q++) {
-      // reach indices were globalised in build_plan: map back to the class-local array
-      const sc::Reach& R = C.reach[(size_t)(q - C.tiles[0].reach_begin)];
-      for (int32_t r = R.e; r < R.c1; r++)
-        for (int32_t j = 0; j < t.width; j++)
-          X[(int64_t)(t.col0 + j) * n + r] = strips[(size_t)(t.x_off + (int64_t)(R.off + r - R.e) * T + j)];
+  for (const sc::Group& G : C.groups)
+    for (int32_t q = G.reach_begin; q < G.reach_end; q++) {
+      const sc::Reach& R = C.greach[(size_t)(q - greach0)];
+      const sc::Panel& pn = C.panels[(size_t)(R.panel - panel0)];
+      for (int32_t r = 0; r < pn.kw; r++)
+        for (int32_t j = 0; j < G.width; j++)
+          X[(int64_t)(G.col0 + j) * n + pn.a + r] = strips[(size_t)(G.x_off + (int64_t)(R.off + r) * p->P.G + j)];
     }
-  }
   return SC_OK;
 }
 
@@ -149,11 +151,13 @@ sc_status sc_plan_strip_rows(sc_plan_t p, int32_t i, int32_t a, int32_t* rows, i
   if (i < 0 || i >= p->P.nsub) return fail(SC_ERR_INVALID_ARG, "subdomain index out of range");
   const sc::ClassPlan& C = p->P.classes[(size_t)p->P.sub_cls[(size_t)i]];
   if (a < 0 || a >= C.m) return fail(SC_ERR_INVALID_ARG, "column out of range");
+  const int32_t panel0 = p->P.cls_panel_begin[(size_t)p->P.sub_cls[(size_t)i]];
+  const int32_t step0 = C.tiles[0].step_begin;  // globalised indices
   const sc::Tile& t = C.tiles[(size_t)(a / p->P.T)];
   int32_t k = 0;
-  for (int32_t q = t.reach_begin; q < t.reach_end; q++) {
-    const sc::Reach& R = C.reach[(size_t)(q - C.tiles[0].reach_begin)];
-    for (int32_t r = R.e; r < R.c1; r++) rows[k++] = r;
+  for (int32_t s = t.step_begin; s < t.step_end; s++) {
+    const sc::Panel& pn = C.panels[(size_t)(C.steps[(size_t)(s - step0)].panel - panel0)];
+    for (int32_t r = 0; r < pn.kw; r++) rows[k++] = pn.a + r;
   }
   *nrows = k;
   return SC_OK;
@@ -162,6 +166,15 @@ sc_status sc_plan_strip_rows(sc_plan_t p, int32_t i, int32_t a, int32_t* rows, i
 sc_status sc_plan_stats(sc_plan_t p, sc_stats* out) {
   if (!p || !out) return fail(SC_ERR_INVALID_ARG, "NULL argument");
   *out = p->P.stats;
+  return SC_OK;
+}
+
+sc_status sc_plan_subdomain_costs(sc_plan_t p, double* costs) {
+  if (!p || (!costs && p->P.nsub > 0)) return fail(SC_ERR_INVALID_ARG, "NULL argument");
+  for (int32_t i = 0; i < p->P.nsub; i++) {
+    const sc::ClassPlan& C = p->P.classes[(size_t)p->P.sub_cls[(size_t)i]];
+    costs[i] = C.fl_prep_exec + C.fl_trsm_exec + C.fl_syrk_exec;
+  }
   return SC_OK;
 }
 

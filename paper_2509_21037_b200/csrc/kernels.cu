@@ -1,15 +1,23 @@
 // kernels.cu — the device hot path (sm_100a, FP64).
 //
-//   trsm_tile_kernel<T>  "X init + stepped supernodal TRSM" (SURVEY §8 rows a2+a3): one CTA per
-//                        (subdomain, RHS column tile).  Zeroes the tile's X strip, scatters the
-//                        permuted B~^T, then walks the factor panels of the tile's reach
-//                        in order: diagonal-block forward substitution (warp-per-column with shuffle
-//                        broadcasts), then the pruned sub-diagonal update X[R] -= L[R,panel] X[panel]
-//                        as an FP64 DMMA (mma.sync m8n8k4) gather-GEMM-scatter.
-//   syrk_pair_kernel<T>  "block-sparse SYRK" (row a4): one CTA per output tile (I >= J) of F'
-//                        = X^T X, k restricted to rows both strips hold, DMMA tiles.
-//   apply_*              "explicit apply" (row a6): batched symmetric mat-vec on the lower F'
-//                        with the stepped-order gather of lambda and a deterministic scatter-sum.
+//   prep_panel_kernel     one CTA per (subdomain, factor panel): scatters the panel's CSC values of
+//                         L into the panel buffer (dense diagonal block, pruned below-diagonal rows in
+//                         64-row chunks) and replaces the diagonal block by its inverse
+//                         (recursive doubling: 8x8 substitutions + DMMA products), so every tile's
+//                         diagonal solve becomes a tensor-core product.
+//   trsm_smem_kernel<T>   "X init + stepped supernodal TRSM" (SURVEY §8 rows a2+a3): one CTA per
+//                         (subdomain, RHS column tile of T columns).  The tile's X strip (the rows of
+//                         the panels of its reach only) lives in shared memory for the whole solve:
+//                         zero + scatter of the permuted B~^T, then per panel
+//                         Y = inv(L_pp) X_p and X[R_p] -= L[R_p,p] Y as FP64 DMMA (mma.sync m8n8k4)
+//                         tiles.  A dedicated producer warp streams the L blocks with cp.async.bulk
+//                         (TMA bulk copies) into a byte ring guarded by full/empty mbarriers; the
+//                         eight consumer warps synchronise only per panel.  The strip is written out
+//                         once into the G-column group layout the SYRK reads.
+//   syrk_pair_kernel<G>   "block-sparse SYRK" (row a4): one CTA per G x G output tile (I >= J) of
+//                         F' = X^T X, k restricted to rows both group strips hold.
+//   apply_*               "explicit apply" (row a6): batched symmetric mat-vec on the lower F' with
+//                         the stepped-order gather of lambda and a deterministic scatter-sum.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -39,166 +47,376 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// Shared-memory strides (in doubles) chosen == 4 (mod 16) so the fragment loads
-// (4 consecutive k rows x 8 consecutive columns) hit 16 distinct 8-byte bank pairs per phase.
-constexpr int kLdL = kChunk + 4;   // L chunk / triangle, column-major [col][row]
+// ---- mbarrier + bulk async copy (TMA, non-tensor form) ------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+
+// ------------------------------------------------------------------------------------------------
+// prep: panel buffer = [inv(L_pp) | L[R_p, p] chunks]
+// ------------------------------------------------------------------------------------------------
+constexpr int kLdT = kMaxPanel + 4;  // smem triangle, column-major [col][row]
+
+constexpr size_t kPrepSmem = 2 * sizeof(double) * kMaxPanel * kLdT;
+
+__global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
+  extern __shared__ __align__(16) unsigned char prep_smem[];
+  double* D = reinterpret_cast<double*>(prep_smem);  // triangle, then temporaries
+  double* W = D + kMaxPanel * kLdT;                  // inverse
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const I2 task = P.prep_tasks[blockIdx.x];
+  const int sub = task.x;
+  const Panel pn = P.panels[task.y];
+  const int cls = P.sub_cls[sub];
+  const int32_t* __restrict__ dest = P.dest + P.cls_csc_off[cls];
+  const double* __restrict__ Lv = P.Lptr[sub];
+  double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
+  const int kw = pn.kw, kw4 = pn.kw4;
+  int npad = 8;  // triangle padded to npad = 8 * 2^k >= kw with a unit diagonal
+  while (npad < kw) npad *= 2;
+  {
+    double2* D2 = reinterpret_cast<double2*>(D);
+    double2* W2 = reinterpret_cast<double2*>(W);
+    for (int q = tid; q < npad * kLdT / 2; q += kThreads) D2[q] = W2[q] = make_double2(0.0, 0.0);
+  }
+  // zero the chunk region (structural zeros of relaxed panels + padding)
+  {
+    const int64_t c0 = pn.buf_off + (int64_t)pn.ldD * kw4;
+    const int64_t len = (pn.nchunk > 0) ? ((int64_t)(pn.nchunk - 1) * block_ld(kChunk) + pn.ldLast) * kw4 : 0;
+    double2* z = reinterpret_cast<double2*>(PB + c0);
+    for (int64_t q = tid; q < len / 2; q += kThreads) z[q] = make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  for (int64_t q = pn.csc_begin + tid; q < pn.csc_end; q += kThreads) {
+    const double v = Lv[q];
+    const int32_t d = dest[q];
+    if (d < 0) {
+      const int idx = -1 - d;
+      D[(idx >> 6) * kLdT + (idx & 63)] = v;
+    } else {
+      PB[d] = v;
+    }
+  }
+  // unit diagonal in the padding (its inverse stays the identity)
+  for (int i = kw + tid; i < npad; i += kThreads) D[i * kLdT + i] = 1.0;
+  __syncthreads();
+  // inverse of the lower-triangular diagonal block by recursive doubling:
+  //   inv([[A, 0], [C, B]]) = [[inv(A), 0], [-inv(B) C inv(A), inv(B)]]
+  // level 0: 8x8 diagonal blocks by forward substitution (one warp each); levels 16..npad: the
+  // off-diagonal blocks as two DMMA products per pair.  W holds the inverse; D's consumed diagonal
+  // squares serve as the temporary C inv(A).
+  if (warp * 8 < npad && lane < 8) {
+    const int base = warp * 8, j = lane;
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      double s = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < i; k++) s -= (k >= j) ? D[(base + k) * kLdT + base + i] * x[k] : 0.0;
+      const double dii = D[(base + i) * kLdT + base + i];
+      if (base + i < kw && (!(dii > 0.0) || !isfinite(dii)))
+        atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + base + i));
+      x[i] = (i >= j) ? s / dii : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; i++) W[(base + j) * kLdT + base + i] = x[i];
+  }
+  __syncthreads();
+  const int g = lane >> 2, t4 = lane & 3;
+  for (int b = 16; b <= npad; b *= 2) {
+    const int h = b / 2, nbh = h / 8, npairs = npad / b;
+    // T1 = C inv(A) -> D[A rows, A cols] (diagonal square of the pair's top block)
+    for (int blk = warp; blk < npairs * nbh * nbh; blk += kThreads / 32) {
+      const int pr = blk / (nbh * nbh), rem = blk - pr * nbh * nbh, bi = rem % nbh, bj = rem / nbh;
+      const int base = pr * b;
+      const double* Cm = D + base * kLdT + base + h;  // C: rows base+h.., cols base..
+      const double* Ai = W + base * kLdT + base;
+      double c0 = 0.0, c1 = 0.0;
+      for (int k = 0; k < h; k += 4) dmma(c0, c1, Cm[(k + t4) * kLdT + bi * 8 + g], Ai[(bj * 8 + g) * kLdT + k + t4]);
+      double* Tt = D + base * kLdT + base;
+      Tt[(bj * 8 + 2 * t4) * kLdT + bi * 8 + g] = c0;
+      Tt[(bj * 8 + 2 * t4 + 1) * kLdT + bi * 8 + g] = c1;
+    }
+    __syncthreads();
+    // W[B rows, A cols] = -inv(B) T1
+    for (int blk = warp; blk < npairs * nbh * nbh; blk += kThreads / 32) {
+      const int pr = blk / (nbh * nbh), rem = blk - pr * nbh * nbh, bi = rem % nbh, bj = rem / nbh;
+      const int base = pr * b;
+      const double* Bi = W + (base + h) * kLdT + base + h;
+      const double* Tt = D + base * kLdT + base;
+      double c0 = 0.0, c1 = 0.0;
+      for (int k = 0; k < h; k += 4) dmma(c0, c1, Bi[(k + t4) * kLdT + bi * 8 + g], Tt[(bj * 8 + g) * kLdT + k + t4]);
+      double* Wo = W + base * kLdT + base + h;
+      Wo[(bj * 8 + 2 * t4) * kLdT + bi * 8 + g] = -c0;
+      Wo[(bj * 8 + 2 * t4 + 1) * kLdT + bi * 8 + g] = -c1;
+    }
+    __syncthreads();
+  }
+  // write inv(L_pp): ldD x kw4 column-major, zero outside [0,kw) x [0,kw)
+  double* Dinv = PB + pn.buf_off;
+  const int ldD = pn.ldD;
+  for (int q = tid; q < ldD * kw4; q += kThreads) {
+    const int j = q / ldD, i = q - j * ldD;
+    Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * kLdT + i] : 0.0;
+  }
+}
+
+
+// ------------------------------------------------------------------------------------------------
+// TRSM with the X strip resident in shared memory (warp-specialised: 8 DMMA consumer warps + one
+// TMA producer warp streaming the tile's L blocks through a byte ring with full/empty mbarriers)
+// ------------------------------------------------------------------------------------------------
+static_assert(kLdC == block_ld(kChunk), "chunk ld");
 
 template <int T>
 struct TileCfg {
-  static constexpr int LDX = T + 4;            // X rows, row-major [row][col]
-  static constexpr int NB = T / 8;             // 8-wide column blocks in a tile
-  // update GEMM C(64 x T): warps as (8/NWC) x NWC, each WM x WN blocks of 8x8
-  static constexpr int WN = (T == 64) ? 4 : 2;
-  static constexpr int NWC = NB / WN;
-  static constexpr int WM = 8 / (8 / NWC);     // block rows per warp so that all 8 rows covered
+  static constexpr int LDX = T + 4;             // strip row stride (conflict-free fragment loads)
+  static constexpr int NB = T / 8;              // 8-wide column blocks
+  static constexpr int WN = NB < 2 ? NB : 2;    // column blocks per warp
+  static constexpr int NWC = NB / WN;           // warps along the columns
+  static constexpr int WM = NWC;                // row blocks per warp: (8/NWC) warp rows x WM = 8
 };
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void consumer_sync() {  // named barrier over the 8 consumer warps
+  asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads) : "memory");
+}
+
+// Producer (one lane): walks the tile's block stream [inv(L_pp), chunk 0, chunk 1, ...] per step
+// and issues each block with cp.async.bulk into the ring as soon as a slot and the bytes are free.
+__device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, const double* PB, unsigned char* ring,
+                                           uint64_t* full, uint64_t* empty, int32_t* off) {
+  int q_slot[kSlots], q_start[kSlots];  // FIFO of in-flight blocks
+  int q_head = 0, inflight = 0, ring_head = 0, ring_tail = 0;
+  int b = 0;
+  for (int s = tile.step_begin; s < tile.step_end; s++) {
+    const Panel pn = P.panels[P.steps[s].panel];
+    for (int c = -1; c < pn.nchunk; c++, b++) {
+      const double* src;
+      int bytes;
+      if (c < 0) {
+        src = PB + pn.buf_off;
+        bytes = pn.ldD * pn.kw4 * 8;
+      } else {
+        src = PB + pn.buf_off + (int64_t)pn.ldD * pn.kw4 + (int64_t)c * kLdC * pn.kw4;
+        bytes = ((c == pn.nchunk - 1) ? pn.ldLast : kLdC) * pn.kw4 * 8;
+      }
+      // wait until a slot and `bytes` contiguous ring bytes are free (pop oldest in-flight blocks)
+      int start = 0;
+      while (true) {
+        bool ok = false;
+        if (inflight == 0) {
+          ring_head = ring_tail = 0;
+          start = 0;
+          ok = true;
+        } else if (inflight < kSlots) {
+          if (ring_tail > ring_head) {
+            if (kRingBytes - ring_tail >= bytes) {
+              start = ring_tail;
+              ok = true;
+            } else if (ring_head >= bytes) {
+              start = 0;
+              ok = true;
+            }
+          } else if (ring_tail < ring_head && ring_head - ring_tail >= bytes) {
+            start = ring_tail;
+            ok = true;
+          }
+        }
+        if (ok) break;
+        const int os = q_slot[q_head];
+        mbar_wait(&empty[os], (uint32_t)((b - inflight) / kSlots) & 1u);
+        q_head = (q_head + 1) % kSlots;
+        inflight--;
+        ring_head = inflight ? q_start[q_head] : ring_tail;
+      }
+      const int slot = b % kSlots;
+      const int qi = (q_head + inflight) % kSlots;
+      q_slot[qi] = slot;
+      q_start[qi] = start;
+      inflight++;
+      ring_tail = start + bytes;
+      off[slot] = start;
+      mbar_expect_tx(&full[slot], (uint32_t)bytes);
+      bulk_g2s(ring + start, src, (uint32_t)bytes, &full[slot]);
+    }
+  }
+}
+
 template <int T>
-__global__ void __launch_bounds__(kThreads) trsm_tile_kernel(DevPlan P) {
+__global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
   using Cfg = TileCfg<T>;
-  constexpr int LDX = Cfg::LDX;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* Xs = reinterpret_cast<double*>(smem_raw);                 // [kMaxPanel][LDX]
-  double* Ls = Xs + kMaxPanel * LDX;                                // [kMaxPanel][kLdL] triangle
-  double* Lc = Ls + kMaxPanel * kLdL;                               // [kMaxPanel][kLdL] chunk
-  int64_t* colS = reinterpret_cast<int64_t*>(Lc + kMaxPanel * kLdL);  // [kMaxPanel]
-  int32_t* rowsS = reinterpret_cast<int32_t*>(colS + kMaxPanel);      // [kChunk]
-  uint16_t* map = reinterpret_cast<uint16_t*>(rowsS + kChunk);        // [max_n]
+  constexpr int LDX = Cfg::LDX, WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const TrsmSmem L = trsm_smem_layout(T, P.max_n, P.strip_cap);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.full);
+  uint64_t* empty = reinterpret_cast<uint64_t*>(smem_raw + L.empty);
+  int32_t* off = reinterpret_cast<int32_t*>(smem_raw + L.off);
+  unsigned char* ring = smem_raw + L.ring;
+  uint16_t* map = reinterpret_cast<uint16_t*>(smem_raw + L.map);
+  double* Xs = reinterpret_cast<double*>(smem_raw + L.strip);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t4 = lane & 3;
   const I2 task = P.trsm_tasks[blockIdx.x];
   const int sub = task.x;
   const Tile tile = P.tiles[task.y];
-  const int cls = P.sub_cls[sub];
-  const int64_t* __restrict__ colptr = P.colptr + P.cls_colptr_off[cls];
-  const double* __restrict__ Lv = P.Lptr[sub];
-  double* __restrict__ X = P.X + P.sub_X_base[sub] + tile.x_off;
+  const double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
 
-  // ---- X init (row a2): zero the strip, build the row map, scatter B~^T
-  {
-    const int64_t nvec = (int64_t)tile.strip_rows * T / 2;
-    double2* X2 = reinterpret_cast<double2*>(X);
-    for (int64_t q = tid; q < nvec; q += kThreads) X2[q] = make_double2(0.0, 0.0);
-    for (int q = tile.reach_begin + warp; q < tile.reach_end; q += kThreads / 32) {
-      const Reach R = P.reach[q];
-      for (int r = R.e + lane; r < R.c1; r += 32) map[r] = (uint16_t)(R.off + (r - R.e));
+  if (tid == 0) {
+    for (int k = 0; k < kSlots; k++) {
+      mbar_init(&full[k], 1);
+      mbar_init(&empty[k], kThreads / 32);
     }
+    fence_mbar_init();
   }
   __syncthreads();
+  if (warp == kThreads / 32) {  // ---- TMA producer warp
+    if (lane == 0) trsm_producer(P, tile, PB, ring, full, empty, off);
+    return;
+  }
+
+  // ---- consumers.  X init (row a2): zero the strip (+4 pad rows), row map, scatter B~^T
+  const int g = lane >> 2, t4 = lane & 3;
+  const int br0 = (warp / NWC) * WM, bc0 = (warp % NWC) * WN;
+  {
+    double2* X2 = reinterpret_cast<double2*>(Xs);
+    const int nvec = (tile.strip_rows + 4) * LDX / 2;
+    for (int q = tid; q < nvec; q += kThreads) X2[q] = make_double2(0.0, 0.0);
+    uint32_t* m2 = reinterpret_cast<uint32_t*>(map);
+    for (int q = tid; q < (P.max_n + 1) / 2; q += kThreads) m2[q] = 0xFFFFFFFFu;
+  }
+  consumer_sync();
+  for (int s = tile.step_begin + warp; s < tile.step_end; s += kThreads / 32) {
+    const Step st = P.steps[s];
+    const Panel pn = P.panels[st.panel];
+    for (int r = lane; r < pn.kw; r += 32) map[pn.a + r] = (uint16_t)(st.strip_row + r);
+  }
   for (int q = tile.binit_begin + tid; q < tile.binit_end; q += kThreads) {
     const BInit b = P.binit[q];
-    X[(int64_t)b.strip_row * T + b.col] = b.val;
+    Xs[b.strip_row * LDX + b.col] = b.val;
   }
-  __syncthreads();
+  consumer_sync();
 
   // ---- stepped supernodal TRSM (row a3)
-  for (int st = tile.step_begin; st < tile.step_end; st++) {
-    const Step S = P.steps[st];
-    const int kw = S.kw, e = S.e;
-    const int kw4 = (kw + 3) & ~3;
-    if (tid < kw) colS[tid] = colptr[e + tid];
-    __syncthreads();
-    // panel triangle L[e:e+kw, e:e+kw] -> Ls (column-major, zero outside the lower triangle)
-    for (int q = tid; q < kMaxPanel * kMaxPanel; q += kThreads) {
-      const int c = q >> 6, r = q & 63;
-      double v = 0.0;
-      if (c < kw && r < kw && r >= c) v = Lv[colS[c] + (r - c)];
-      Ls[c * kLdL + r] = v;
-    }
-    // panel rows of X -> Xs (rows kw..kw4 zero for the k padding of the update GEMM)
-    for (int q = tid; q < kw4 * T; q += kThreads) {
-      const int r = q / T, j = q - r * T;
-      Xs[r * LDX + j] = (r < kw) ? X[(int64_t)(S.strip_row + r) * T + j] : 0.0;
-    }
-    __syncthreads();
-    // diagonal block: forward substitution, warp w owns columns j = w + 8q, lanes own rows
+  int b = 0;  // block counter (same order as the producer)
+  for (int s = tile.step_begin; s < tile.step_end; s++, b++) {
+    const Step st = P.steps[s];
+    const Panel pn = P.panels[st.panel];
+    const int kw = pn.kw, kw4 = pn.kw4;
+    double* Xp = Xs + st.strip_row * LDX;
+    double acc[WM][WN][2];
+    // Y = inv(L_pp) X_p  (inv(L_pp) lower triangular: row block i needs k < 8 (i + 1))
     {
-      constexpr int CPW = T / 8;
-      double x0[CPW], x1[CPW];
+      const int slot = b % kSlots;
+      mbar_wait(&full[slot], (uint32_t)(b / kSlots) & 1u);
+      const double* A = reinterpret_cast<const double*>(ring + off[slot]);
+      const int ld = pn.ldD;
 #pragma unroll
-      for (int q = 0; q < CPW; q++) {
-        const int j = warp + 8 * q;
-        x0[q] = (lane < kw) ? Xs[lane * LDX + j] : 0.0;
-        x1[q] = (lane + 32 < kw) ? Xs[(lane + 32) * LDX + j] : 0.0;
-      }
-      for (int c = 0; c < kw; c++) {
-        const double d = Ls[c * kLdL + c];
-        if (!(d > 0.0) || !isfinite(d)) {
-          if (tid == 0 && warp == 0)
-            atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(e + c));
-        }
-        const double rcp = 1.0 / d;
-        const double l0 = (lane > c) ? Ls[c * kLdL + lane] : 0.0;
-        const double l1 = (lane + 32 > c) ? Ls[c * kLdL + lane + 32] : 0.0;
+      for (int i = 0; i < WM; i++)
 #pragma unroll
-        for (int q = 0; q < CPW; q++) {
-          const double xc = __shfl_sync(0xffffffffu, (c < 32) ? x0[q] : x1[q], c & 31) * rcp;
-          if (c < 32) {
-            if (lane == c) x0[q] = xc;
-          } else {
-            if (lane == c - 32) x1[q] = xc;
-          }
-          x0[q] = fma(-l0, xc, x0[q]);
-          x1[q] = fma(-l1, xc, x1[q]);
+        for (int j = 0; j < WN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+      const int kend = min(kw4, (br0 + WM) * 8);
+      if (br0 * 8 < kw4) {
+        for (int k = 0; k < kend; k += 4) {
+          double a[WM], bb[WN];
+#pragma unroll
+          for (int i = 0; i < WM; i++) a[i] = A[(k + t4) * ld + (br0 + i) * 8 + g];
+#pragma unroll
+          for (int j = 0; j < WN; j++) bb[j] = Xp[(k + t4) * LDX + (bc0 + j) * 8 + g];
+#pragma unroll
+          for (int i = 0; i < WM; i++)
+#pragma unroll
+            for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
         }
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      consumer_sync();  // every warp has read X_p
 #pragma unroll
-      for (int q = 0; q < CPW; q++) {
-        const int j = warp + 8 * q;
-        if (lane < kw) Xs[lane * LDX + j] = x0[q];
-        if (lane + 32 < kw) Xs[(lane + 32) * LDX + j] = x1[q];
+      for (int i = 0; i < WM; i++) {
+        const int r = (br0 + i) * 8 + g;
+        if (r < kw) {
+#pragma unroll
+          for (int j = 0; j < WN; j++)
+            *reinterpret_cast<double2*>(Xp + r * LDX + (bc0 + j) * 8 + 2 * t4) =
+                make_double2(acc[i][j][0], acc[i][j][1]);
+        }
       }
+      consumer_sync();  // Y visible
     }
-    __syncthreads();
-    // solved panel rows are final: store them
-    for (int q = tid; q < kw * T; q += kThreads) {
-      const int r = q / T, j = q - r * T;
-      X[(int64_t)(S.strip_row + r) * T + j] = Xs[r * LDX + j];
-    }
-    // pruned sub-diagonal update, chunks of 64 rows: rows [e+kw, c1) of the supernode, then R_s
-    const int nin = S.c1 - e - kw;
-    const int M = nin + S.nR;
-    for (int m0 = 0; m0 < M; m0 += kChunk) {
-      if (tid < kChunk) {
-        const int k = m0 + tid;
-        int row = -1;
-        if (k < M) row = (k < nin) ? (S.strip_row + kw + k) : (int)map[P.Rrows[S.R_off + (k - nin)]];
-        rowsS[tid] = row;
+    // X[R_p] -= L[R_p, p] Y, one 64-row chunk (one ring block) at a time; no CTA barrier between
+    // chunks: chunks update disjoint rows and each warp releases its ring slot itself
+    for (int c = 0; c < pn.nchunk; c++) {
+      b++;
+      const int rows_c = min(kChunk, pn.nR - c * kChunk);
+      const int ld = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
+      int srow[WM];
+#pragma unroll
+      for (int i = 0; i < WM; i++) {
+        const int r = (br0 + i) * 8 + g;
+        srow[i] = (r < rows_c) ? (int)map[P.Rrows[pn.R_off + c * kChunk + r]] : 0xFFFF;
       }
-      for (int q = tid; q < kw4 * kChunk; q += kThreads) {
-        const int c = q >> 6, k = q & 63;
-        double v = 0.0;
-        if (c < kw && m0 + k < M) v = Lv[colS[c] + (kw - c) + m0 + k];
-        Lc[c * kLdL + k] = v;
-      }
-      __syncthreads();
-      {
-        constexpr int WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC;
-        const int br0 = (warp / NWC) * WM, bc0 = (warp % NWC) * WN;
-        double acc[WM][WN][2];
+      const int slot = b % kSlots;
+      mbar_wait(&full[slot], (uint32_t)(b / kSlots) & 1u);
+      const double* A = reinterpret_cast<const double*>(ring + off[slot]);
+      if (br0 * 8 < rows_c) {
 #pragma unroll
         for (int i = 0; i < WM; i++)
 #pragma unroll
           for (int j = 0; j < WN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
         for (int k = 0; k < kw4; k += 4) {
-          double a[WM], b[WN];
+          double a[WM], bb[WN];
 #pragma unroll
-          for (int i = 0; i < WM; i++) a[i] = Lc[(k + t4) * kLdL + (br0 + i) * 8 + g];
+          for (int i = 0; i < WM; i++) a[i] = A[(k + t4) * ld + (br0 + i) * 8 + g];
 #pragma unroll
-          for (int j = 0; j < WN; j++) b[j] = Xs[(k + t4) * LDX + (bc0 + j) * 8 + g];
+          for (int j = 0; j < WN; j++) bb[j] = Xp[(k + t4) * LDX + (bc0 + j) * 8 + g];
 #pragma unroll
           for (int i = 0; i < WM; i++)
 #pragma unroll
-            for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+            for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
         }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (br0 * 8 < rows_c) {
 #pragma unroll
         for (int i = 0; i < WM; i++) {
-          const int row = rowsS[(br0 + i) * 8 + g];
-          if (row < 0) continue;
+          if (srow[i] == 0xFFFF) continue;  // row outside this tile's reach: its update is exactly 0
 #pragma unroll
           for (int j = 0; j < WN; j++) {
-            double2* p = reinterpret_cast<double2*>(X + (int64_t)row * T + (bc0 + j) * 8 + 2 * t4);
+            double2* p = reinterpret_cast<double2*>(Xs + srow[i] * LDX + (bc0 + j) * 8 + 2 * t4);
             double2 v = *p;
             v.x -= acc[i][j][0];
             v.y -= acc[i][j][1];
@@ -206,42 +424,54 @@ __global__ void __launch_bounds__(kThreads) trsm_tile_kernel(DevPlan P) {
           }
         }
       }
-      __syncthreads();
+    }
+    consumer_sync();  // updates visible before the next panel reads its rows
+  }
+
+  // ---- write the strip into the group strip (row-major, G columns) for the SYRK
+  const Group G = P.groups[tile.group];
+  double* __restrict__ Xg = P.X + P.sub_X_base[sub] + G.x_off + tile.col_in_group;
+  for (int w = tile.wseg_begin; w < tile.wseg_end; w++) {
+    const WSeg ws = P.wsegs[w];
+    for (int q = tid; q < ws.len * (T / 2); q += kThreads) {
+      const int r = q / (T / 2), j = 2 * (q - r * (T / 2));
+      double2 v = make_double2(0.0, 0.0);
+      if (ws.src >= 0) v = *reinterpret_cast<const double2*>(Xs + (ws.src + r) * LDX + j);
+      *reinterpret_cast<double2*>(Xg + (int64_t)(ws.dst + r) * P.G + j) = v;
     }
   }
 }
 
-// ------------------------------------------------------------------------------------------------
-// SYRK: F'[I,J] = sum_seg X_I[seg]^T X_J[seg]  (T x T output tile, lower part of F' only)
-// ------------------------------------------------------------------------------------------------
-template <int T>
-struct SyrkCfg {
-  static constexpr int LDX = T + 4;
-  static constexpr int NB = T / 8;                       // block rows/cols of the output tile
-  static constexpr int NBLK = NB * NB;                   // 8x8 output blocks
-  static constexpr int PER_WARP = (NBLK + 7) / 8;        // blocks per warp (T=16: 1 with 4 idle warps)
-  static constexpr int WN = (T == 64) ? 4 : (T == 32 ? 2 : 1);
-  static constexpr int WM = PER_WARP / WN;
-  static constexpr int NWC = NB / WN;
-};
-constexpr int kKC = 32;  // k rows staged per chunk
 
-template <int T>
+// ------------------------------------------------------------------------------------------------
+// SYRK over G-column groups: F'[I,J] = sum_seg X_I[seg]^T X_J[seg] (lower part of F' only)
+// ------------------------------------------------------------------------------------------------
+constexpr int kKC = 32;       // k rows staged per chunk
+
+template <int G>
+struct SyrkCfg {              // (G/8)^2 output blocks of 8x8 over 8 warps
+  static constexpr int NB = G / 8;
+  static constexpr int WN = (G == 64) ? 4 : (G == 32 ? 2 : 1);
+  static constexpr int WM = (G == 64) ? 2 : 1;
+  static constexpr int NWC = NB / WN;
+  static constexpr int ACTIVE = (NB / WM) * NWC;   // warps with work (4 for G = 16)
+};
+
+template <int G>
 __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P) {
-  using Cfg = SyrkCfg<T>;
-  constexpr int LDX = Cfg::LDX;
-  __shared__ __align__(16) double As[kKC * LDX];
-  __shared__ __align__(16) double Bs[kKC * LDX];
+  constexpr int kLdG = G + 4, kGroup = G;
+  __shared__ __align__(16) double As[kKC * kLdG];
+  __shared__ __align__(16) double Bs[kKC * kLdG];
+  constexpr int WM = SyrkCfg<G>::WM, WN = SyrkCfg<G>::WN, NWC = SyrkCfg<G>::NWC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool active = warp < SyrkCfg<G>::ACTIVE;
   const int g = lane >> 2, t4 = lane & 3;
   const I2 task = P.syrk_tasks[blockIdx.x];
   const int sub = task.x;
   const Pair pr = P.pairs[task.y];
-  const Tile tI = P.tiles[pr.I], tJ = P.tiles[pr.J];
-  const double* __restrict__ XI = P.X + P.sub_X_base[sub] + tI.x_off;
-  const double* __restrict__ XJ = P.X + P.sub_X_base[sub] + tJ.x_off;
-  constexpr int WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC;
-  const bool active = warp < (Cfg::NB / WM) * NWC;
+  const Group gI = P.groups[pr.I], gJ = P.groups[pr.J];
+  const double* __restrict__ XI = P.X + P.sub_X_base[sub] + gI.x_off;
+  const double* __restrict__ XJ = P.X + P.sub_X_base[sub] + gJ.x_off;
   const int br0 = (warp / NWC) * WM, bc0 = (warp % NWC) * WN;
   double acc[WM][WN][2];
 #pragma unroll
@@ -253,20 +483,25 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P) {
     const Seg s = P.segs[sg];
     for (int k0 = 0; k0 < s.len; k0 += kKC) {
       const int kn = min(kKC, s.len - k0);
-      for (int q = tid; q < kKC * T; q += kThreads) {
-        const int r = q / T, j = q - r * T;
-        As[r * LDX + j] = (r < kn) ? XI[(int64_t)(s.offI + k0 + r) * T + j] : 0.0;
-        Bs[r * LDX + j] = (r < kn) ? XJ[(int64_t)(s.offJ + k0 + r) * T + j] : 0.0;
+      for (int q = tid; q < kKC * (kGroup / 2); q += kThreads) {
+        const int r = q / (kGroup / 2), j = 2 * (q - r * (kGroup / 2));
+        double2 va = make_double2(0.0, 0.0), vb = make_double2(0.0, 0.0);
+        if (r < kn) {
+          va = *reinterpret_cast<const double2*>(XI + (int64_t)(s.offI + k0 + r) * kGroup + j);
+          vb = *reinterpret_cast<const double2*>(XJ + (int64_t)(s.offJ + k0 + r) * kGroup + j);
+        }
+        *reinterpret_cast<double2*>(As + r * kLdG + j) = va;
+        *reinterpret_cast<double2*>(Bs + r * kLdG + j) = vb;
       }
       __syncthreads();
+      const int kn4 = (kn + 3) & ~3;
       if (active) {
-        const int kn4 = (kn + 3) & ~3;
         for (int k = 0; k < kn4; k += 4) {
           double a[WM], b[WN];
 #pragma unroll
-          for (int i = 0; i < WM; i++) a[i] = As[(k + t4) * LDX + (br0 + i) * 8 + g];
+          for (int i = 0; i < WM; i++) a[i] = As[(k + t4) * kLdG + (br0 + i) * 8 + g];
 #pragma unroll
-          for (int j = 0; j < WN; j++) b[j] = Bs[(k + t4) * LDX + (bc0 + j) * 8 + g];
+          for (int j = 0; j < WN; j++) b[j] = Bs[(k + t4) * kLdG + (bc0 + j) * 8 + g];
 #pragma unroll
           for (int i = 0; i < WM; i++)
 #pragma unroll
@@ -282,15 +517,15 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P) {
   const bool diag = (pr.I == pr.J);
 #pragma unroll
   for (int i = 0; i < WM; i++) {
-    const int r = (br0 + i) * 8 + g;  // row within tile I
-    if (r >= tI.width) continue;
+    const int r = (br0 + i) * 8 + g;  // row within group I
+    if (r >= gI.width) continue;
 #pragma unroll
     for (int j = 0; j < WN; j++) {
 #pragma unroll
       for (int h = 0; h < 2; h++) {
-        const int c = (bc0 + j) * 8 + 2 * t4 + h;  // column within tile J
-        if (c >= tJ.width || (diag && r < c)) continue;
-        F[(int64_t)(tJ.col0 + c) * m + (tI.col0 + r)] = acc[i][j][h];
+        const int c = (bc0 + j) * 8 + 2 * t4 + h;  // column within group J
+        if (c >= gJ.width || (diag && r < c)) continue;
+        F[(int64_t)(gJ.col0 + c) * m + (gI.col0 + r)] = acc[i][j][h];
       }
     }
   }
@@ -361,6 +596,7 @@ __global__ void __launch_bounds__(kThreads) apply_scatter_kernel(DevPlan P, doub
   q[gidx] = s;
 }
 
+
 // ------------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------------
@@ -388,13 +624,6 @@ sc_status alloc_zero(Plan& P, int64_t count, V** dst, std::string& err) {
   return SC_OK;
 }
 
-size_t trsm_smem_bytes(int T, int max_n) {
-  size_t b = sizeof(double) * (size_t)(kMaxPanel * (T + 4) + 2 * kMaxPanel * kLdL);
-  b += sizeof(int64_t) * kMaxPanel + sizeof(int32_t) * kChunk;
-  b += sizeof(uint16_t) * (size_t)std::max(max_n, 1);
-  return (b + 15) & ~(size_t)15;
-}
-
 #define TRY(x)                   \
   do {                           \
     sc_status s_ = (x);          \
@@ -408,38 +637,49 @@ sc_status upload_plan(Plan& P, std::string& err) {
   DevPlan& D = P.dev;
   std::memset(&D, 0, sizeof(D));
   // concatenate class data
-  std::vector<int64_t> colptr, cls_off;
-  std::vector<int32_t> Rrows;
+  std::vector<Panel> panels;
+  std::vector<int32_t> Rrows, dest;
+  std::vector<int64_t> csc_off;
   std::vector<Tile> tiles;
   std::vector<Step> steps;
-  std::vector<Reach> reach;
+  std::vector<WSeg> wsegs;
+  std::vector<Group> groups;
+  std::vector<Reach> greach;
   std::vector<BInit> binit;
   std::vector<Pair> pairs;
   std::vector<Seg> segs;
   for (auto& C : P.classes) {
-    cls_off.push_back((int64_t)colptr.size());
-    colptr.insert(colptr.end(), C.colptr.begin(), C.colptr.end());
+    csc_off.push_back((int64_t)dest.size());
+    dest.insert(dest.end(), C.dest.begin(), C.dest.end());
+    panels.insert(panels.end(), C.panels.begin(), C.panels.end());
     Rrows.insert(Rrows.end(), C.Rrows.begin(), C.Rrows.end());
     tiles.insert(tiles.end(), C.tiles.begin(), C.tiles.end());
     steps.insert(steps.end(), C.steps.begin(), C.steps.end());
-    reach.insert(reach.end(), C.reach.begin(), C.reach.end());
+    wsegs.insert(wsegs.end(), C.wsegs.begin(), C.wsegs.end());
+    groups.insert(groups.end(), C.groups.begin(), C.groups.end());
+    greach.insert(greach.end(), C.greach.begin(), C.greach.end());
     binit.insert(binit.end(), C.binit.begin(), C.binit.end());
     pairs.insert(pairs.end(), C.pairs.begin(), C.pairs.end());
     segs.insert(segs.end(), C.segs.begin(), C.segs.end());
   }
-  TRY(upload(P, colptr, &D.colptr, err));
-  TRY(upload(P, cls_off, &D.cls_colptr_off, err));
+  TRY(upload(P, panels, &D.panels, err));
   TRY(upload(P, Rrows, &D.Rrows, err));
+  TRY(upload(P, dest, &D.dest, err));
+  TRY(upload(P, csc_off, &D.cls_csc_off, err));
   TRY(upload(P, tiles, &D.tiles, err));
   TRY(upload(P, steps, &D.steps, err));
-  TRY(upload(P, reach, &D.reach, err));
+  TRY(upload(P, wsegs, &D.wsegs, err));
+  TRY(upload(P, groups, &D.groups, err));
+  TRY(upload(P, greach, &D.greach, err));
   TRY(upload(P, binit, &D.binit, err));
   TRY(upload(P, pairs, &D.pairs, err));
   TRY(upload(P, segs, &D.segs, err));
   TRY(upload(P, P.sub_cls, &D.sub_cls, err));
   TRY(upload(P, P.sub_X_base, &D.sub_X_base, err));
   TRY(upload(P, P.sub_F_base, &D.sub_F_base, err));
+  TRY(upload(P, P.sub_PB_base, &D.sub_PB_base, err));
   TRY(upload(P, P.sub_m, &D.sub_m, err));
+  TRY(upload(P, P.prep_tasks, &D.prep_tasks, err));
   TRY(upload(P, P.trsm_tasks, &D.trsm_tasks, err));
   TRY(upload(P, P.syrk_tasks, &D.syrk_tasks, err));
   TRY(upload(P, P.apply_tasks, &D.apply_tasks, err));
@@ -450,6 +690,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, P.qg_sub_a, &D.qg_sub_a, err));
   TRY(alloc_zero(P, P.X_doubles, &D.X, err));
   TRY(alloc_zero(P, P.F_doubles, &D.F, err));
+  TRY(alloc_zero(P, P.PB_doubles, &D.PB, err));
   TRY(alloc_zero(P, P.part_doubles, &D.part, err));
   TRY(alloc_zero(P, 1, &D.err, err));
   double** dl = nullptr;
@@ -464,20 +705,29 @@ sc_status upload_plan(Plan& P, std::string& err) {
   P.lptr_event = ev;
   D.nsub = P.nsub;
   D.max_n = P.max_n;
-  P.smem_trsm = trsm_smem_bytes(P.T, P.max_n);
-  if (P.smem_trsm > 227 * 1024) {
-    err = "TRSM shared memory exceeds 227 KB";
+  D.T = P.T;
+  D.strip_cap = P.max_strip_rows;
+  D.G = P.G;
+  P.smem_trsm = trsm_smem_layout(P.T, P.max_n, P.max_strip_rows).total;
+  int dev_smem = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.opt.device));
+  if (P.smem_trsm > (size_t)dev_smem) {
+    err = "X strip of " + std::to_string(P.max_strip_rows) + " rows x " + std::to_string(P.T) +
+          " columns does not fit in shared memory (" + std::to_string(P.smem_trsm) + " > " + std::to_string(dev_smem) +
+          " bytes); use smaller tile_cols";
     return SC_ERR_INVALID_ARG;
   }
+  CUDA_TRY(cudaFuncSetAttribute(prep_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem));
   switch (P.T) {
-    case 16: CUDA_TRY(cudaFuncSetAttribute(trsm_tile_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
-    case 32: CUDA_TRY(cudaFuncSetAttribute(trsm_tile_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
-    default: CUDA_TRY(cudaFuncSetAttribute(trsm_tile_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
+    case 8: CUDA_TRY(cudaFuncSetAttribute(trsm_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
+    case 16: CUDA_TRY(cudaFuncSetAttribute(trsm_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
+    case 32: CUDA_TRY(cudaFuncSetAttribute(trsm_smem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
+    default: CUDA_TRY(cudaFuncSetAttribute(trsm_smem_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
   }
-  double total = 0;
-  total += 8.0 * (P.X_doubles + P.F_doubles + P.part_doubles);
-  total += colptr.size() * 8.0 + Rrows.size() * 4.0 + tiles.size() * sizeof(Tile) + steps.size() * sizeof(Step) +
-           reach.size() * sizeof(Reach) + binit.size() * sizeof(BInit) + pairs.size() * sizeof(Pair) +
+  double total = 8.0 * (P.X_doubles + P.F_doubles + P.PB_doubles + P.part_doubles);
+  total += dest.size() * 4.0 + Rrows.size() * 4.0 + panels.size() * sizeof(Panel) + tiles.size() * sizeof(Tile) +
+           steps.size() * sizeof(Step) + wsegs.size() * sizeof(WSeg) + groups.size() * sizeof(Group) +
+           greach.size() * sizeof(Reach) + binit.size() * sizeof(BInit) + pairs.size() * sizeof(Pair) +
            segs.size() * sizeof(Seg) + P.slm.size() * 8.0 + P.qg_sub_a.size() * 8.0 + P.qg_ptr.size() * 8.0;
   P.stats.device_bytes = total;
   P.on_device = true;
@@ -517,19 +767,24 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
     P.last_Lptr.assign(Lptr_host, Lptr_host + P.nsub);
   }
   P.last_stream = stream_v;
-  const int ntr = (int)P.trsm_tasks.size(), nsy = (int)P.syrk_tasks.size();
+  const int npr = (int)P.prep_tasks.size(), ntr = (int)P.trsm_tasks.size(), nsy = (int)P.syrk_tasks.size();
   if (P.tev[0]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[0], stream));
+  if (npr > 0) {
+    prep_panel_kernel<<<npr, kThreads, kPrepSmem, stream>>>(P.dev);
+    CUDA_TRY(cudaGetLastError());
+  }
   if (ntr > 0) {
     switch (P.T) {
-      case 16: trsm_tile_kernel<16><<<ntr, kThreads, P.smem_trsm, stream>>>(P.dev); break;
-      case 32: trsm_tile_kernel<32><<<ntr, kThreads, P.smem_trsm, stream>>>(P.dev); break;
-      default: trsm_tile_kernel<64><<<ntr, kThreads, P.smem_trsm, stream>>>(P.dev); break;
+      case 8: trsm_smem_kernel<8><<<ntr, kTrsmThreads, P.smem_trsm, stream>>>(P.dev); break;
+      case 16: trsm_smem_kernel<16><<<ntr, kTrsmThreads, P.smem_trsm, stream>>>(P.dev); break;
+      case 32: trsm_smem_kernel<32><<<ntr, kTrsmThreads, P.smem_trsm, stream>>>(P.dev); break;
+      default: trsm_smem_kernel<64><<<ntr, kTrsmThreads, P.smem_trsm, stream>>>(P.dev); break;
     }
     CUDA_TRY(cudaGetLastError());
   }
   if (P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
   if (nsy > 0) {
-    switch (P.T) {
+    switch (P.G) {
       case 16: syrk_pair_kernel<16><<<nsy, kThreads, 0, stream>>>(P.dev); break;
       case 32: syrk_pair_kernel<32><<<nsy, kThreads, 0, stream>>>(P.dev); break;
       default: syrk_pair_kernel<64><<<nsy, kThreads, 0, stream>>>(P.dev); break;

@@ -4,22 +4,26 @@
 //   1. validate L (lower CSC, diagonal first, rows ascending) and that its pattern is a Cholesky fill
 //      pattern (closed under the elimination tree), B~^T rows, perm;
 //   2. elimination tree parent(j) = first sub-diagonal row of column j, maximal supernodes (chains
-//      j -> j+1 with equal row structure below), their pruned row structures R_s ("extract
-//      only the non-empty rows", CHOLMOD-like);
+//      j -> j+1 with equal row structure below); factor panels of <= 64 columns: wide supernodes
+//      split, runs of small consecutive supernodes merged into one dense panel while it stays mostly
+//      non-zero (relaxed amalgamation); each panel's pruned below-diagonal row set R_p (P:494
+//      "extract only the non-empty rows", CHOLMOD-like) and the CSC -> panel-buffer scatter map;
 //   3. row-permute B~^T by perm, column pivots p_j (first non-zero), stepped order sigma =
 //      stable sort by (p_j, j) (ties: SURVEY §8.3 reading 7);
-//   4. RHS column tiles of width T and, per tile, the rows its X strip must hold:
-//        exact    : elimination-tree reach of the tile's B~^T non-zeros (zeros above the pivots and
-//                   off the etree paths are preserved),
-//        envelope : every row >= the tile's highest (smallest) pivot (the paper's stepped envelope),
-//        none     : every row (the original algorithm);
+//   4. RHS column tiles of width T and, per tile, the panels its X strip must hold:
+//        exact    : panels met by the elimination-tree reach of the tile's B~^T non-zeros (zeros
+//                   above the pivots and off the etree paths are preserved),
+//        envelope : every panel ending below the tile's highest pivot (the paper's stepped envelope),
+//        none     : every panel (the original algorithm);
 //   5. per tile the ordered factor panels ("factor splitting") it must apply;
-//   6. SYRK output tiles I >= J with the row segments both strips hold (output splitting with the
-//      k range restricted to non-zero rows);
+//   6. SYRK column groups of 64 and output tiles I >= J with the row segments both group strips
+//      hold (output splitting with the k range restricted to non-zero rows);
 //   7. work counters and memory layout.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
+#include <iterator>
 #include <numeric>
 #include <unordered_map>
 
@@ -107,19 +111,32 @@ sc_status validate_desc(const sc_subdomain_desc& d, int32_t i, std::string& err)
 }
 
 // Steps 2-7 for one class.
-sc_status analyse_class(const sc_subdomain_desc& d, int T, int PW, int skip, ClassPlan& C, std::string& err) {
+// Relaxation thresholds for merging consecutive small supernodes into one dense panel (the GPU
+// analogue of relaxed supernode amalgamation; zeros are stored explicitly).  Overridable with the
+// environment variables SC_RELAX_ZMAX / SC_RELAX_WSMALL for tuning experiments.
+double relax_zmax() {
+  const char* e = std::getenv("SC_RELAX_ZMAX");
+  return e ? std::atof(e) : 0.5;
+}
+int relax_wsmall() {
+  const char* e = std::getenv("SC_RELAX_WSMALL");
+  return e ? std::atoi(e) : 16;
+}
+
+// Steps 2-7 for one class.
+sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, int skip, ClassPlan& C,
+                        std::string& err) {
   const int32_t n = d.n, m = d.m;
   C.n = n;
   C.m = m;
   C.colptr.assign(d.L_colptr, d.L_colptr + n + 1);
-  C.rowidx.assign(d.L_rowidx, d.L_rowidx + d.L_colptr[n]);
   C.perm.resize((size_t)n);
   for (int32_t k = 0; k < n; k++) C.perm[(size_t)k] = d.perm ? d.perm[k] : k;
   const int64_t* cp = d.L_colptr;
   const int32_t* ri = d.L_rowidx;
   auto cc = [&](int32_t c) { return (int32_t)(cp[c + 1] - cp[c]); };
 
-  // --- 2. etree + closure check + supernodes
+  // --- 2. etree + closure check + maximal supernodes
   std::vector<int32_t> parent((size_t)n, -1);
   for (int32_t c = 0; c < n; c++)
     if (cc(c) > 1) parent[(size_t)c] = ri[cp[c] + 1];
@@ -136,22 +153,124 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int PW, int skip, Cla
                                    " row " + std::to_string(ri[q]) + " not in the structure of its etree parent)");
     }
   }
-  std::vector<int32_t> snode_of((size_t)n);
+  std::vector<int32_t> sn_c0, sn_c1;
   for (int32_t c = 0; c < n;) {
     int32_t c0 = c;
     c++;
     while (c < n && parent[(size_t)(c - 1)] == c && cc(c - 1) == cc(c) + 1) c++;
-    int32_t s = (int32_t)C.sn_c0.size();
-    C.sn_c0.push_back(c0);
-    C.sn_c1.push_back(c);
-    int32_t last = c - 1;
-    int32_t nR = cc(last) - 1;
-    C.sn_nR.push_back(nR);
-    C.sn_Roff.push_back((int32_t)C.Rrows.size());
-    for (int64_t q = cp[last] + 1; q < cp[last + 1]; q++) C.Rrows.push_back(ri[q]);
-    for (int32_t k = c0; k < c; k++) snode_of[(size_t)k] = s;
+    sn_c0.push_back(c0);
+    sn_c1.push_back(c);
   }
-  C.nsup = (int32_t)C.sn_c0.size();
+  C.nsup = (int32_t)sn_c0.size();
+
+  // --- panels: split wide supernodes at PW columns, merge runs of small consecutive supernodes
+  // while the merged dense trapezoid stays mostly non-zero (or tiny)
+  const double zmax = relax_zmax();
+  const int wsmall = relax_wsmall();
+  struct Open {
+    int32_t a = -1, b = -1;
+    std::vector<int32_t> R;
+    double nnz = 0;
+  } open;
+  std::vector<int32_t> panel_of_col((size_t)n, -1);
+  auto close_open = [&]() {
+    if (open.a < 0) return;
+    Panel p{};
+    p.a = open.a;
+    p.kw = open.b - open.a;
+    p.nR = (int32_t)open.R.size();
+    p.R_off = (int32_t)C.Rrows.size();
+    C.Rrows.insert(C.Rrows.end(), open.R.begin(), open.R.end());
+    for (int32_t c = open.a; c < open.b; c++) panel_of_col[(size_t)c] = (int32_t)C.panels.size();
+    C.panels.push_back(p);
+    open = Open();
+  };
+  auto snode_R = [&](int32_t c0, int32_t c1) {  // rows of the supernode's columns below c1
+    std::vector<int32_t> R;
+    int32_t last = c1 - 1;
+    for (int64_t q = cp[last] + 1; q < cp[last + 1]; q++) R.push_back(ri[q]);
+    (void)c0;
+    return R;
+  };
+  for (int32_t s = 0; s < C.nsup; s++) {
+    const int32_t c0 = sn_c0[(size_t)s], c1 = sn_c1[(size_t)s], w = c1 - c0;
+    std::vector<int32_t> Rs = snode_R(c0, c1);
+    double nnz_s = 0;
+    for (int32_t c = c0; c < c1; c++) nnz_s += cc(c);
+    if (w > PW) {
+      close_open();
+      const int32_t np = (w + PW - 1) / PW;
+      for (int32_t k = 0; k < np; k++) {
+        int32_t pa = c0 + (int32_t)((int64_t)w * k / np), pb = c0 + (int32_t)((int64_t)w * (k + 1) / np);
+        open.a = pa;
+        open.b = pb;
+        open.R.clear();
+        for (int32_t r = pb; r < c1; r++) open.R.push_back(r);
+        open.R.insert(open.R.end(), Rs.begin(), Rs.end());
+        close_open();
+      }
+      continue;
+    }
+    if (open.a >= 0) {
+      // candidate merge of [open.a, open.b) with [c0, c1)
+      std::vector<int32_t> R2;
+      R2.reserve(open.R.size() + Rs.size());
+      std::vector<int32_t> tail;
+      for (int32_t r : open.R)
+        if (r >= c1) tail.push_back(r);
+      std::set_union(tail.begin(), tail.end(), Rs.begin(), Rs.end(), std::back_inserter(R2));
+      const double w2 = (double)(c1 - open.a);
+      const double dense = w2 * (w2 + 1) / 2 + w2 * (double)R2.size();
+      const double nnz2 = open.nnz + nnz_s;
+      const double zf = 1.0 - nnz2 / dense;
+      if (w2 <= PW && (zf <= zmax || w2 <= wsmall)) {
+        open.b = c1;
+        open.R.swap(R2);
+        open.nnz = nnz2;
+        continue;
+      }
+      close_open();
+    }
+    open.a = c0;
+    open.b = c1;
+    open.R = Rs;
+    open.nnz = nnz_s;
+  }
+  close_open();
+
+  // --- panel-buffer layout and the CSC -> panel-buffer scatter map
+  int64_t pb = 0;
+  C.dest.assign((size_t)cp[n], 0);
+  for (auto& p : C.panels) {
+    p.kw4 = (p.kw + 3) & ~3;
+    p.ldD = block_ld(p.kw);
+    p.nchunk = (p.nR + kChunk - 1) / kChunk;
+    p.ldLast = p.nchunk ? block_ld(p.nR - (p.nchunk - 1) * kChunk) : 4;
+    p.buf_off = pb;
+    p.csc_begin = cp[p.a];
+    p.csc_end = cp[p.a + p.kw];
+    const int64_t chunk0 = pb + (int64_t)p.ldD * p.kw4;
+    const int32_t b = p.a + p.kw;
+    const int32_t* R = C.Rrows.data() + p.R_off;
+    for (int32_t c = p.a; c < b; c++)
+      for (int64_t q = cp[c]; q < cp[c + 1]; q++) {
+        const int32_t r = ri[q];
+        if (r < b) {
+          C.dest[(size_t)q] = -1 - ((c - p.a) * kMaxPanel + (r - p.a));
+        } else {
+          const int32_t k = (int32_t)(std::lower_bound(R, R + p.nR, r) - R);
+          const int32_t ch = k / kChunk, kr = k % kChunk;
+          const int64_t off = chunk0 + (int64_t)ch * block_ld(kChunk) * p.kw4 +
+                              (int64_t)(c - p.a) * (ch == p.nchunk - 1 ? p.ldLast : block_ld(kChunk)) + kr;
+          if (off > INT32_MAX) FAIL(SC_ERR_INVALID_ARG, "panel buffer exceeds 2^31 doubles per subdomain");
+          C.dest[(size_t)q] = (int32_t)off;
+        }
+      }
+    pb = chunk0 + (int64_t)(p.nchunk > 0 ? (p.nchunk - 1) : 0) * block_ld(kChunk) * p.kw4 +
+         (p.nchunk > 0 ? (int64_t)p.ldLast * p.kw4 : 0);
+    C.fl_prep_exec += (double)p.kw * p.kw * p.kw / 3.0;
+  }
+  C.pb_doubles = pb;
 
   // --- 3. permuted B~^T, pivots, stepped order
   std::vector<int32_t> iperm((size_t)n);
@@ -204,118 +323,149 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int PW, int skip, Cla
     C.fl_trsm_sparse = (double)m * (2.0 * (double)cp[n] - (double)n);
   }
 
-  // --- 4/5. tiles, reach, panel steps, B scatter
+  // --- 4/5. TRSM tiles: reach at panel granularity, steps (panels in order), B scatter
+  const int32_t np = (int32_t)C.panels.size();
   const int32_t ntiles = (m + T - 1) / T;
-  std::vector<int32_t> entry((size_t)C.nsup, INT32_MAX);
-  std::vector<int32_t> strip_base((size_t)C.nsup, -1);
-  int64_t xoff = 0;
+  std::vector<int32_t> inreach((size_t)np, -1), stamp((size_t)n, -1), strip_base((size_t)np, -1);
+  std::vector<std::vector<int32_t>> tile_panels((size_t)ntiles);
   for (int32_t J = 0; J < ntiles; J++) {
     Tile t{};
     t.col0 = J * T;
     t.width = std::min(T, m - J * T);
-    std::fill(entry.begin(), entry.end(), INT32_MAX);
+    t.group = t.col0 / kGroup;
+    t.col_in_group = t.col0 - t.group * kGroup;
     int32_t pmin = n;
     for (int32_t a = t.col0; a < t.col0 + t.width; a++) pmin = std::min(pmin, C.pivot[(size_t)a]);
+    auto& tp = tile_panels[(size_t)J];
     if (skip == SC_SKIP_EXACT) {
       for (int32_t a = t.col0; a < t.col0 + t.width; a++)
-        for (auto& e : bcol[(size_t)C.sigma[(size_t)a]]) {
-          int32_t cur = e.first;
-          while (true) {
-            int32_t s = snode_of[(size_t)cur];
-            if (entry[(size_t)s] <= cur) break;
-            entry[(size_t)s] = cur;
-            if (C.sn_nR[(size_t)s] == 0) break;
-            cur = C.Rrows[(size_t)C.sn_Roff[(size_t)s]];
+        for (auto& e : bcol[(size_t)C.sigma[(size_t)a]])
+          for (int32_t c = e.first; c >= 0 && stamp[(size_t)c] != J; c = parent[(size_t)c]) {
+            stamp[(size_t)c] = J;
+            inreach[(size_t)panel_of_col[(size_t)c]] = J;
           }
-        }
+      for (int32_t p = 0; p < np; p++)
+        if (inreach[(size_t)p] == J) tp.push_back(p);
     } else if (pmin < n) {
-      int32_t from = (skip == SC_SKIP_ENVELOPE) ? pmin : 0;
-      for (int32_t s = 0; s < C.nsup; s++)
-        if (C.sn_c1[(size_t)s] > from) entry[(size_t)s] = std::max(C.sn_c0[(size_t)s], from);
+      const int32_t from = (skip == SC_SKIP_ENVELOPE) ? pmin : 0;
+      for (int32_t p = 0; p < np; p++)
+        if (C.panels[(size_t)p].a + C.panels[(size_t)p].kw > from) tp.push_back(p);
     }
-    t.reach_begin = (int32_t)C.reach.size();
     t.step_begin = (int32_t)C.steps.size();
     int32_t rows = 0;
-    for (int32_t s = 0; s < C.nsup; s++) {
-      if (entry[(size_t)s] == INT32_MAX) {
-        strip_base[(size_t)s] = -1;
-        continue;
-      }
-      int32_t e = entry[(size_t)s], c1 = C.sn_c1[(size_t)s];
-      C.reach.push_back({s, e, c1, rows});
-      strip_base[(size_t)s] = rows;
-      for (int32_t a = e; a < c1; a += PW) {
-        Step st{};
-        st.e = a;
-        st.kw = std::min(PW, c1 - a);
-        st.c1 = c1;
-        st.nR = C.sn_nR[(size_t)s];
-        st.R_off = C.sn_Roff[(size_t)s];
-        st.strip_row = rows + (a - e);
-        C.steps.push_back(st);
-        int64_t M = (int64_t)(c1 - a - st.kw) + st.nR;
-        C.fl_trsm_exec += (double)T * st.kw * ((double)st.kw + 2.0 * (double)M);
-      }
-      rows += c1 - e;
+    for (int32_t p : tp) {
+      strip_base[(size_t)p] = rows;
+      C.steps.push_back({p, rows});
+      const Panel& P = C.panels[(size_t)p];
+      C.fl_trsm_exec += 2.0 * T * P.kw4 * ((double)P.kw4 + (double)P.nR);
+      rows += P.kw;
     }
-    t.reach_end = (int32_t)C.reach.size();
     t.step_end = (int32_t)C.steps.size();
     t.strip_rows = rows;
+    C.max_strip_rows = std::max(C.max_strip_rows, rows);
     t.binit_begin = (int32_t)C.binit.size();
     for (int32_t a = t.col0; a < t.col0 + t.width; a++)
       for (auto& e : bcol[(size_t)C.sigma[(size_t)a]]) {
-        int32_t s = snode_of[(size_t)e.first];
-        int32_t sr = strip_base[(size_t)s] + (e.first - entry[(size_t)s]);
-        C.binit.push_back({sr, a - t.col0, e.second});
+        const int32_t p = panel_of_col[(size_t)e.first];
+        C.binit.push_back({strip_base[(size_t)p] + (e.first - C.panels[(size_t)p].a), a - t.col0, e.second});
       }
     t.binit_end = (int32_t)C.binit.size();
-    t.x_off = xoff;
-    xoff += (int64_t)rows * T;
     C.tiles.push_back(t);
+  }
+
+  // --- SYRK groups (kGroup columns): union of member tiles' panels; tile write-out segments
+  const int32_t ngroups = (m + kGroup - 1) / kGroup;
+  int64_t xoff = 0;
+  for (int32_t g = 0; g < ngroups; g++) {
+    Group G{};
+    G.col0 = g * kGroup;
+    G.width = std::min(kGroup, m - g * kGroup);
+    std::vector<int32_t> gp;
+    for (int32_t J = 0; J < ntiles; J++)
+      if (C.tiles[(size_t)J].group == g) {
+        std::vector<int32_t> u;
+        std::set_union(gp.begin(), gp.end(), tile_panels[(size_t)J].begin(), tile_panels[(size_t)J].end(),
+                       std::back_inserter(u));
+        gp.swap(u);
+      }
+    G.reach_begin = (int32_t)C.greach.size();
+    int32_t rows = 0;
+    for (int32_t p : gp) {
+      C.greach.push_back({p, rows});
+      rows += C.panels[(size_t)p].kw;
+    }
+    G.reach_end = (int32_t)C.greach.size();
+    G.strip_rows = rows;
+    G.x_off = xoff;
+    xoff += (int64_t)rows * kGroup;
+    for (int32_t J = 0; J < ntiles; J++) {
+      Tile& t = C.tiles[(size_t)J];
+      if (t.group != g) continue;
+      t.wseg_begin = (int32_t)C.wsegs.size();
+      const auto& tpn = tile_panels[(size_t)J];
+      size_t k = 0;
+      int32_t src = 0;
+      for (int32_t q = G.reach_begin; q < G.reach_end; q++) {
+        const Reach& R = C.greach[(size_t)q];
+        const int32_t kw = C.panels[(size_t)R.panel].kw;
+        int32_t s = -1;
+        if (k < tpn.size() && tpn[k] == R.panel) {
+          s = src;
+          src += kw;
+          k++;
+        }
+        if ((int32_t)C.wsegs.size() > t.wseg_begin) {
+          WSeg& last = C.wsegs.back();
+          const bool contig_dst = last.dst + last.len == R.off;
+          if (contig_dst && ((s < 0 && last.src < 0) || (s >= 0 && last.src >= 0 && last.src + last.len == s))) {
+            last.len += kw;
+            continue;
+          }
+        }
+        C.wsegs.push_back({s, R.off, kw, 0});
+      }
+      t.wseg_end = (int32_t)C.wsegs.size();
+    }
+    C.groups.push_back(G);
   }
   C.x_doubles = xoff;
 
-  // --- 6. SYRK output tiles I >= J with their common-row segments
-  for (int32_t I = 0; I < ntiles; I++)
+  // --- 6. SYRK output tiles I >= J over groups with their common-row segments
+  for (int32_t I = 0; I < ngroups; I++)
     for (int32_t J = 0; J <= I; J++) {
-      const Tile &ti = C.tiles[(size_t)I], &tj = C.tiles[(size_t)J];
+      const Group &gi = C.groups[(size_t)I], &gj = C.groups[(size_t)J];
       Pair pr{I, J, (int32_t)C.segs.size(), 0};
-      int32_t qi = ti.reach_begin, qj = tj.reach_begin;
+      int32_t qi = gi.reach_begin, qj = gj.reach_begin;
       int64_t K = 0;
-      while (qi < ti.reach_end && qj < tj.reach_end) {
-        const Reach &ri_ = C.reach[(size_t)qi], &rj = C.reach[(size_t)qj];
-        if (ri_.s < rj.s) {
+      while (qi < gi.reach_end && qj < gj.reach_end) {
+        const Reach &a = C.greach[(size_t)qi], &b = C.greach[(size_t)qj];
+        if (a.panel < b.panel) {
           qi++;
           continue;
         }
-        if (rj.s < ri_.s) {
+        if (b.panel < a.panel) {
           qj++;
           continue;
         }
-        int32_t start = std::max(ri_.e, rj.e);
-        int32_t len = ri_.c1 - start;
-        int32_t oi = ri_.off + (start - ri_.e), oj = rj.off + (start - rj.e);
-        if (len > 0) {
-          if ((int32_t)C.segs.size() > pr.seg_begin) {
-            Seg& last = C.segs.back();
-            if (last.offI + last.len == oi && last.offJ + last.len == oj) {
-              last.len += len;
-              K += len;
-              qi++;
-              qj++;
-              continue;
-            }
+        const int32_t len = C.panels[(size_t)a.panel].kw;
+        K += len;
+        if ((int32_t)C.segs.size() > pr.seg_begin) {
+          Seg& last = C.segs.back();
+          if (last.offI + last.len == a.off && last.offJ + last.len == b.off) {
+            last.len += len;
+            qi++;
+            qj++;
+            continue;
           }
-          C.segs.push_back({oi, oj, len, 0});
-          K += len;
         }
+        C.segs.push_back({a.off, b.off, len, 0});
         qi++;
         qj++;
       }
       pr.seg_end = (int32_t)C.segs.size();
       if (pr.seg_end > pr.seg_begin) {
         C.pairs.push_back(pr);
-        C.fl_syrk_exec += 2.0 * T * T * (double)K;
+        C.fl_syrk_exec += 2.0 * kGroup * kGroup * (double)K;
       }
     }
   return SC_OK;
@@ -327,28 +477,26 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   if (nsub < 0 || (nsub > 0 && !sd)) FAIL(SC_ERR_INVALID_ARG, "sd is NULL or nsub < 0");
   if (opt.precision != 64) FAIL(SC_ERR_INVALID_ARG, "only precision = 64 (FP64) is supported");
   if (opt.skip < 0 || opt.skip > 2) FAIL(SC_ERR_INVALID_ARG, "skip must be 0, 1 or 2");
-  if (!(opt.tile_cols == 0 || opt.tile_cols == 16 || opt.tile_cols == 32 || opt.tile_cols == 64))
-    FAIL(SC_ERR_INVALID_ARG, "tile_cols must be 0, 16, 32 or 64");
+  if (!(opt.tile_cols == 0 || opt.tile_cols == 8 || opt.tile_cols == 16 || opt.tile_cols == 32 || opt.tile_cols == 64))
+    FAIL(SC_ERR_INVALID_ARG, "tile_cols must be 0, 8, 16, 32 or 64");
   if (opt.panel_cols < 0 || opt.panel_cols > kMaxPanel) FAIL(SC_ERR_INVALID_ARG, "panel_cols must be in [0, 64]");
   for (int k = 0; k < 7; k++)
     if (opt.reserved[k] != 0) FAIL(SC_ERR_INVALID_ARG, "reserved options must be zero");
   P.opt = opt;
   P.nsub = nsub;
   P.n_lambda = opt.n_lambda_global;
-  int32_t max_m = 0;
   for (int32_t i = 0; i < nsub; i++) {
     sc_status st = validate_desc(sd[i], i, err);
     if (st != SC_OK) return st;
-    max_m = std::max(max_m, sd[i].m);
     if (sd[i].lambda_map)
       for (int32_t a = 0; a < sd[i].m; a++)
         if (sd[i].lambda_map[a] < 0 || sd[i].lambda_map[a] >= opt.n_lambda_global)
           FAIL(SC_ERR_INVALID_ARG, "subdomain " + std::to_string(i) + ": lambda_map entry outside [0, n_lambda_global)");
   }
-  P.T = opt.tile_cols ? opt.tile_cols : (max_m <= 64 ? 16 : (max_m <= 512 ? 32 : 64));
   P.PW = opt.panel_cols ? opt.panel_cols : kMaxPanel;
 
-  // --- classes (dedup identical patterns)
+  // --- classes (dedup identical patterns); the TRSM tile width is chosen so the largest X strip
+  // fits in shared memory (T = 32 when possible, else 16; tile_cols forces a width)
   std::unordered_map<uint64_t, std::vector<int32_t>> by_hash;
   std::vector<int32_t> rep;  // representative subdomain of each class
   P.sub_cls.assign((size_t)nsub, -1);
@@ -367,60 +515,107 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
       P.classes.back().hash = h;
       rep.push_back(i);
       cands.push_back(cls);
-      sc_status st = analyse_class(sd[i], P.T, P.PW, opt.skip, P.classes.back(), err);
-      if (st != SC_OK) {
-        err = "subdomain " + std::to_string(i) + ": " + err;
-        return st;
-      }
     }
     P.sub_cls[(size_t)i] = cls;
   }
+  // SYRK output tile (group) width: 64 for large local operators, 32 otherwise (never below T)
+  int32_t max_m = 0;
+  for (int32_t i = 0; i < nsub; i++) max_m = std::max(max_m, sd[i].m);
+  int32_t G0 = max_m > 512 ? 64 : 32;
+  if (const char* e = std::getenv("SC_GROUP")) G0 = std::atoi(e);
+  if (!(G0 == 16 || G0 == 32 || G0 == 64)) FAIL(SC_ERR_INVALID_ARG, "SC_GROUP must be 16, 32 or 64");
+  auto analyse_all = [&](int T) -> sc_status {
+    P.T = T;
+    P.G = std::max(G0, T);
+    for (size_t c = 0; c < P.classes.size(); c++) {
+      uint64_t h = P.classes[c].hash;
+      P.classes[c] = ClassPlan();
+      P.classes[c].hash = h;
+      sc_status st = analyse_class(sd[rep[c]], T, P.G, P.PW, opt.skip, P.classes[c], err);
+      if (st != SC_OK) {
+        err = "subdomain " + std::to_string(rep[c]) + ": " + err;
+        return st;
+      }
+    }
+    return SC_OK;
+  };
+  // TRSM tile width: the widest of 32 / 16 / 8 whose largest X strip fits in shared memory
+  int32_t max_n = 0;
+  for (int32_t i = 0; i < nsub; i++) max_n = std::max(max_n, sd[i].n);
+  auto fits = [&](int T) {
+    int32_t mx = 0;
+    for (auto& C : P.classes) mx = std::max(mx, C.max_strip_rows);
+    return trsm_smem_layout(T, max_n, mx).total <= kSmemBudget;
+  };
+  if (opt.tile_cols) {
+    sc_status st = analyse_all(opt.tile_cols);
+    if (st != SC_OK) return st;
+  } else {
+    const int cand[3] = {32, 16, 8};
+    for (int k = 0; k < 3; k++) {
+      sc_status st = analyse_all(cand[k]);
+      if (st != SC_OK) return st;
+      if (fits(cand[k])) break;
+    }
+  }
+  for (auto& C : P.classes) P.max_strip_rows = std::max(P.max_strip_rows, C.max_strip_rows);
 
   // --- global concatenation: class-local indices -> global
-  int32_t tile_base = 0, step_base = 0, reach_base = 0, binit_base = 0, seg_base = 0, R_base = 0, pair_base = 0;
+  int32_t tile_base = 0, step_base = 0, binit_base = 0, seg_base = 0, R_base = 0, pair_base = 0, panel_base = 0,
+          group_base = 0, greach_base = 0, wseg_base = 0;
   for (auto& C : P.classes) {
     P.cls_tile_begin.push_back(tile_base);
     P.cls_pair_begin.push_back(pair_base);
+    P.cls_panel_begin.push_back(panel_base);
+    P.cls_group_begin.push_back(group_base);
+    for (auto& p : C.panels) p.R_off += R_base;
+    for (auto& s : C.steps) s.panel += panel_base;
+    for (auto& r : C.greach) r.panel += panel_base;
     for (auto& t : C.tiles) {
       t.step_begin += step_base;
       t.step_end += step_base;
-      t.reach_begin += reach_base;
-      t.reach_end += reach_base;
       t.binit_begin += binit_base;
       t.binit_end += binit_base;
+      t.wseg_begin += wseg_base;
+      t.wseg_end += wseg_base;
+      t.group += group_base;
     }
-    for (auto& s : C.steps) s.R_off += R_base;
+    for (auto& g : C.groups) {
+      g.reach_begin += greach_base;
+      g.reach_end += greach_base;
+    }
     for (auto& p : C.pairs) {
-      p.I += tile_base;
-      p.J += tile_base;
+      p.I += group_base;
+      p.J += group_base;
       p.seg_begin += seg_base;
       p.seg_end += seg_base;
     }
     tile_base += (int32_t)C.tiles.size();
     step_base += (int32_t)C.steps.size();
-    reach_base += (int32_t)C.reach.size();
     binit_base += (int32_t)C.binit.size();
     seg_base += (int32_t)C.segs.size();
     R_base += (int32_t)C.Rrows.size();
     pair_base += (int32_t)C.pairs.size();
+    panel_base += (int32_t)C.panels.size();
+    group_base += (int32_t)C.groups.size();
+    greach_base += (int32_t)C.greach.size();
+    wseg_base += (int32_t)C.wsegs.size();
   }
 
   // --- per subdomain layout + task lists
   P.sub_m.resize((size_t)nsub);
   P.sub_n.resize((size_t)nsub);
   P.sub_nnz.resize((size_t)nsub);
-  P.lambda_map.resize((size_t)nsub);
   sc_stats& S = P.stats;
   std::memset(&S, 0, sizeof(S));
   S.nsub = nsub;
   S.n_classes = (int32_t)P.classes.size();
   S.tile_cols = P.T;
   S.panel_cols = P.PW;
-  std::vector<std::vector<std::pair<int64_t, int64_t>>> contrib;  // unused placeholder
   std::vector<int64_t> qcount((size_t)std::max<int64_t>(opt.n_lambda_global, 0) + 1, 0);
   for (int32_t i = 0; i < nsub; i++) {
-    const ClassPlan& C = P.classes[(size_t)P.sub_cls[(size_t)i]];
-    int32_t cls = P.sub_cls[(size_t)i];
+    const int32_t cls = P.sub_cls[(size_t)i];
+    const ClassPlan& C = P.classes[(size_t)cls];
     P.sub_m[(size_t)i] = C.m;
     P.sub_n[(size_t)i] = C.n;
     P.sub_nnz[(size_t)i] = C.colptr[(size_t)C.n];
@@ -429,25 +624,24 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     P.X_doubles += C.x_doubles;
     P.sub_F_base.push_back(P.F_doubles);
     P.F_doubles += (int64_t)C.m * C.m;
+    P.sub_PB_base.push_back(P.PB_doubles);
+    P.PB_doubles += C.pb_doubles;
     P.sub_part_off.push_back(P.part_doubles);
-    int32_t nblk = (C.m + 31) / 32;
-    P.part_doubles += (int64_t)nblk * C.m;
+    P.part_doubles += (int64_t)((C.m + 31) / 32) * C.m;
+    for (size_t q = 0; q < C.panels.size(); q++) P.prep_tasks.push_back({i, P.cls_panel_begin[(size_t)cls] + (int32_t)q});
     for (size_t t = 0; t < C.tiles.size(); t++)
-      if (C.tiles[t].strip_rows > 0) P.trsm_tasks.push_back({i, P.cls_tile_begin[(size_t)cls] + (int32_t)t});
+      if (C.tiles[t].width > 0) P.trsm_tasks.push_back({i, P.cls_tile_begin[(size_t)cls] + (int32_t)t});
     for (size_t q = 0; q < C.pairs.size(); q++) P.syrk_tasks.push_back({i, P.cls_pair_begin[(size_t)cls] + (int32_t)q});
     for (int32_t b = 0; b < C.m; b += 32) P.apply_tasks.push_back({i, b});
-    auto& lm = P.lambda_map[(size_t)i];
-    lm.assign((size_t)C.m, -1);
     P.sub_slm_off.push_back((int64_t)P.slm.size());
     if (sd[i].lambda_map) {
-      lm.assign(sd[i].lambda_map, sd[i].lambda_map + C.m);
       for (int32_t a = 0; a < C.m; a++) {
-        int64_t g = lm[(size_t)C.sigma[(size_t)a]];
+        int64_t g = sd[i].lambda_map[C.sigma[(size_t)a]];
         P.slm.push_back(g);
         qcount[(size_t)g]++;
       }
     } else {
-      for (int32_t a = 0; a < C.m; a++) P.slm.push_back(-1);
+      for (int32_t a = 0; a < C.m; a++) P.slm.push_back(0);
     }
     S.sum_n += C.n;
     S.sum_m += C.m;
@@ -464,24 +658,25 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     S.flops_syrk_executed += C.fl_syrk_exec;
     S.bytes_L_values += 8.0 * (double)C.colptr[(size_t)C.n];
     S.bytes_F_lower += 8.0 * (double)C.m * (C.m + 1) / 2.0;
-    S.trsm_steps += 0;
-    for (auto& t : C.tiles) S.trsm_steps += t.step_end - t.step_begin;
-    for (auto& p : C.pairs) S.syrk_segments += p.seg_end - p.seg_begin;
+    S.trsm_steps += (int64_t)C.steps.size();
+    S.syrk_segments += (int64_t)C.segs.size();
     S.bytes_apply += 8.0 * (double)C.m * (C.m + 1) / 2.0 + 8.0 * 3.0 * C.m;
+    S.bytes_panels += 8.0 * (double)C.pb_doubles;
+    S.panels += (int64_t)C.panels.size();
   }
-  (void)contrib;
+  S.group_cols = P.G;
   S.trsm_tasks = (int64_t)P.trsm_tasks.size();
   S.syrk_tasks = (int64_t)P.syrk_tasks.size();
   S.bytes_X = 8.0 * (double)P.X_doubles;
   // CSR over global multipliers of the (sub, stepped position) contributions, in (sub, a) order
-  int64_t NL = std::max<int64_t>(opt.n_lambda_global, 0);
+  const int64_t NL = std::max<int64_t>(opt.n_lambda_global, 0);
   P.qg_ptr.assign((size_t)NL + 1, 0);
   for (int64_t g = 0; g < NL; g++) P.qg_ptr[(size_t)g + 1] = P.qg_ptr[(size_t)g] + qcount[(size_t)g];
   P.qg_sub_a.assign((size_t)P.qg_ptr[(size_t)NL], 0);
-  std::vector<int64_t> fillpos(P.qg_ptr.begin(), P.qg_ptr.end() - (NL >= 0 ? 1 : 0));
+  std::vector<int64_t> fillpos(P.qg_ptr.begin(), P.qg_ptr.begin() + NL);
   for (int32_t i = 0; i < nsub; i++) {
-    const ClassPlan& C = P.classes[(size_t)P.sub_cls[(size_t)i]];
     if (!sd[i].lambda_map) continue;
+    const ClassPlan& C = P.classes[(size_t)P.sub_cls[(size_t)i]];
     for (int32_t a = 0; a < C.m; a++) {
       int64_t g = P.slm[(size_t)(P.sub_slm_off[(size_t)i] + a)];
       P.qg_sub_a[(size_t)fillpos[(size_t)g]++] = ((int64_t)i << 32) | (int64_t)a;

@@ -12,30 +12,88 @@ namespace sc {
 
 constexpr int kThreads = 256;   // every kernel uses 8 warps
 constexpr int kMaxPanel = 64;   // max factor panel width (factor-splitting block)
-constexpr int kChunk = 64;      // rows per update / GEMM chunk
+constexpr int kChunk = 64;      // below-diagonal rows per L block
 
-// One RHS column tile of one pattern class: stepped columns [col0, col0+width) (P:473-480 RHS
-// splitting at tile granularity).  Its X strip holds only the rows of its reach, row-major with
-// T doubles per row, at offset x_off inside the subdomain's X region.
+#ifdef __CUDACC__
+#define SC_HD __host__ __device__
+#else
+#define SC_HD
+#endif
+
+// Leading dimension (in doubles) of a staged block holding `rows` rows: the smallest value
+// >= rows that is == 4 (mod 16), so DMMA fragment loads (4 consecutive k x 8 consecutive rows)
+// hit 16 distinct 8-byte bank pairs.
+SC_HD constexpr int block_ld(int rows) { return rows <= 4 ? 4 : 4 + 16 * ((rows - 4 + 15) / 16); }
+
+constexpr int kLdC = 68;                        // block_ld(kChunk): ld of a full 64-row chunk
+constexpr size_t kSmemBudget = 232448;          // B200 max dynamic shared memory per block (227 KB)
+constexpr int kSlots = 8;                       // TRSM L-block pipeline depth (mbarrier pairs)
+constexpr int kRingBytes = 73728;               // TRSM L-block ring (holds >= 2 full 68x64 blocks)
+constexpr int kTrsmThreads = kThreads + 32;     // 8 consumer warps + 1 TMA producer warp
+
+// Byte offsets of the TRSM kernel's dynamic shared memory: full/empty mbarriers and ring offsets
+// of the L-block pipeline, the byte ring of L blocks, the row -> strip map (uint16 per factor
+// row) and the X strip ((strip_cap + 4) rows of T + 4 doubles).
+struct TrsmSmem {
+  size_t full, empty, off, ring, map, strip, total;
+};
+SC_HD inline TrsmSmem trsm_smem_layout(int T, int max_n, int strip_cap) {
+  TrsmSmem s{};
+  s.full = 0;
+  s.empty = 8 * kSlots;
+  s.off = 16 * kSlots;
+  s.ring = 256;
+  s.map = s.ring + (size_t)kRingBytes;
+  s.strip = (s.map + sizeof(uint16_t) * (size_t)max_n + 127) & ~(size_t)127;
+  s.total = s.strip + sizeof(double) * (size_t)(strip_cap + 4) * (size_t)(T + 4);
+  return s;
+}
+
+// A factor panel (P:482-494 factor splitting; relaxed: several small supernodes may be merged
+// into one dense panel, zeros stored explicitly).  Columns [a, a+kw); below-diagonal row set
+// R_p = Rrows[R_off .. R_off+nR) (ascending, all >= a+kw: the pruned rows).  In the
+// per-subdomain panel buffer (written by the prep kernel) it occupies, from buf_off: the inverse
+// of its diagonal block (ldD x kw4, column-major) then ceil(nR/64) row chunks of L[R_p, panel]
+// (chunk c: ld = block_ld(rows_c) x kw4, column-major).
+struct Panel {
+  int32_t a, kw, kw4, nR;
+  int32_t R_off, nchunk, ldD, ldLast;   // ldLast = ld of the last chunk
+  int64_t buf_off;                      // doubles from the subdomain's panel-buffer base
+  int64_t csc_begin, csc_end;           // L entries of columns [a, a+kw) in CSC order
+};
+
+// One RHS column tile of TRSM width T of one pattern class: stepped columns [col0, col0+width)
+// (P:473-480 RHS splitting at tile granularity).  Its X strip holds the rows of the panels of
+// its reach (whole panels), in panel order.
 struct Tile {
-  int32_t col0, width, strip_rows, pad;
-  int32_t step_begin, step_end;    // TRSM panel steps (global indices into steps[])
-  int32_t reach_begin, reach_end;  // reach entries (global indices into reach[])
+  int32_t col0, width, strip_rows, group;
+  int32_t step_begin, step_end;    // panels visited (global indices into steps[])
   int32_t binit_begin, binit_end;  // B~^T scatter entries (global indices into binit[])
-  int64_t x_off;                   // doubles from the subdomain's X base
+  int32_t wseg_begin, wseg_end;    // write-out segments into the group strip (global, wsegs[])
+  int32_t col_in_group, pad;
 };
 
-// One factor panel of a supernode as a TRSM step of one tile (diagonal-block TRSM
-// then GEMM update of the pruned sub-diagonal rows).  Panel columns [e, e+kw) of the supernode
-// whose last column is c1-1 and whose pruned row structure is R_s = Rrows[R_off .. R_off+nR).
+// TRSM step: tile visits panel `panel` (global index) whose rows start at `strip_row`.
 struct Step {
-  int32_t e, kw, c1, nR;
-  int32_t R_off, strip_row;        // strip row of factor row e in the tile's X strip
+  int32_t panel, strip_row;
 };
 
-// The rows [e, c1) of supernode s held by a tile's strip, starting at strip row `off`.
+// Write-out of a tile strip into its group strip: rows [src, src+len) of the tile strip go to
+// rows [dst, dst+len) of the group strip; src < 0: the tile does not hold that panel (zeros).
+struct WSeg {
+  int32_t src, dst, len, pad;
+};
+
+// SYRK column group (width kGroup, a union of TRSM tiles): its X strip in global memory holds
+// the union of the member tiles' panels; reach entries (panel, off) in panel order.
+struct Group {
+  int32_t col0, width, strip_rows, pad;
+  int32_t reach_begin, reach_end;
+  int64_t x_off;                   // doubles from the subdomain's X base (row-major, kGroup wide)
+};
+
 struct Reach {
-  int32_t s, e, c1, off;
+  int32_t panel, off;              // global panel index, first strip row
 };
 
 // One structural non-zero of B~^T placed in a tile strip (P:399-405 stepped column permutation).
@@ -44,10 +102,10 @@ struct BInit {
   double val;
 };
 
-// SYRK output tile (I >= J) of a class: F'[I,J] = sum over segments of X_I[seg]^T X_J[seg]
+// SYRK output tile (I >= J) of a class over groups: F'[I,J] = sum_seg X_I[seg]^T X_J[seg]
 // (P:534-540 output splitting with per-block k range; segments = rows both strips hold).
 struct Pair {
-  int32_t I, J;                    // global tile indices
+  int32_t I, J;                    // global group indices
   int32_t seg_begin, seg_end;      // global indices into segs[]
 };
 
@@ -68,42 +126,51 @@ struct ClassPlan {
   int32_t n = 0, m = 0, nsup = 0;
   uint64_t hash = 0;
   std::vector<int64_t> colptr;     // copy of L_colptr (n+1)
-  std::vector<int32_t> rowidx;     // copy of L_rowidx (host: X export + checks)
   std::vector<int32_t> perm;       // perm[new] = old
-  std::vector<int32_t> sn_c0, sn_c1, sn_nR;  // supernodes
-  std::vector<int32_t> sn_Roff;    // offset into Rrows (class-local)
-  std::vector<int32_t> Rrows;      // concatenated R_s
+  std::vector<int32_t> dest;       // per CSC entry: >= 0 panel-buffer offset (below rows),
+                                   //   < 0: -1 - (col_in_panel * 64 + row_in_panel) (triangle)
+  std::vector<Panel> panels;
+  std::vector<int32_t> Rrows;      // concatenated R_p
   std::vector<int32_t> sigma;      // stepped position -> original local column
   std::vector<int32_t> pivot;      // per stepped position (permuted row), n for empty columns
-  std::vector<Tile> tiles;         // class-local indices in the *_begin/_end fields
+  std::vector<Tile> tiles;         // *_begin/_end: class-local until build_plan globalises them
   std::vector<Step> steps;
-  std::vector<Reach> reach;
+  std::vector<WSeg> wsegs;
+  std::vector<Group> groups;
+  std::vector<Reach> greach;
   std::vector<BInit> binit;
   std::vector<Pair> pairs;
   std::vector<Seg> segs;
-  int64_t x_doubles = 0;           // X region size per subdomain
+  int64_t x_doubles = 0;           // X region (group strips) per subdomain
+  int64_t pb_doubles = 0;          // panel buffer per subdomain
+  int32_t max_strip_rows = 0;      // over TRSM tiles
   // counters (per subdomain of this class)
   double fl_trsm_useful = 0, fl_syrk_useful = 0, fl_trsm_env = 0, fl_syrk_env = 0;
   double fl_trsm_dense = 0, fl_syrk_dense = 0, fl_trsm_sparse = 0;
-  double fl_trsm_exec = 0, fl_syrk_exec = 0;
+  double fl_trsm_exec = 0, fl_syrk_exec = 0, fl_prep_exec = 0;
 };
 
 // Device-side view passed by value to every kernel.
 struct DevPlan {
-  const int64_t* colptr;           // concatenated class colptrs
-  const int64_t* cls_colptr_off;   // per class
-  const int32_t* Rrows;            // concatenated (global offsets baked into Step.R_off)
+  const Panel* panels;             // all classes, concatenated
+  const int32_t* Rrows;
+  const int32_t* dest;             // concatenated per class (offset cls_csc_off)
+  const int64_t* cls_csc_off;
   const Tile* tiles;
   const Step* steps;
-  const Reach* reach;
+  const WSeg* wsegs;
+  const Group* groups;
+  const Reach* greach;
   const BInit* binit;
   const Pair* pairs;
   const Seg* segs;
   const int32_t* sub_cls;          // per subdomain
   const int64_t* sub_X_base;       // per subdomain, doubles
   const int64_t* sub_F_base;       // per subdomain, doubles (F' lower, column-major, ld = m)
+  const int64_t* sub_PB_base;      // per subdomain panel buffer, doubles
   const int32_t* sub_m;
   const double* const* Lptr;       // per subdomain L values (device)
+  const I2* prep_tasks;            // (sub, global panel)
   const I2* trsm_tasks;            // (sub, global tile)
   const I2* syrk_tasks;            // (sub, global pair)
   const ApplyTask* apply_tasks;
@@ -114,28 +181,28 @@ struct DevPlan {
   const int64_t* qg_sub_a;         // (sub << 32) | a
   double* X;
   double* F;
+  double* PB;                      // panel buffers
   double* part;
   unsigned long long* err;         // sticky device error: ((sub+1) << 32) | col
-  int32_t nsub, max_n;
+  int32_t nsub, max_n, T, G, strip_cap;  // strip_cap: rows of the shared-memory strip
 };
 
 struct Plan {
   sc_options opt{};
-  int32_t T = 64, PW = 64;
+  int32_t T = 32, G = 64, PW = 64;
   int32_t nsub = 0;
   std::vector<ClassPlan> classes;
   std::vector<int32_t> sub_cls;
   std::vector<int32_t> sub_m, sub_n;
   std::vector<int64_t> sub_nnz;
-  std::vector<std::vector<int64_t>> lambda_map;  // per subdomain (original local order)
   // global (concatenated) arrays
-  std::vector<int32_t> cls_tile_begin, cls_pair_begin;
-  std::vector<I2> trsm_tasks, syrk_tasks;
+  std::vector<int32_t> cls_tile_begin, cls_pair_begin, cls_panel_begin, cls_group_begin;
+  std::vector<I2> prep_tasks, trsm_tasks, syrk_tasks;
   std::vector<ApplyTask> apply_tasks;
-  std::vector<int64_t> sub_X_base, sub_F_base, sub_part_off, sub_slm_off;
+  std::vector<int64_t> sub_X_base, sub_F_base, sub_PB_base, sub_part_off, sub_slm_off;
   std::vector<int64_t> slm, qg_ptr, qg_sub_a;
-  int64_t X_doubles = 0, F_doubles = 0, part_doubles = 0;
-  int32_t max_n = 0;
+  int64_t X_doubles = 0, F_doubles = 0, PB_doubles = 0, part_doubles = 0;
+  int32_t max_n = 0, max_strip_rows = 0;
   sc_stats stats{};
   // device state
   bool on_device = false;
@@ -150,7 +217,7 @@ struct Plan {
   void* last_stream = nullptr;
   void* tev[3] = {nullptr, nullptr, nullptr};  // optional timing events (sc_set_timing_events)
   int64_t n_lambda = 0;
-  size_t smem_trsm = 0, smem_syrk = 0;
+  size_t smem_trsm = 0;
 };
 
 // plan.cpp

@@ -48,7 +48,8 @@ class Stats(ctypes.Structure):
                                                "flops_syrk_envelope", "flops_trsm_dense", "flops_syrk_dense",
                                                "flops_trsm_sparse_orig", "flops_trsm_executed",
                                                "flops_syrk_executed", "bytes_L_values", "bytes_F_lower", "bytes_X",
-                                               "device_bytes", "bytes_apply")]
+                                               "device_bytes", "bytes_apply", "bytes_panels")] + \
+               [("panels", ctypes.c_int64), ("group_cols", ctypes.c_int32), ("pad0", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -57,7 +58,8 @@ class Stats(ctypes.Structure):
 _lib = None
 
 EXPORTS = ["sc_options_default", "sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply",
-           "sc_check", "sc_get_F", "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_set_timing_events", "sc_launches_per_assemble",
+           "sc_check", "sc_get_F", "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_plan_subdomain_costs",
+           "sc_set_timing_events", "sc_launches_per_assemble",
            "sc_launches_per_apply", "sc_plan_destroy", "sc_last_error"]
 
 
@@ -81,6 +83,7 @@ def lib():
     L.sc_plan_strip_rows.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _P, _P]
     L.sc_plan_stats.argtypes = [_P, ctypes.POINTER(Stats)]
     L.sc_set_timing_events.argtypes = [_P, _P, _P, _P]
+    L.sc_plan_subdomain_costs.argtypes = [_P, _P]
     L.sc_launches_per_assemble.argtypes = [_P]
     L.sc_launches_per_assemble.restype = ctypes.c_int32
     L.sc_launches_per_apply.argtypes = [_P]
@@ -90,7 +93,7 @@ def lib():
     L.sc_last_error.argtypes = []
     L.sc_last_error.restype = ctypes.c_char_p
     for f in ("sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply", "sc_check", "sc_get_F",
-              "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_set_timing_events"):
+              "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_set_timing_events", "sc_plan_subdomain_costs"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
     return L
@@ -212,6 +215,11 @@ class SCPlan:
         k = ctypes.c_int32(0)
         _check(lib().sc_plan_strip_rows(self._h, i, a, rows.ctypes.data, ctypes.addressof(k)))
         return rows[:k.value]
+
+    def subdomain_costs(self) -> np.ndarray:
+        c = np.zeros(max(self.nsub, 1))
+        _check(lib().sc_plan_subdomain_costs(self._h, c.ctypes.data))
+        return c[:self.nsub]
 
     def stats(self) -> dict:
         s = Stats()
