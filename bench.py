@@ -165,6 +165,7 @@ def main():
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-amortization", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
@@ -204,7 +205,7 @@ def main():
     plan.check()
 
     # timed region: K steps, per-kernel events recorded inside sc_assemble_batch on `stream`
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
     for row in evs:  # torch creates the CUDA event lazily on first record
         for e in row:
             e.record(stream)
@@ -215,16 +216,17 @@ def main():
     with ClockSampler(local) as clk:
         start.record(stream)
         for k in range(args.steps):
-            plan.set_timing_events(*evs[k])
+            plan.set_timing_events(evs[k])
             plan.assemble(Ls)
         stop.record(stream)
         torch.cuda.synchronize()
-    plan.set_timing_events(None, None, None)
+    plan.set_timing_events(None)
     if world > 1:
         dist.barrier()
     ms_total = start.elapsed_time(stop)
-    ms_trsm = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    ms_syrk = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    ms_prep = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    ms_trsm = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    ms_syrk = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
     plan.check()
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -271,20 +273,63 @@ def main():
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel (useful FP64 flops per launch / live event time)
-    dom = "trsm" if ms_trsm >= ms_syrk else "syrk"
-    dom_ms = ms_trsm if dom == "trsm" else ms_syrk
-    dom_flops = st["flops_trsm_useful"] if dom == "trsm" else st["flops_syrk_useful"]
-    achieved = dom_flops / (dom_ms / 1e3) / 1e12
+    # roofline of the dominant kernel: prep is HBM-bound (algorithmic bytes: L values read once),
+    # TRSM and SYRK are FP64-tensor-bound (algorithmic flops: useful etree-exact flops)
+    phases = {"prep": ms_prep, "trsm": ms_trsm, "syrk": ms_syrk}
+    dom = max(phases, key=phases.get)
+    dom_ms = phases[dom]
     prof_traffic = None
     tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
     if os.path.exists(tp):
         prof_traffic = json.load(open(tp)).get(dom)
-    roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                "frac": achieved / peaks["fp64_tflops"], "traffic": prof_traffic, "kernel": f"{dom}",
-                "dtype": "f64 (DMMA m8n8k4)", "peak_source": peaks["fp64_tflops_source"],
-                "algorithmic": "useful (etree-exact) FP64 flops of the phase per launch",
-                "share_of_step": dom_ms / ms_step}
+    kernel_names = {"prep": "prep_panel_kernel + prep_small_kernel", "trsm": f"trsm_smem_kernel<{st['tile_cols']}>",
+                    "syrk": f"syrk_pair_kernel<{st['group_cols']}>"}
+    if dom == "prep":
+        achieved = st["bytes_L_values"] / (dom_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": achieved / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                    "algorithmic": "L values read once (8 B / nnz(L)) per launch"}
+    else:
+        dom_flops = st["flops_trsm_useful"] if dom == "trsm" else st["flops_syrk_useful"]
+        achieved = dom_flops / (dom_ms / 1e3) / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+                    "frac": achieved / peaks["fp64_tflops"], "dtype": "f64 (DMMA m8n8k4)",
+                    "peak_source": peaks["fp64_tflops_source"],
+                    "algorithmic": "useful (etree-exact) FP64 flops of the phase per launch"}
+    roofline.update({"traffic": prof_traffic, "kernel": kernel_names[dom], "share_of_step": dom_ms / ms_step})
+    # amortization point: explicit GPU (assembly + apply per
+    # iteration) vs implicit CPU apply per iteration on the host cores; the factorization is common
+    # to both and cancels.  k* = smallest k with t_asm + k t_expl < k t_impl.
+    amort = None
+    if not args.no_amortization:
+        lam_d = torch.from_numpy(np.random.default_rng(7).standard_normal(P.n_lambda)).cuda()
+        q_d = torch.empty_like(lam_d)
+        for _ in range(3):
+            plan.apply(lam_d, q_d)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 20
+        torch.cuda.synchronize()
+        a0.record(stream)
+        for _ in range(reps):
+            plan.apply(lam_d, q_d)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        t_expl = a0.elapsed_time(a1) / reps
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from implicit_cpu import ImplicitCPU
+        ic = ImplicitCPU(P)
+        t_impl = 1e3 * ic.time(reps=5, warmup=1)
+        q_impl = ic.apply(lam_d.cpu().numpy())
+        agree = float(np.linalg.norm(q_d.cpu().numpy() - q_impl) / np.linalg.norm(q_impl))
+
+        def kstar(t_asm):
+            d = t_impl - t_expl
+            return int(t_asm // d) + 1 if d > 0 else None
+
+        amort = {"iters": kstar(ms_step), "iters_e2e": kstar(e2e["ms_per_step"]) if e2e else None,
+                 "t_assembly_ms": ms_step, "t_apply_explicit_gpu_ms": t_expl, "t_apply_implicit_cpu_ms": t_impl,
+                 "cpu_threads": ic.used_threads, "explicit_vs_implicit_rel_diff": agree,
+                 "paper": "~10 iterations (A100 + 16 EPYC cores, P:56, P:2919)"}
     cpu = None
     if not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
@@ -304,8 +349,8 @@ def main():
         "gflops_useful": world * useful / (ms_step / 1e3) / 1e9,
         "gflops_executed": world * (st["flops_trsm_executed"] + st["flops_syrk_executed"]) / (ms_step / 1e3) / 1e9,
         "fp64_frac_useful": useful / (ms_step / 1e3) / 1e12 / peaks["fp64_tflops"],
-        "phase_ms": {"trsm": ms_trsm, "syrk": ms_syrk},
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "phase_ms": {"prep": ms_prep, "trsm": ms_trsm, "syrk": ms_syrk},
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "amortization": amort,
         "gpu_launches": args.steps * plan.launches_per_assemble,
         "clocks": clocks, "plan_s": t_plan,
         "paper_context": {"a100_sep_opt_ms_per_subdomain": PAPER_A100_MS.get(args.config),

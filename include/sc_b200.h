@@ -157,10 +157,11 @@ sc_status sc_plan_stats(sc_plan_t p, sc_stats* out);
    size-balanced assignment of subdomains to GPUs (works for host-only plans). */
 sc_status sc_plan_subdomain_costs(sc_plan_t p, double* costs);
 
-/* Measurement hook: when set (non-NULL), every following sc_assemble_batch records the three
-   cudaEvent_t handles (passed as void*) on its stream: ev0 before the TRSM kernel, ev1 between the
-   TRSM and the SYRK kernel, ev2 after the SYRK kernel.  Pass NULLs to disable. */
-sc_status sc_set_timing_events(sc_plan_t p, void* ev0, void* ev1, void* ev2);
+/* Measurement hook: with n == 4, every following sc_assemble_batch records the cudaEvent_t handles
+   events[0..3] (passed as void*) on its stream: before the prep kernels, after prep (before the
+   TRSM), after the TRSM (before the SYRK), after the SYRK.  n == 0 disables.  The plan keeps the
+   handles, not copies; the caller keeps the events alive. */
+sc_status sc_set_timing_events(sc_plan_t p, void* const* events, int32_t n);
 
 /* Number of kernel launches one sc_assemble_batch / sc_apply enqueues. */
 int32_t sc_launches_per_assemble(sc_plan_t p);

@@ -178,17 +178,17 @@ sc_status sc_plan_subdomain_costs(sc_plan_t p, double* costs) {
   return SC_OK;
 }
 
-sc_status sc_set_timing_events(sc_plan_t p, void* ev0, void* ev1, void* ev2) {
+sc_status sc_set_timing_events(sc_plan_t p, void* const* events, int32_t n) {
   if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
-  p->P.tev[0] = ev0;
-  p->P.tev[1] = ev1;
-  p->P.tev[2] = ev2;
+  if (!(n == 0 || (n == 4 && events))) return fail(SC_ERR_INVALID_ARG, "n must be 0 or 4 (with events)");
+  for (int k = 0; k < 4; k++) p->P.tev[k] = n ? events[k] : nullptr;
   return SC_OK;
 }
 
 int32_t sc_launches_per_assemble(sc_plan_t p) {
   if (!p) return 0;
-  return (p->P.trsm_tasks.empty() ? 0 : 1) + (p->P.syrk_tasks.empty() ? 0 : 1);
+  return (p->P.prep_tasks.empty() ? 0 : 1) + (p->P.prep_small_tasks.empty() ? 0 : 1) +
+         (p->P.trsm_tasks.empty() ? 0 : 1) + (p->P.syrk_tasks.empty() ? 0 : 1);
 }
 
 int32_t sc_launches_per_apply(sc_plan_t p) {

@@ -104,10 +104,9 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
   const int kw = pn.kw, kw4 = pn.kw4;
   int npad = 8;  // triangle padded to npad = 8 * 2^k >= kw with a unit diagonal
   while (npad < kw) npad *= 2;
-  {
+  {  // W needs no clearing: every block it is read at is written first (triangular loop bounds)
     double2* D2 = reinterpret_cast<double2*>(D);
-    double2* W2 = reinterpret_cast<double2*>(W);
-    for (int q = tid; q < npad * kLdT / 2; q += kThreads) D2[q] = W2[q] = make_double2(0.0, 0.0);
+    for (int q = tid; q < npad * kLdT / 2; q += kThreads) D2[q] = make_double2(0.0, 0.0);
   }
   // zero the chunk region (structural zeros of relaxed panels + padding)
   {
@@ -162,7 +161,8 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
       const double* Cm = D + base * kLdT + base + h;  // C: rows base+h.., cols base..
       const double* Ai = W + base * kLdT + base;
       double c0 = 0.0, c1 = 0.0;
-      for (int k = 0; k < h; k += 4) dmma(c0, c1, Cm[(k + t4) * kLdT + bi * 8 + g], Ai[(bj * 8 + g) * kLdT + k + t4]);
+      // inv(A) is lower triangular: only k >= 8 bj contributes
+      for (int k = bj * 8; k < h; k += 4) dmma(c0, c1, Cm[(k + t4) * kLdT + bi * 8 + g], Ai[(bj * 8 + g) * kLdT + k + t4]);
       double* Tt = D + base * kLdT + base;
       Tt[(bj * 8 + 2 * t4) * kLdT + bi * 8 + g] = c0;
       Tt[(bj * 8 + 2 * t4 + 1) * kLdT + bi * 8 + g] = c1;
@@ -175,7 +175,8 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
       const double* Bi = W + (base + h) * kLdT + base + h;
       const double* Tt = D + base * kLdT + base;
       double c0 = 0.0, c1 = 0.0;
-      for (int k = 0; k < h; k += 4) dmma(c0, c1, Bi[(k + t4) * kLdT + bi * 8 + g], Tt[(bj * 8 + g) * kLdT + k + t4]);
+      // inv(B) is lower triangular: only k < 8 (bi + 1) contributes
+      for (int k = 0; k < (bi + 1) * 8; k += 4) dmma(c0, c1, Bi[(k + t4) * kLdT + bi * 8 + g], Tt[(bj * 8 + g) * kLdT + k + t4]);
       double* Wo = W + base * kLdT + base + h;
       Wo[(bj * 8 + 2 * t4) * kLdT + bi * 8 + g] = -c0;
       Wo[(bj * 8 + 2 * t4 + 1) * kLdT + bi * 8 + g] = -c1;
@@ -191,6 +192,102 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
   }
 }
 
+
+// Panels of <= kSmallPanel columns: one warp per panel (no CTA barriers), same algorithm.
+constexpr int kLdS = kSmallPanel + 4;              // 36 == 4 (mod 16)
+constexpr int kSmallWarps = 4;
+constexpr size_t kPrepSmallSmem = 2 * sizeof(double) * kSmallPanel * kLdS * kSmallWarps;
+
+__global__ void __launch_bounds__(32 * kSmallWarps) prep_small_kernel(DevPlan P) {
+  extern __shared__ __align__(16) unsigned char prep_smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * kSmallWarps + warp;
+  if (t >= P.n_prep_small) return;
+  double* D = reinterpret_cast<double*>(prep_smem) + (size_t)warp * 2 * kSmallPanel * kLdS;
+  double* W = D + kSmallPanel * kLdS;
+  const I2 task = P.prep_small_tasks[t];
+  const int sub = task.x;
+  const Panel pn = P.panels[task.y];
+  const int32_t* __restrict__ dest = P.dest + P.cls_csc_off[P.sub_cls[sub]];
+  const double* __restrict__ Lv = P.Lptr[sub];
+  double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
+  const int kw = pn.kw, kw4 = pn.kw4;
+  int npad = 8;
+  while (npad < kw) npad *= 2;
+  for (int q = lane; q < npad * kLdS / 2; q += 32) reinterpret_cast<double2*>(D)[q] = make_double2(0.0, 0.0);
+  {
+    const int64_t c0 = pn.buf_off + (int64_t)pn.ldD * kw4;
+    const int64_t len = (pn.nchunk > 0) ? ((int64_t)(pn.nchunk - 1) * kLdC + pn.ldLast) * kw4 : 0;
+    double2* z = reinterpret_cast<double2*>(PB + c0);
+    for (int64_t q = lane; q < len / 2; q += 32) z[q] = make_double2(0.0, 0.0);
+  }
+  __syncwarp();
+  for (int64_t q = pn.csc_begin + lane; q < pn.csc_end; q += 32) {
+    const double v = Lv[q];
+    const int32_t d = dest[q];
+    if (d < 0) {
+      const int idx = -1 - d;
+      D[(idx >> 6) * kLdS + (idx & 63)] = v;
+    } else {
+      PB[d] = v;
+    }
+  }
+  for (int i = kw + lane; i < npad; i += 32) D[i * kLdS + i] = 1.0;
+  __syncwarp();
+  {  // level 0: lane -> (8x8 block lane/8, column lane%8)
+    const int base = (lane >> 3) * 8, j = lane & 7;
+    if (base < npad) {
+      double x[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        double s = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+        for (int k = 0; k < i; k++) s -= (k >= j) ? D[(base + k) * kLdS + base + i] * x[k] : 0.0;
+        const double dii = D[(base + i) * kLdS + base + i];
+        if (j == 0 && base + i < kw && (!(dii > 0.0) || !isfinite(dii)))
+          atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + base + i));
+        x[i] = (i >= j) ? s / dii : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; i++) W[(base + j) * kLdS + base + i] = x[i];
+    }
+  }
+  __syncwarp();
+  const int g = lane >> 2, t4 = lane & 3;
+  for (int b = 16; b <= npad; b *= 2) {
+    const int h = b / 2, nbh = h / 8, npairs = npad / b;
+    for (int blk = 0; blk < npairs * nbh * nbh; blk++) {
+      const int pr = blk / (nbh * nbh), rem = blk - pr * nbh * nbh, bi = rem % nbh, bj = rem / nbh;
+      const int base = pr * b;
+      const double* Cm = D + base * kLdS + base + h;
+      const double* Ai = W + base * kLdS + base;
+      double c0 = 0.0, c1 = 0.0;
+      for (int k = bj * 8; k < h; k += 4) dmma(c0, c1, Cm[(k + t4) * kLdS + bi * 8 + g], Ai[(bj * 8 + g) * kLdS + k + t4]);
+      double* Tt = D + base * kLdS + base;
+      Tt[(bj * 8 + 2 * t4) * kLdS + bi * 8 + g] = c0;
+      Tt[(bj * 8 + 2 * t4 + 1) * kLdS + bi * 8 + g] = c1;
+    }
+    __syncwarp();
+    for (int blk = 0; blk < npairs * nbh * nbh; blk++) {
+      const int pr = blk / (nbh * nbh), rem = blk - pr * nbh * nbh, bi = rem % nbh, bj = rem / nbh;
+      const int base = pr * b;
+      const double* Bi = W + (base + h) * kLdS + base + h;
+      const double* Tt = D + base * kLdS + base;
+      double c0 = 0.0, c1 = 0.0;
+      for (int k = 0; k < (bi + 1) * 8; k += 4) dmma(c0, c1, Bi[(k + t4) * kLdS + bi * 8 + g], Tt[(bj * 8 + g) * kLdS + k + t4]);
+      double* Wo = W + base * kLdS + base + h;
+      Wo[(bj * 8 + 2 * t4) * kLdS + bi * 8 + g] = -c0;
+      Wo[(bj * 8 + 2 * t4 + 1) * kLdS + bi * 8 + g] = -c1;
+    }
+    __syncwarp();
+  }
+  double* Dinv = PB + pn.buf_off;
+  const int ldD = pn.ldD;
+  for (int q = lane; q < ldD * kw4; q += 32) {
+    const int j = q / ldD, i = q - j * ldD;
+    Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * kLdS + i] : 0.0;
+  }
+}
 
 // ------------------------------------------------------------------------------------------------
 // TRSM with the X strip resident in shared memory (warp-specialised: 8 DMMA consumer warps + one
@@ -214,15 +311,17 @@ __device__ __forceinline__ void consumer_sync() {  // named barrier over the 8 c
   asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads) : "memory");
 }
 
-// Producer (one lane): walks the tile's block stream [inv(L_pp), chunk 0, chunk 1, ...] per step
-// and issues each block with cp.async.bulk into the ring as soon as a slot and the bytes are free.
+// Producer (one lane): walks the tile's block stream [inv(L_pp), chunk 0, chunk 1, ...] per step,
+// issues each block with cp.async.bulk into the ring as soon as a slot and the bytes are free; a
+// chunk block travels with its 64 precomputed strip rows (128 B, same mbarrier).
 __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, const double* PB, unsigned char* ring,
-                                           uint64_t* full, uint64_t* empty, int32_t* off) {
+                                           uint64_t* full, uint64_t* empty, int32_t* off, uint16_t* srow) {
   int q_slot[kSlots], q_start[kSlots];  // FIFO of in-flight blocks
   int q_head = 0, inflight = 0, ring_head = 0, ring_tail = 0;
   int b = 0;
   for (int s = tile.step_begin; s < tile.step_end; s++) {
-    const Panel pn = P.panels[P.steps[s].panel];
+    const Step st = P.steps[s];
+    const Panel pn = P.panels[st.panel];
     for (int c = -1; c < pn.nchunk; c++, b++) {
       const double* src;
       int bytes;
@@ -269,8 +368,10 @@ __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, c
       inflight++;
       ring_tail = start + bytes;
       off[slot] = start;
-      mbar_expect_tx(&full[slot], (uint32_t)bytes);
+      const uint32_t rb = (c >= 0) ? (uint32_t)(kChunk * sizeof(uint16_t)) : 0u;
+      mbar_expect_tx(&full[slot], (uint32_t)bytes + rb);
       bulk_g2s(ring + start, src, (uint32_t)bytes, &full[slot]);
+      if (c >= 0) bulk_g2s(srow + slot * kChunk, P.srows + st.srow_off + (int64_t)c * kChunk, rb, &full[slot]);
     }
   }
 }
@@ -284,8 +385,9 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem_raw + L.empty);
   int32_t* off = reinterpret_cast<int32_t*>(smem_raw + L.off);
+  uint16_t* srow = reinterpret_cast<uint16_t*>(smem_raw + L.srow);
   unsigned char* ring = smem_raw + L.ring;
-  uint16_t* map = reinterpret_cast<uint16_t*>(smem_raw + L.map);
+  double* Ys = reinterpret_cast<double*>(smem_raw + L.ys);
   double* Xs = reinterpret_cast<double*>(smem_raw + L.strip);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -303,40 +405,33 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
   }
   __syncthreads();
   if (warp == kThreads / 32) {  // ---- TMA producer warp
-    if (lane == 0) trsm_producer(P, tile, PB, ring, full, empty, off);
+    if (lane == 0) trsm_producer(P, tile, PB, ring, full, empty, off, srow);
     return;
   }
 
-  // ---- consumers.  X init (row a2): zero the strip (+4 pad rows), row map, scatter B~^T
+  // ---- consumers.  X init (row a2): zero the strip (+4 pad rows), scatter B~^T
   const int g = lane >> 2, t4 = lane & 3;
   const int br0 = (warp / NWC) * WM, bc0 = (warp % NWC) * WN;
   {
     double2* X2 = reinterpret_cast<double2*>(Xs);
     const int nvec = (tile.strip_rows + 4) * LDX / 2;
     for (int q = tid; q < nvec; q += kThreads) X2[q] = make_double2(0.0, 0.0);
-    uint32_t* m2 = reinterpret_cast<uint32_t*>(map);
-    for (int q = tid; q < (P.max_n + 1) / 2; q += kThreads) m2[q] = 0xFFFFFFFFu;
   }
   consumer_sync();
-  for (int s = tile.step_begin + warp; s < tile.step_end; s += kThreads / 32) {
-    const Step st = P.steps[s];
-    const Panel pn = P.panels[st.panel];
-    for (int r = lane; r < pn.kw; r += 32) map[pn.a + r] = (uint16_t)(st.strip_row + r);
-  }
   for (int q = tile.binit_begin + tid; q < tile.binit_end; q += kThreads) {
-    const BInit b = P.binit[q];
-    Xs[b.strip_row * LDX + b.col] = b.val;
+    const BInit bi = P.binit[q];
+    Xs[bi.strip_row * LDX + bi.col] = bi.val;
   }
   consumer_sync();
 
-  // ---- stepped supernodal TRSM (row a3)
+  // ---- stepped supernodal TRSM (row a3); two consumer barriers per factor panel
   int b = 0;  // block counter (same order as the producer)
   for (int s = tile.step_begin; s < tile.step_end; s++, b++) {
     const Step st = P.steps[s];
     const Panel pn = P.panels[st.panel];
     const int kw = pn.kw, kw4 = pn.kw4;
     double* Xp = Xs + st.strip_row * LDX;
-    double acc[WM][WN][2];
+    double yacc[WM][WN][2], acc[WM][WN][2];
     // Y = inv(L_pp) X_p  (inv(L_pp) lower triangular: row block i needs k < 8 (i + 1))
     {
       const int slot = b % kSlots;
@@ -346,7 +441,7 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
 #pragma unroll
       for (int i = 0; i < WM; i++)
 #pragma unroll
-        for (int j = 0; j < WN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < WN; j++) yacc[i][j][0] = yacc[i][j][1] = 0.0;
       const int kend = min(kw4, (br0 + WM) * 8);
       if (br0 * 8 < kw4) {
         for (int k = 0; k < kend; k += 4) {
@@ -358,54 +453,57 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
 #pragma unroll
           for (int i = 0; i < WM; i++)
 #pragma unroll
-            for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+            for (int j = 0; j < WN; j++) dmma(yacc[i][j][0], yacc[i][j][1], a[i], bb[j]);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
-      consumer_sync();  // every warp has read X_p
 #pragma unroll
       for (int i = 0; i < WM; i++) {
         const int r = (br0 + i) * 8 + g;
-        if (r < kw) {
+        if (r < kw4) {
 #pragma unroll
           for (int j = 0; j < WN; j++)
-            *reinterpret_cast<double2*>(Xp + r * LDX + (bc0 + j) * 8 + 2 * t4) =
-                make_double2(acc[i][j][0], acc[i][j][1]);
+            *reinterpret_cast<double2*>(Ys + r * LDX + (bc0 + j) * 8 + 2 * t4) =
+                make_double2(yacc[i][j][0], yacc[i][j][1]);
         }
       }
-      consumer_sync();  // Y visible
+      consumer_sync();  // Y visible to every warp
     }
-    // X[R_p] -= L[R_p, p] Y, one 64-row chunk (one ring block) at a time; no CTA barrier between
-    // chunks: chunks update disjoint rows and each warp releases its ring slot itself
+    // X[R_p] -= L[R_p, p] Y, one 64-row chunk (one ring block) at a time; chunks update disjoint
+    // rows and each warp releases its ring slot itself, so no barrier between chunks.  The warp's
+    // Y fragments stay in registers for all chunks of the panel: only L is read from shared memory.
+    double yf[kMaxPanel / 4][WN];
+#pragma unroll
+    for (int ks = 0; ks < kMaxPanel / 4; ks++)
+#pragma unroll
+      for (int j = 0; j < WN; j++) yf[ks][j] = (4 * ks < kw4) ? Ys[(4 * ks + t4) * LDX + (bc0 + j) * 8 + g] : 0.0;
     for (int c = 0; c < pn.nchunk; c++) {
       b++;
       const int rows_c = min(kChunk, pn.nR - c * kChunk);
       const int ld = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
-      int srow[WM];
-#pragma unroll
-      for (int i = 0; i < WM; i++) {
-        const int r = (br0 + i) * 8 + g;
-        srow[i] = (r < rows_c) ? (int)map[P.Rrows[pn.R_off + c * kChunk + r]] : 0xFFFF;
-      }
       const int slot = b % kSlots;
       mbar_wait(&full[slot], (uint32_t)(b / kSlots) & 1u);
       const double* A = reinterpret_cast<const double*>(ring + off[slot]);
+      int sr[WM];
+#pragma unroll
+      for (int i = 0; i < WM; i++) sr[i] = (int)srow[slot * kChunk + (br0 + i) * 8 + g];
       if (br0 * 8 < rows_c) {
 #pragma unroll
         for (int i = 0; i < WM; i++)
 #pragma unroll
           for (int j = 0; j < WN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
-        for (int k = 0; k < kw4; k += 4) {
-          double a[WM], bb[WN];
 #pragma unroll
-          for (int i = 0; i < WM; i++) a[i] = A[(k + t4) * ld + (br0 + i) * 8 + g];
+        for (int ks = 0; ks < kMaxPanel / 4; ks++) {
+          if (4 * ks < kw4) {
+            double a[WM];
 #pragma unroll
-          for (int j = 0; j < WN; j++) bb[j] = Xp[(k + t4) * LDX + (bc0 + j) * 8 + g];
+            for (int i = 0; i < WM; i++) a[i] = A[(4 * ks + t4) * ld + (br0 + i) * 8 + g];
 #pragma unroll
-          for (int i = 0; i < WM; i++)
+            for (int i = 0; i < WM; i++)
 #pragma unroll
-            for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+              for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], yf[ks][j]);
+          }
         }
       }
       __syncwarp();
@@ -413,10 +511,10 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
       if (br0 * 8 < rows_c) {
 #pragma unroll
         for (int i = 0; i < WM; i++) {
-          if (srow[i] == 0xFFFF) continue;  // row outside this tile's reach: its update is exactly 0
+          if (sr[i] == 0xFFFF) continue;  // row outside this tile's reach (or padding): update is 0
 #pragma unroll
           for (int j = 0; j < WN; j++) {
-            double2* p = reinterpret_cast<double2*>(Xs + srow[i] * LDX + (bc0 + j) * 8 + 2 * t4);
+            double2* p = reinterpret_cast<double2*>(Xs + sr[i] * LDX + (bc0 + j) * 8 + 2 * t4);
             double2 v = *p;
             v.x -= acc[i][j][0];
             v.y -= acc[i][j][1];
@@ -425,7 +523,17 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
         }
       }
     }
-    consumer_sync();  // updates visible before the next panel reads its rows
+    // the panel's rows are final: X_p = Y (GEMM1's reads of X_p finished before the barrier above)
+#pragma unroll
+    for (int i = 0; i < WM; i++) {
+      const int r = (br0 + i) * 8 + g;
+      if (r < kw) {
+#pragma unroll
+        for (int j = 0; j < WN; j++)
+          *reinterpret_cast<double2*>(Xp + r * LDX + (bc0 + j) * 8 + 2 * t4) = make_double2(yacc[i][j][0], yacc[i][j][1]);
+      }
+    }
+    consumer_sync();  // strip updates visible before the next panel reads its rows; Ys reusable
   }
 
   // ---- write the strip into the group strip (row-major, G columns) for the SYRK
@@ -442,7 +550,6 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
   }
 }
 
-
 // ------------------------------------------------------------------------------------------------
 // SYRK over G-column groups: F'[I,J] = sum_seg X_I[seg]^T X_J[seg] (lower part of F' only)
 // ------------------------------------------------------------------------------------------------
@@ -457,11 +564,26 @@ struct SyrkCfg {              // (G/8)^2 output blocks of 8x8 over 8 warps
   static constexpr int ACTIVE = (NB / WM) * NWC;   // warps with work (4 for G = 16)
 };
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int G>
+constexpr size_t syrk_smem_bytes() {
+  return sizeof(double) * 4 * kKC * (G + 4);  // 2 stages x (X_I chunk, X_J chunk)
+}
+
 template <int G>
 __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P) {
   constexpr int kLdG = G + 4, kGroup = G;
-  __shared__ __align__(16) double As[kKC * kLdG];
-  __shared__ __align__(16) double Bs[kKC * kLdG];
+  extern __shared__ __align__(16) unsigned char syrk_smem[];
+  double* Sbuf = reinterpret_cast<double*>(syrk_smem);
   constexpr int WM = SyrkCfg<G>::WM, WN = SyrkCfg<G>::WN, NWC = SyrkCfg<G>::NWC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool active = warp < SyrkCfg<G>::ACTIVE;
@@ -479,38 +601,56 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P) {
 #pragma unroll
     for (int j = 0; j < WN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  for (int sg = pr.seg_begin; sg < pr.seg_end; sg++) {
-    const Seg s = P.segs[sg];
-    for (int k0 = 0; k0 < s.len; k0 += kKC) {
-      const int kn = min(kKC, s.len - k0);
+  // k chunks of kKC rows over the segments, two-stage cp.async pipeline (load chunk i+1 while
+  // the tensor cores work on chunk i)
+  int csg = pr.seg_begin, ck0 = 0;  // cursor of the next chunk to load
+  auto load = [&](int stage) -> int {
+    int kn = 0;
+    if (csg < pr.seg_end) {
+      const Seg s = P.segs[csg];
+      kn = min(kKC, s.len - ck0);
+      double* As = Sbuf + (2 * stage) * kKC * kLdG;
+      double* Bs = As + kKC * kLdG;
       for (int q = tid; q < kKC * (kGroup / 2); q += kThreads) {
         const int r = q / (kGroup / 2), j = 2 * (q - r * (kGroup / 2));
-        double2 va = make_double2(0.0, 0.0), vb = make_double2(0.0, 0.0);
-        if (r < kn) {
-          va = *reinterpret_cast<const double2*>(XI + (int64_t)(s.offI + k0 + r) * kGroup + j);
-          vb = *reinterpret_cast<const double2*>(XJ + (int64_t)(s.offJ + k0 + r) * kGroup + j);
-        }
-        *reinterpret_cast<double2*>(As + r * kLdG + j) = va;
-        *reinterpret_cast<double2*>(Bs + r * kLdG + j) = vb;
+        const int rr = r < kn ? r : 0;
+        cp_async16(As + r * kLdG + j, XI + (int64_t)(s.offI + ck0 + rr) * kGroup + j, r < kn ? 16 : 0);
+        cp_async16(Bs + r * kLdG + j, XJ + (int64_t)(s.offJ + ck0 + rr) * kGroup + j, r < kn ? 16 : 0);
       }
-      __syncthreads();
-      const int kn4 = (kn + 3) & ~3;
-      if (active) {
-        for (int k = 0; k < kn4; k += 4) {
-          double a[WM], b[WN];
-#pragma unroll
-          for (int i = 0; i < WM; i++) a[i] = As[(k + t4) * kLdG + (br0 + i) * 8 + g];
-#pragma unroll
-          for (int j = 0; j < WN; j++) b[j] = Bs[(k + t4) * kLdG + (bc0 + j) * 8 + g];
-#pragma unroll
-          for (int i = 0; i < WM; i++)
-#pragma unroll
-            for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
-        }
+      ck0 += kKC;
+      if (ck0 >= s.len) {
+        csg++;
+        ck0 = 0;
       }
-      __syncthreads();
     }
+    cp_async_commit();
+    return kn;
+  };
+  int kn_next = load(0);
+  for (int it = 0; kn_next > 0; it++) {
+    const int cur = it & 1, kn = kn_next;
+    kn_next = load(cur ^ 1);
+    cp_async_wait<1>();
+    __syncthreads();
+    const double* As = Sbuf + (2 * cur) * kKC * kLdG;
+    const double* Bs = As + kKC * kLdG;
+    const int kn4 = (kn + 3) & ~3;
+    if (active) {
+      for (int k = 0; k < kn4; k += 4) {
+        double a[WM], b[WN];
+#pragma unroll
+        for (int i = 0; i < WM; i++) a[i] = As[(k + t4) * kLdG + (br0 + i) * 8 + g];
+#pragma unroll
+        for (int j = 0; j < WN; j++) b[j] = Bs[(k + t4) * kLdG + (bc0 + j) * 8 + g];
+#pragma unroll
+        for (int i = 0; i < WM; i++)
+#pragma unroll
+          for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+    }
+    __syncthreads();
   }
+  cp_async_wait<0>();
   if (!active) return;
   const int m = P.sub_m[sub];
   double* __restrict__ F = P.F + P.sub_F_base[sub];
@@ -642,6 +782,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   std::vector<int64_t> csc_off;
   std::vector<Tile> tiles;
   std::vector<Step> steps;
+  std::vector<uint16_t> srows;
   std::vector<WSeg> wsegs;
   std::vector<Group> groups;
   std::vector<Reach> greach;
@@ -655,6 +796,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
     Rrows.insert(Rrows.end(), C.Rrows.begin(), C.Rrows.end());
     tiles.insert(tiles.end(), C.tiles.begin(), C.tiles.end());
     steps.insert(steps.end(), C.steps.begin(), C.steps.end());
+    srows.insert(srows.end(), C.srows.begin(), C.srows.end());
     wsegs.insert(wsegs.end(), C.wsegs.begin(), C.wsegs.end());
     groups.insert(groups.end(), C.groups.begin(), C.groups.end());
     greach.insert(greach.end(), C.greach.begin(), C.greach.end());
@@ -668,6 +810,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, csc_off, &D.cls_csc_off, err));
   TRY(upload(P, tiles, &D.tiles, err));
   TRY(upload(P, steps, &D.steps, err));
+  TRY(upload(P, srows, &D.srows, err));
   TRY(upload(P, wsegs, &D.wsegs, err));
   TRY(upload(P, groups, &D.groups, err));
   TRY(upload(P, greach, &D.greach, err));
@@ -680,6 +823,8 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, P.sub_PB_base, &D.sub_PB_base, err));
   TRY(upload(P, P.sub_m, &D.sub_m, err));
   TRY(upload(P, P.prep_tasks, &D.prep_tasks, err));
+  TRY(upload(P, P.prep_small_tasks, &D.prep_small_tasks, err));
+  D.n_prep_small = (int32_t)P.prep_small_tasks.size();
   TRY(upload(P, P.trsm_tasks, &D.trsm_tasks, err));
   TRY(upload(P, P.syrk_tasks, &D.syrk_tasks, err));
   TRY(upload(P, P.apply_tasks, &D.apply_tasks, err));
@@ -718,6 +863,8 @@ sc_status upload_plan(Plan& P, std::string& err) {
     return SC_ERR_INVALID_ARG;
   }
   CUDA_TRY(cudaFuncSetAttribute(prep_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem));
+  CUDA_TRY(cudaFuncSetAttribute(prep_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmallSmem));
+  CUDA_TRY(cudaFuncSetAttribute(syrk_pair_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)syrk_smem_bytes<64>()));
   switch (P.T) {
     case 8: CUDA_TRY(cudaFuncSetAttribute(trsm_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
     case 16: CUDA_TRY(cudaFuncSetAttribute(trsm_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
@@ -773,6 +920,12 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
     prep_panel_kernel<<<npr, kThreads, kPrepSmem, stream>>>(P.dev);
     CUDA_TRY(cudaGetLastError());
   }
+  const int nps = (int)P.prep_small_tasks.size();
+  if (nps > 0) {
+    prep_small_kernel<<<(nps + kSmallWarps - 1) / kSmallWarps, 32 * kSmallWarps, kPrepSmallSmem, stream>>>(P.dev);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
   if (ntr > 0) {
     switch (P.T) {
       case 8: trsm_smem_kernel<8><<<ntr, kTrsmThreads, P.smem_trsm, stream>>>(P.dev); break;
@@ -782,16 +935,16 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
     }
     CUDA_TRY(cudaGetLastError());
   }
-  if (P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
+  if (P.tev[2]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[2], stream));
   if (nsy > 0) {
     switch (P.G) {
-      case 16: syrk_pair_kernel<16><<<nsy, kThreads, 0, stream>>>(P.dev); break;
-      case 32: syrk_pair_kernel<32><<<nsy, kThreads, 0, stream>>>(P.dev); break;
-      default: syrk_pair_kernel<64><<<nsy, kThreads, 0, stream>>>(P.dev); break;
+      case 16: syrk_pair_kernel<16><<<nsy, kThreads, syrk_smem_bytes<16>(), stream>>>(P.dev); break;
+      case 32: syrk_pair_kernel<32><<<nsy, kThreads, syrk_smem_bytes<32>(), stream>>>(P.dev); break;
+      default: syrk_pair_kernel<64><<<nsy, kThreads, syrk_smem_bytes<64>(), stream>>>(P.dev); break;
     }
     CUDA_TRY(cudaGetLastError());
   }
-  if (P.tev[2]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[2], stream));
+  if (P.tev[3]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[3], stream));
   return SC_OK;
 }
 

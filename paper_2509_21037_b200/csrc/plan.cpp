@@ -326,7 +326,8 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
   // --- 4/5. TRSM tiles: reach at panel granularity, steps (panels in order), B scatter
   const int32_t np = (int32_t)C.panels.size();
   const int32_t ntiles = (m + T - 1) / T;
-  std::vector<int32_t> inreach((size_t)np, -1), stamp((size_t)n, -1), strip_base((size_t)np, -1);
+  std::vector<int32_t> inreach((size_t)np, -1), stamp((size_t)n, -1), strip_base((size_t)np, -1),
+      in_tile((size_t)np, -1);
   std::vector<std::vector<int32_t>> tile_panels((size_t)ntiles);
   for (int32_t J = 0; J < ntiles; J++) {
     Tile t{};
@@ -355,12 +356,29 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     int32_t rows = 0;
     for (int32_t p : tp) {
       strip_base[(size_t)p] = rows;
-      C.steps.push_back({p, rows});
+      in_tile[(size_t)p] = J;
+      C.steps.push_back({p, rows, 0});
       const Panel& P = C.panels[(size_t)p];
-      C.fl_trsm_exec += 2.0 * T * P.kw4 * ((double)P.kw4 + (double)P.nR);
+      // GEMM1 skips the zero blocks above the diagonal of inv(L_pp)
+      C.fl_trsm_exec += 2.0 * T * P.kw4 * (0.5 * (double)P.kw4 + 4.0 + (double)P.nR);
       rows += P.kw;
     }
     t.step_end = (int32_t)C.steps.size();
+    // strip rows of each step's pruned rows R_p, 64 per chunk (0xFFFF: not in this tile's strip)
+    for (int32_t s = t.step_begin; s < t.step_end; s++) {
+      Step& st = C.steps[(size_t)s];
+      const Panel& P = C.panels[(size_t)st.panel];
+      st.srow_off = (int64_t)C.srows.size();
+      for (int32_t k = 0; k < P.nchunk * kChunk; k++) {
+        uint16_t v = 0xFFFF;
+        if (k < P.nR) {
+          const int32_t r = C.Rrows[(size_t)(P.R_off + k)];
+          const int32_t q = panel_of_col[(size_t)r];
+          if (in_tile[(size_t)q] == J) v = (uint16_t)(strip_base[(size_t)q] + (r - C.panels[(size_t)q].a));
+        }
+        C.srows.push_back(v);
+      }
+    }
     t.strip_rows = rows;
     C.max_strip_rows = std::max(C.max_strip_rows, rows);
     t.binit_begin = (int32_t)C.binit.size();
@@ -561,6 +579,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   for (auto& C : P.classes) P.max_strip_rows = std::max(P.max_strip_rows, C.max_strip_rows);
 
   // --- global concatenation: class-local indices -> global
+  int64_t srow_base = 0;
   int32_t tile_base = 0, step_base = 0, binit_base = 0, seg_base = 0, R_base = 0, pair_base = 0, panel_base = 0,
           group_base = 0, greach_base = 0, wseg_base = 0;
   for (auto& C : P.classes) {
@@ -569,7 +588,10 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     P.cls_panel_begin.push_back(panel_base);
     P.cls_group_begin.push_back(group_base);
     for (auto& p : C.panels) p.R_off += R_base;
-    for (auto& s : C.steps) s.panel += panel_base;
+    for (auto& s : C.steps) {
+      s.panel += panel_base;
+      s.srow_off += srow_base;
+    }
     for (auto& r : C.greach) r.panel += panel_base;
     for (auto& t : C.tiles) {
       t.step_begin += step_base;
@@ -600,6 +622,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     group_base += (int32_t)C.groups.size();
     greach_base += (int32_t)C.greach.size();
     wseg_base += (int32_t)C.wsegs.size();
+    srow_base += (int64_t)C.srows.size();
   }
 
   // --- per subdomain layout + task lists
@@ -628,7 +651,9 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     P.PB_doubles += C.pb_doubles;
     P.sub_part_off.push_back(P.part_doubles);
     P.part_doubles += (int64_t)((C.m + 31) / 32) * C.m;
-    for (size_t q = 0; q < C.panels.size(); q++) P.prep_tasks.push_back({i, P.cls_panel_begin[(size_t)cls] + (int32_t)q});
+    for (size_t q = 0; q < C.panels.size(); q++)
+      (C.panels[q].kw > kSmallPanel ? P.prep_tasks : P.prep_small_tasks)
+          .push_back({i, P.cls_panel_begin[(size_t)cls] + (int32_t)q});
     for (size_t t = 0; t < C.tiles.size(); t++)
       if (C.tiles[t].width > 0) P.trsm_tasks.push_back({i, P.cls_tile_begin[(size_t)cls] + (int32_t)t});
     for (size_t q = 0; q < C.pairs.size(); q++) P.syrk_tasks.push_back({i, P.cls_pair_begin[(size_t)cls] + (int32_t)q});

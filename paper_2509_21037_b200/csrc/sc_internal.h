@@ -13,6 +13,7 @@ namespace sc {
 constexpr int kThreads = 256;   // every kernel uses 8 warps
 constexpr int kMaxPanel = 64;   // max factor panel width (factor-splitting block)
 constexpr int kChunk = 64;      // below-diagonal rows per L block
+constexpr int kSmallPanel = 32; // panels up to this width are prepared by one warp each
 
 #ifdef __CUDACC__
 #define SC_HD __host__ __device__
@@ -32,19 +33,22 @@ constexpr int kRingBytes = 73728;               // TRSM L-block ring (holds >= 2
 constexpr int kTrsmThreads = kThreads + 32;     // 8 consumer warps + 1 TMA producer warp
 
 // Byte offsets of the TRSM kernel's dynamic shared memory: full/empty mbarriers and ring offsets
-// of the L-block pipeline, the byte ring of L blocks, the row -> strip map (uint16 per factor
-// row) and the X strip ((strip_cap + 4) rows of T + 4 doubles).
+// of the L-block pipeline, per-slot strip rows of a chunk's R_p rows (uint16, copied with the
+// block), the byte ring of L blocks, the solved panel Y (64 x T+4) and the X strip
+// ((strip_cap + 4) rows of T + 4 doubles).
 struct TrsmSmem {
-  size_t full, empty, off, ring, map, strip, total;
+  size_t full, empty, off, srow, ring, ys, strip, total;
 };
 SC_HD inline TrsmSmem trsm_smem_layout(int T, int max_n, int strip_cap) {
+  (void)max_n;
   TrsmSmem s{};
   s.full = 0;
   s.empty = 8 * kSlots;
   s.off = 16 * kSlots;
-  s.ring = 256;
-  s.map = s.ring + (size_t)kRingBytes;
-  s.strip = (s.map + sizeof(uint16_t) * (size_t)max_n + 127) & ~(size_t)127;
+  s.srow = 256;
+  s.ring = s.srow + sizeof(uint16_t) * kSlots * kChunk;
+  s.ys = s.ring + (size_t)kRingBytes;
+  s.strip = s.ys + sizeof(double) * (size_t)kMaxPanel * (size_t)(T + 4);
   s.total = s.strip + sizeof(double) * (size_t)(strip_cap + 4) * (size_t)(T + 4);
   return s;
 }
@@ -74,8 +78,11 @@ struct Tile {
 };
 
 // TRSM step: tile visits panel `panel` (global index) whose rows start at `strip_row`.
+// srow_off: offset (uint16 units, 64 per chunk) of the strip rows of R_p for this tile in srows[]
+// (0xFFFF = row outside the tile's reach, whose update is exactly zero).
 struct Step {
   int32_t panel, strip_row;
+  int64_t srow_off;
 };
 
 // Write-out of a tile strip into its group strip: rows [src, src+len) of the tile strip go to
@@ -135,6 +142,7 @@ struct ClassPlan {
   std::vector<int32_t> pivot;      // per stepped position (permuted row), n for empty columns
   std::vector<Tile> tiles;         // *_begin/_end: class-local until build_plan globalises them
   std::vector<Step> steps;
+  std::vector<uint16_t> srows;     // per step, per chunk: 64 strip rows of R_p (see Step)
   std::vector<WSeg> wsegs;
   std::vector<Group> groups;
   std::vector<Reach> greach;
@@ -158,6 +166,7 @@ struct DevPlan {
   const int64_t* cls_csc_off;
   const Tile* tiles;
   const Step* steps;
+  const uint16_t* srows;           // concatenated per class (Step.srow_off globalised)
   const WSeg* wsegs;
   const Group* groups;
   const Reach* greach;
@@ -170,7 +179,9 @@ struct DevPlan {
   const int64_t* sub_PB_base;      // per subdomain panel buffer, doubles
   const int32_t* sub_m;
   const double* const* Lptr;       // per subdomain L values (device)
-  const I2* prep_tasks;            // (sub, global panel)
+  const I2* prep_tasks;            // (sub, global panel), panels wider than kSmallPanel
+  const I2* prep_small_tasks;      // (sub, global panel), panels of <= kSmallPanel columns
+  int32_t n_prep_small;
   const I2* trsm_tasks;            // (sub, global tile)
   const I2* syrk_tasks;            // (sub, global pair)
   const ApplyTask* apply_tasks;
@@ -197,7 +208,7 @@ struct Plan {
   std::vector<int64_t> sub_nnz;
   // global (concatenated) arrays
   std::vector<int32_t> cls_tile_begin, cls_pair_begin, cls_panel_begin, cls_group_begin;
-  std::vector<I2> prep_tasks, trsm_tasks, syrk_tasks;
+  std::vector<I2> prep_tasks, prep_small_tasks, trsm_tasks, syrk_tasks;
   std::vector<ApplyTask> apply_tasks;
   std::vector<int64_t> sub_X_base, sub_F_base, sub_PB_base, sub_part_off, sub_slm_off;
   std::vector<int64_t> slm, qg_ptr, qg_sub_a;
@@ -215,7 +226,7 @@ struct Plan {
   double* d_Lstage = nullptr;              // staging for sc_assemble_batch_host
   std::vector<int64_t> Lstage_off;
   void* last_stream = nullptr;
-  void* tev[3] = {nullptr, nullptr, nullptr};  // optional timing events (sc_set_timing_events)
+  void* tev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional timing events (sc_set_timing_events)
   int64_t n_lambda = 0;
   size_t smem_trsm = 0;
 };

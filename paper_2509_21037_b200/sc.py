@@ -82,7 +82,7 @@ def lib():
     L.sc_get_X.argtypes = [_P, ctypes.c_int32, _P, _P]
     L.sc_plan_strip_rows.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _P, _P]
     L.sc_plan_stats.argtypes = [_P, ctypes.POINTER(Stats)]
-    L.sc_set_timing_events.argtypes = [_P, _P, _P, _P]
+    L.sc_set_timing_events.argtypes = [_P, _P, ctypes.c_int32]
     L.sc_plan_subdomain_costs.argtypes = [_P, _P]
     L.sc_launches_per_assemble.argtypes = [_P]
     L.sc_launches_per_assemble.restype = ctypes.c_int32
@@ -226,10 +226,15 @@ class SCPlan:
         _check(lib().sc_plan_stats(self._h, ctypes.byref(s)))
         return s.as_dict()
 
-    def set_timing_events(self, ev0=None, ev1=None, ev2=None):
-        """torch.cuda.Event objects recorded around the TRSM and SYRK kernels of each assemble."""
-        h = [None if e is None else e.cuda_event for e in (ev0, ev1, ev2)]
-        _check(lib().sc_set_timing_events(self._h, *h))
+    def set_timing_events(self, events=None):
+        """4 torch.cuda.Event objects (already recorded once, so they exist) recorded before prep,
+        after prep, after the TRSM and after the SYRK of each following assemble; None disables."""
+        if not events:
+            _check(lib().sc_set_timing_events(self._h, None, 0))
+            return
+        arr = (_P * 4)(*[e.cuda_event for e in events])
+        self._tev_keep = (events, arr)
+        _check(lib().sc_set_timing_events(self._h, arr, 4))
 
     @property
     def launches_per_assemble(self) -> int:
