@@ -89,6 +89,39 @@ constexpr int kLdT = kMaxPanel + 4;  // smem triangle, column-major [col][row]
 
 constexpr size_t kPrepSmem = 2 * sizeof(double) * kMaxPanel * kLdT;
 
+// Zero the entries of a panel's chunk region that the CSC scatter will not write: everything for
+// a relaxed panel (structural zeros of merged supernodes), only the padding (rows past nR in the
+// last chunk, columns past kw) for a single-supernode panel, whose pruned rows are all present in
+// every column.  Work split over `nthr` threads starting at `t`.
+__device__ __forceinline__ void zero_chunk_gaps(double* PB, const Panel& pn, int t, int nthr) {
+  if (pn.nchunk == 0) return;
+  const int kw4 = pn.kw4;
+  double* c0 = PB + pn.buf_off + (int64_t)pn.ldD * kw4;
+  if (pn.relaxed) {
+    const int64_t len = ((int64_t)(pn.nchunk - 1) * kLdC + pn.ldLast) * kw4;
+    double2* z = reinterpret_cast<double2*>(c0);
+    for (int64_t q = t; q < len / 2; q += nthr) z[q] = make_double2(0.0, 0.0);
+    return;
+  }
+  const int last_rows = pn.nR - (pn.nchunk - 1) * kChunk;
+  for (int ch = 0; ch < pn.nchunk; ch++) {
+    const int ld = (ch == pn.nchunk - 1) ? pn.ldLast : kLdC;
+    const int rows = (ch == pn.nchunk - 1) ? last_rows : kChunk;
+    double* blk = c0 + (int64_t)ch * kLdC * kw4;
+    const int gap = ld - rows;
+    // rows [rows, ld) of columns [0, kw) and all ld rows of columns [kw, kw4)
+    for (int q = t; q < gap * pn.kw + ld * (kw4 - pn.kw); q += nthr) {
+      if (q < gap * pn.kw) {
+        const int c = q / gap;
+        blk[(int64_t)c * ld + rows + (q - c * gap)] = 0.0;
+      } else {
+        const int q2 = q - gap * pn.kw;
+        blk[(int64_t)(pn.kw + q2 / ld) * ld + (q2 % ld)] = 0.0;
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
   extern __shared__ __align__(16) unsigned char prep_smem[];
   double* D = reinterpret_cast<double*>(prep_smem);  // triangle, then temporaries
@@ -108,13 +141,7 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
     double2* D2 = reinterpret_cast<double2*>(D);
     for (int q = tid; q < npad * kLdT / 2; q += kThreads) D2[q] = make_double2(0.0, 0.0);
   }
-  // zero the chunk region (structural zeros of relaxed panels + padding)
-  {
-    const int64_t c0 = pn.buf_off + (int64_t)pn.ldD * kw4;
-    const int64_t len = (pn.nchunk > 0) ? ((int64_t)(pn.nchunk - 1) * block_ld(kChunk) + pn.ldLast) * kw4 : 0;
-    double2* z = reinterpret_cast<double2*>(PB + c0);
-    for (int64_t q = tid; q < len / 2; q += kThreads) z[q] = make_double2(0.0, 0.0);
-  }
+  zero_chunk_gaps(PB, pn, tid, kThreads);
   __syncthreads();
   for (int64_t q = pn.csc_begin + tid; q < pn.csc_end; q += kThreads) {
     const double v = Lv[q];
@@ -215,12 +242,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps) prep_small_kernel(DevPlan P)
   int npad = 8;
   while (npad < kw) npad *= 2;
   for (int q = lane; q < npad * kLdS / 2; q += 32) reinterpret_cast<double2*>(D)[q] = make_double2(0.0, 0.0);
-  {
-    const int64_t c0 = pn.buf_off + (int64_t)pn.ldD * kw4;
-    const int64_t len = (pn.nchunk > 0) ? ((int64_t)(pn.nchunk - 1) * kLdC + pn.ldLast) * kw4 : 0;
-    double2* z = reinterpret_cast<double2*>(PB + c0);
-    for (int64_t q = lane; q < len / 2; q += 32) z[q] = make_double2(0.0, 0.0);
-  }
+  zero_chunk_gaps(PB, pn, lane, 32);
   __syncwarp();
   for (int64_t q = pn.csc_begin + lane; q < pn.csc_end; q += 32) {
     const double v = Lv[q];
@@ -297,11 +319,22 @@ static_assert(kLdC == block_ld(kChunk), "chunk ld");
 
 template <int T>
 struct TileCfg {
-  static constexpr int LDX = T + 4;             // strip row stride (conflict-free fragment loads)
+  static constexpr int LDX = strip_ld(T);       // strip / Y row stride in doubles
   static constexpr int NB = T / 8;              // 8-wide column blocks
   static constexpr int WN = NB < 2 ? NB : 2;    // column blocks per warp
   static constexpr int NWC = NB / WN;           // warps along the columns
   static constexpr int WM = NWC;                // row blocks per warp: (8/NWC) warp rows x WM = 8
+  // Column swizzle of the unpadded strip (T >= 16): word (row, col) lives at row*T + (col ^ swz(row))
+  // with swz = 0, 8, 4, 12 for row & 3 = 0..3.  DMMA B-fragment loads (rows k..k+3 x 8 columns)
+  // and the 16-byte C-fragment stores (rows g, g+1 x 8 columns) are then bank-conflict free.
+  // T == 8 keeps a padded stride of 12 (== 12 mod 16) instead.
+  static __device__ __forceinline__ int idx(int row, int col) {
+    if constexpr (T >= 16) {
+      return row * LDX + (col ^ (((row & 1) << 3) | ((row & 2) << 1)));
+    } else {
+      return row * LDX + col;
+    }
+  }
 };
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
@@ -342,7 +375,7 @@ __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, c
           ok = true;
         } else if (inflight < kSlots) {
           if (ring_tail > ring_head) {
-            if (kRingBytes - ring_tail >= bytes) {
+            if (P.ring_bytes - ring_tail >= bytes) {
               start = ring_tail;
               ok = true;
             } else if (ring_head >= bytes) {
@@ -380,8 +413,9 @@ template <int T>
 __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
   using Cfg = TileCfg<T>;
   constexpr int LDX = Cfg::LDX, WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC;
+  constexpr int KS = kMaxPanel / 4;  // k steps of 4 in a full panel
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const TrsmSmem L = trsm_smem_layout(T, P.max_n, P.strip_cap);
+  const TrsmSmem L = trsm_smem_layout(T, P.ring_bytes, P.strip_cap);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem_raw + L.empty);
   int32_t* off = reinterpret_cast<int32_t*>(smem_raw + L.off);
@@ -420,40 +454,53 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
   consumer_sync();
   for (int q = tile.binit_begin + tid; q < tile.binit_end; q += kThreads) {
     const BInit bi = P.binit[q];
-    Xs[bi.strip_row * LDX + bi.col] = bi.val;
+    Xs[Cfg::idx(bi.strip_row, bi.col)] = bi.val;
   }
   consumer_sync();
 
   // ---- stepped supernodal TRSM (row a3); two consumer barriers per factor panel
   int b = 0;  // block counter (same order as the producer)
+  Step st_next = P.steps[tile.step_begin < tile.step_end ? tile.step_begin : 0];
+  Panel pn_next = P.panels[st_next.panel];
   for (int s = tile.step_begin; s < tile.step_end; s++, b++) {
-    const Step st = P.steps[s];
-    const Panel pn = P.panels[st.panel];
+    const Step st = st_next;
+    const Panel pn = pn_next;
+    if (s + 1 < tile.step_end) {  // descriptors of the next panel, off the critical path
+      st_next = P.steps[s + 1];
+      pn_next = P.panels[st_next.panel];
+    }
     const int kw = pn.kw, kw4 = pn.kw4;
-    double* Xp = Xs + st.strip_row * LDX;
-    double yacc[WM][WN][2], acc[WM][WN][2];
-    // Y = inv(L_pp) X_p  (inv(L_pp) lower triangular: row block i needs k < 8 (i + 1))
+    const int row0 = st.strip_row;
+    // Y = inv(L_pp) X_p  (inv(L_pp) lower triangular: row block i needs k < 8 (i + 1)); two
+    // accumulators per output block (even / odd k steps) for DMMA latency hiding
+    double yacc[WM][WN][2];
     {
+      double ya[2][WM][WN][2];
+#pragma unroll
+      for (int h = 0; h < 2; h++)
+#pragma unroll
+        for (int i = 0; i < WM; i++)
+#pragma unroll
+          for (int j = 0; j < WN; j++) ya[h][i][j][0] = ya[h][i][j][1] = 0.0;
       const int slot = b % kSlots;
       mbar_wait(&full[slot], (uint32_t)(b / kSlots) & 1u);
       const double* A = reinterpret_cast<const double*>(ring + off[slot]);
       const int ld = pn.ldD;
-#pragma unroll
-      for (int i = 0; i < WM; i++)
-#pragma unroll
-        for (int j = 0; j < WN; j++) yacc[i][j][0] = yacc[i][j][1] = 0.0;
       const int kend = min(kw4, (br0 + WM) * 8);
       if (br0 * 8 < kw4) {
-        for (int k = 0; k < kend; k += 4) {
-          double a[WM], bb[WN];
 #pragma unroll
-          for (int i = 0; i < WM; i++) a[i] = A[(k + t4) * ld + (br0 + i) * 8 + g];
+        for (int ks = 0; ks < KS; ks++) {
+          if (4 * ks < kend) {
+            double a[WM], bb[WN];
 #pragma unroll
-          for (int j = 0; j < WN; j++) bb[j] = Xp[(k + t4) * LDX + (bc0 + j) * 8 + g];
+            for (int i = 0; i < WM; i++) a[i] = A[(4 * ks + t4) * ld + (br0 + i) * 8 + g];
 #pragma unroll
-          for (int i = 0; i < WM; i++)
+            for (int j = 0; j < WN; j++) bb[j] = Xs[Cfg::idx(row0 + 4 * ks + t4, (bc0 + j) * 8 + g)];
 #pragma unroll
-            for (int j = 0; j < WN; j++) dmma(yacc[i][j][0], yacc[i][j][1], a[i], bb[j]);
+            for (int i = 0; i < WM; i++)
+#pragma unroll
+              for (int j = 0; j < WN; j++) dmma(ya[ks & 1][i][j][0], ya[ks & 1][i][j][1], a[i], bb[j]);
+          }
         }
       }
       __syncwarp();
@@ -461,10 +508,12 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
 #pragma unroll
       for (int i = 0; i < WM; i++) {
         const int r = (br0 + i) * 8 + g;
-        if (r < kw4) {
 #pragma unroll
-          for (int j = 0; j < WN; j++)
-            *reinterpret_cast<double2*>(Ys + r * LDX + (bc0 + j) * 8 + 2 * t4) =
+        for (int j = 0; j < WN; j++) {
+          yacc[i][j][0] = ya[0][i][j][0] + ya[1][i][j][0];
+          yacc[i][j][1] = ya[0][i][j][1] + ya[1][i][j][1];
+          if (r < kw4)
+            *reinterpret_cast<double2*>(Ys + Cfg::idx(r, (bc0 + j) * 8 + 2 * t4)) =
                 make_double2(yacc[i][j][0], yacc[i][j][1]);
         }
       }
@@ -473,11 +522,11 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
     // X[R_p] -= L[R_p, p] Y, one 64-row chunk (one ring block) at a time; chunks update disjoint
     // rows and each warp releases its ring slot itself, so no barrier between chunks.  The warp's
     // Y fragments stay in registers for all chunks of the panel: only L is read from shared memory.
-    double yf[kMaxPanel / 4][WN];
+    double yf[KS][WN];
 #pragma unroll
-    for (int ks = 0; ks < kMaxPanel / 4; ks++)
+    for (int ks = 0; ks < KS; ks++)
 #pragma unroll
-      for (int j = 0; j < WN; j++) yf[ks][j] = (4 * ks < kw4) ? Ys[(4 * ks + t4) * LDX + (bc0 + j) * 8 + g] : 0.0;
+      for (int j = 0; j < WN; j++) yf[ks][j] = (4 * ks < kw4) ? Ys[Cfg::idx(4 * ks + t4, (bc0 + j) * 8 + g)] : 0.0;
     for (int c = 0; c < pn.nchunk; c++) {
       b++;
       const int rows_c = min(kChunk, pn.nR - c * kChunk);
@@ -488,13 +537,19 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
       int sr[WM];
 #pragma unroll
       for (int i = 0; i < WM; i++) sr[i] = (int)srow[slot * kChunk + (br0 + i) * 8 + g];
+      // KSPLIT independent accumulators per output block (k steps round-robin) keep enough DMMA
+      // chains in flight per warp
+      constexpr int KSPLIT = (WM * WN <= 2) ? 4 : 2;
+      double acc[KSPLIT][WM][WN][2];
       if (br0 * 8 < rows_c) {
 #pragma unroll
-        for (int i = 0; i < WM; i++)
+        for (int h = 0; h < KSPLIT; h++)
 #pragma unroll
-          for (int j = 0; j < WN; j++) acc[i][j][0] = acc[i][j][1] = 0.0;
+          for (int i = 0; i < WM; i++)
 #pragma unroll
-        for (int ks = 0; ks < kMaxPanel / 4; ks++) {
+            for (int j = 0; j < WN; j++) acc[h][i][j][0] = acc[h][i][j][1] = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ks++) {
           if (4 * ks < kw4) {
             double a[WM];
 #pragma unroll
@@ -502,7 +557,8 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
 #pragma unroll
             for (int i = 0; i < WM; i++)
 #pragma unroll
-              for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], yf[ks][j]);
+              for (int j = 0; j < WN; j++)
+                dmma(acc[ks % KSPLIT][i][j][0], acc[ks % KSPLIT][i][j][1], a[i], yf[ks][j]);
           }
         }
       }
@@ -514,10 +570,16 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
           if (sr[i] == 0xFFFF) continue;  // row outside this tile's reach (or padding): update is 0
 #pragma unroll
           for (int j = 0; j < WN; j++) {
-            double2* p = reinterpret_cast<double2*>(Xs + sr[i] * LDX + (bc0 + j) * 8 + 2 * t4);
+            double s0 = acc[0][i][j][0], s1 = acc[0][i][j][1];
+#pragma unroll
+            for (int h = 1; h < KSPLIT; h++) {
+              s0 += acc[h][i][j][0];
+              s1 += acc[h][i][j][1];
+            }
+            double2* p = reinterpret_cast<double2*>(Xs + Cfg::idx(sr[i], (bc0 + j) * 8 + 2 * t4));
             double2 v = *p;
-            v.x -= acc[i][j][0];
-            v.y -= acc[i][j][1];
+            v.x -= s0;
+            v.y -= s1;
             *p = v;
           }
         }
@@ -530,7 +592,8 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
       if (r < kw) {
 #pragma unroll
         for (int j = 0; j < WN; j++)
-          *reinterpret_cast<double2*>(Xp + r * LDX + (bc0 + j) * 8 + 2 * t4) = make_double2(yacc[i][j][0], yacc[i][j][1]);
+          *reinterpret_cast<double2*>(Xs + Cfg::idx(row0 + r, (bc0 + j) * 8 + 2 * t4)) =
+              make_double2(yacc[i][j][0], yacc[i][j][1]);
       }
     }
     consumer_sync();  // strip updates visible before the next panel reads its rows; Ys reusable
@@ -544,7 +607,7 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
     for (int q = tid; q < ws.len * (T / 2); q += kThreads) {
       const int r = q / (T / 2), j = 2 * (q - r * (T / 2));
       double2 v = make_double2(0.0, 0.0);
-      if (ws.src >= 0) v = *reinterpret_cast<const double2*>(Xs + (ws.src + r) * LDX + j);
+      if (ws.src >= 0) v = *reinterpret_cast<const double2*>(Xs + Cfg::idx(ws.src + r, j));
       *reinterpret_cast<double2*>(Xg + (int64_t)(ws.dst + r) * P.G + j) = v;
     }
   }
@@ -674,64 +737,60 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P) {
 // ------------------------------------------------------------------------------------------------
 // Apply: y_i = F'_i x_i (x_i(a) = lambda[slm_i(a)]) from the lower triangle; deterministic sum.
 // ------------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) apply_partial_kernel(DevPlan P, const double* __restrict__ lambda) {
-  __shared__ double xs[32];
-  __shared__ double zred[kThreads / 32][32];
+// One 64 x 64 tile (rb >= cb) of the lower F' per CTA, read once from HBM: u = F'_tile x_cols
+// (row partial sums) and v = F'_tile^T x_rows (column partial sums; strictly lower part on the
+// diagonal tiles, F' above its diagonal is never written and stays 0).  y = sum of the partials of
+// a row's tiles, in a fixed order (deterministic, no atomics).
+__device__ __forceinline__ int64_t apply_tile_index(int rb, int cb) { return (int64_t)rb * (rb + 1) / 2 + cb; }
+
+__global__ void __launch_bounds__(kThreads) apply_tile_kernel(DevPlan P, const double* __restrict__ lambda) {
+  constexpr int AT = kApplyTile;
+  __shared__ double Ft[AT][AT + 1];
+  __shared__ double xr[AT], xc[AT];
   const ApplyTask task = P.apply_tasks[blockIdx.x];
-  const int sub = task.sub, b0 = task.b0;
+  const int sub = task.sub, rb = task.rb, cb = task.cb;
   const int m = P.sub_m[sub];
-  const int nb = min(32, m - b0);
+  const int r0 = rb * AT, c0 = cb * AT;
+  const int nr = min(AT, m - r0), nc = min(AT, m - c0);
   const double* __restrict__ F = P.F + P.sub_F_base[sub];
-  const int64_t* slm = P.slm + P.sub_slm_off[sub];
-  double* part = P.part + P.sub_part_off[sub] + (int64_t)(b0 / 32) * m;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < 32) xs[tid] = (tid < nb) ? lambda[slm[b0 + tid]] : 0.0;
-  __syncthreads();
-  double z[32];
-#pragma unroll
-  for (int j = 0; j < 32; j++) z[j] = 0.0;
-  for (int a = b0 + tid; a < m; a += kThreads) {
-    const double xa = lambda[slm[a]];
-    double w = 0.0;
-#pragma unroll
-    for (int j = 0; j < 32; j++) {
-      if (j < nb) {
-        const int b = b0 + j;
-        if (a >= b) {
-          const double f = F[(int64_t)b * m + a];
-          z[j] = fma(f, xa, z[j]);        // column dot: (F' x) contribution to row b
-          if (a > b) w = fma(f, xs[j], w);  // row a contribution from column b
-        }
-      }
-    }
-    part[a] = w;
-  }
-#pragma unroll
-  for (int j = 0; j < 32; j++) {
-    double v = z[j];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if (lane == 0) zred[warp][j] = v;
+  const int64_t* __restrict__ slm = P.slm + P.sub_slm_off[sub];
+  const int tid = threadIdx.x;
+  if (tid < AT) xr[tid] = (tid < nr) ? lambda[slm[r0 + tid]] : 0.0;
+  else if (tid < 2 * AT) xc[tid - AT] = (tid - AT < nc) ? lambda[slm[c0 + tid - AT]] : 0.0;
+  for (int q = tid; q < AT * AT; q += kThreads) {
+    const int c = q / AT, r = q - c * AT;
+    Ft[r][c] = (r < nr && c < nc) ? F[(int64_t)(c0 + c) * m + (r0 + r)] : 0.0;
   }
   __syncthreads();
-  if (tid < nb) {
+  double* part = P.part + P.sub_part_off[sub] + apply_tile_index(rb, cb) * 2 * AT;
+  const bool diag = (rb == cb);
+  if (tid < AT) {
+    double u = 0.0;
+#pragma unroll 8
+    for (int c = 0; c < AT; c++) u = fma(Ft[tid][c], xc[c], u);
+    part[tid] = u;
+  } else if (tid < 2 * AT) {
+    const int c = tid - AT;
     double v = 0.0;
-#pragma unroll
-    for (int w = 0; w < kThreads / 32; w++) v += zred[w][tid];
-    part[b0 + tid] += v;
+#pragma unroll 8
+    for (int r = 0; r < AT; r++) v = (diag && r <= c) ? v : fma(Ft[r][c], xr[r], v);
+    part[AT + c] = v;
   }
 }
 
 __global__ void __launch_bounds__(kThreads) apply_scatter_kernel(DevPlan P, double* __restrict__ q, int64_t nl) {
+  constexpr int AT = kApplyTile;
   const int64_t gidx = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (gidx >= nl) return;
   double s = 0.0;
   for (int64_t p = P.qg_ptr[gidx]; p < P.qg_ptr[gidx + 1]; p++) {
     const int64_t sa = P.qg_sub_a[p];
     const int sub = (int)(sa >> 32), a = (int)(sa & 0xffffffff);
-    const int m = P.sub_m[sub];
+    const int nab = (P.sub_m[sub] + AT - 1) / AT;
     const double* part = P.part + P.sub_part_off[sub];
-    for (int blk = 0; blk <= a / 32; blk++) s += part[(int64_t)blk * m + a];
+    const int b = a / AT, r = a - b * AT;
+    for (int cb = 0; cb <= b; cb++) s += part[apply_tile_index(b, cb) * 2 * AT + r];           // row sums
+    for (int rb = b; rb < nab; rb++) s += part[apply_tile_index(rb, b) * 2 * AT + AT + r];    // column sums
   }
   q[gidx] = s;
 }
@@ -853,7 +912,13 @@ sc_status upload_plan(Plan& P, std::string& err) {
   D.T = P.T;
   D.strip_cap = P.max_strip_rows;
   D.G = P.G;
-  P.smem_trsm = trsm_smem_layout(P.T, P.max_n, P.max_strip_rows).total;
+  D.ring_bytes = P.ring_bytes;
+  if (P.ring_bytes <= 0) {
+    err = "X strip of " + std::to_string(P.max_strip_rows) + " rows x " + std::to_string(P.T) +
+          " columns leaves no room for the L-block ring in shared memory; use smaller tile_cols";
+    return SC_ERR_INVALID_ARG;
+  }
+  P.smem_trsm = trsm_smem_layout(P.T, P.ring_bytes, P.max_strip_rows).total;
   int dev_smem = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.opt.device));
   if (P.smem_trsm > (size_t)dev_smem) {
@@ -980,7 +1045,7 @@ sc_status launch_apply(Plan& P, const double* lambda, double* q, void* stream_v,
   P.last_stream = stream_v;
   const int na = (int)P.apply_tasks.size();
   if (na > 0) {
-    apply_partial_kernel<<<na, kThreads, 0, stream>>>(P.dev, lambda);
+    apply_tile_kernel<<<na, kThreads, 0, stream>>>(P.dev, lambda);
     CUDA_TRY(cudaGetLastError());
   }
   if (P.n_lambda > 0) {

@@ -168,7 +168,7 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
   const double zmax = relax_zmax();
   const int wsmall = relax_wsmall();
   struct Open {
-    int32_t a = -1, b = -1;
+    int32_t a = -1, b = -1, merged = 0;
     std::vector<int32_t> R;
     double nnz = 0;
   } open;
@@ -178,6 +178,7 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     Panel p{};
     p.a = open.a;
     p.kw = open.b - open.a;
+    p.relaxed = open.merged;
     p.nR = (int32_t)open.R.size();
     p.R_off = (int32_t)C.Rrows.size();
     C.Rrows.insert(C.Rrows.end(), open.R.begin(), open.R.end());
@@ -227,6 +228,7 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
         open.b = c1;
         open.R.swap(R2);
         open.nnz = nnz2;
+        open.merged = 1;
         continue;
       }
       close_open();
@@ -557,13 +559,22 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     }
     return SC_OK;
   };
-  // TRSM tile width: the widest of 32 / 16 / 8 whose largest X strip fits in shared memory
-  int32_t max_n = 0;
-  for (int32_t i = 0; i < nsub; i++) max_n = std::max(max_n, sd[i].n);
-  auto fits = [&](int T) {
+  // TRSM tile width: the widest of 32 / 16 / 8 whose largest X strip fits in shared memory next to
+  // an L-block ring of at least two of the plan's largest blocks; the ring gets what is left (up
+  // to 160 KB) so the producer can run ahead
+  auto ring_for = [&](int T) -> int64_t {
     int32_t mx = 0;
-    for (auto& C : P.classes) mx = std::max(mx, C.max_strip_rows);
-    return trsm_smem_layout(T, max_n, mx).total <= kSmemBudget;
+    int64_t maxblk = 16;
+    for (auto& C : P.classes) {
+      mx = std::max(mx, C.max_strip_rows);
+      for (auto& p : C.panels) {
+        maxblk = std::max<int64_t>(maxblk, (int64_t)p.ldD * p.kw4 * 8);
+        if (p.nchunk > 0) maxblk = std::max<int64_t>(maxblk, (int64_t)(p.nchunk > 1 ? kLdC : p.ldLast) * p.kw4 * 8);
+      }
+    }
+    const int64_t fixed = (int64_t)trsm_smem_layout(T, 0, mx).total;
+    int64_t ring = std::min<int64_t>(kRingMaxBytes, (int64_t)kSmemBudget - fixed) & ~(int64_t)127;
+    return ring >= 2 * maxblk ? ring : -1;
   };
   if (opt.tile_cols) {
     sc_status st = analyse_all(opt.tile_cols);
@@ -573,10 +584,11 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     for (int k = 0; k < 3; k++) {
       sc_status st = analyse_all(cand[k]);
       if (st != SC_OK) return st;
-      if (fits(cand[k])) break;
+      if (ring_for(cand[k]) > 0) break;
     }
   }
   for (auto& C : P.classes) P.max_strip_rows = std::max(P.max_strip_rows, C.max_strip_rows);
+  P.ring_bytes = (int32_t)std::max<int64_t>(ring_for(P.T), 0);
 
   // --- global concatenation: class-local indices -> global
   int64_t srow_base = 0;
@@ -650,14 +662,16 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     P.sub_PB_base.push_back(P.PB_doubles);
     P.PB_doubles += C.pb_doubles;
     P.sub_part_off.push_back(P.part_doubles);
-    P.part_doubles += (int64_t)((C.m + 31) / 32) * C.m;
+    const int32_t nab = (C.m + kApplyTile - 1) / kApplyTile;  // apply tiles: nab (nab + 1) / 2
+    P.part_doubles += (int64_t)nab * (nab + 1) / 2 * 2 * kApplyTile;
     for (size_t q = 0; q < C.panels.size(); q++)
       (C.panels[q].kw > kSmallPanel ? P.prep_tasks : P.prep_small_tasks)
           .push_back({i, P.cls_panel_begin[(size_t)cls] + (int32_t)q});
     for (size_t t = 0; t < C.tiles.size(); t++)
       if (C.tiles[t].width > 0) P.trsm_tasks.push_back({i, P.cls_tile_begin[(size_t)cls] + (int32_t)t});
     for (size_t q = 0; q < C.pairs.size(); q++) P.syrk_tasks.push_back({i, P.cls_pair_begin[(size_t)cls] + (int32_t)q});
-    for (int32_t b = 0; b < C.m; b += 32) P.apply_tasks.push_back({i, b});
+    for (int32_t rb = 0; rb < nab; rb++)
+      for (int32_t cb = 0; cb <= rb; cb++) P.apply_tasks.push_back({i, rb, cb, 0});
     P.sub_slm_off.push_back((int64_t)P.slm.size());
     if (sd[i].lambda_map) {
       for (int32_t a = 0; a < C.m; a++) {

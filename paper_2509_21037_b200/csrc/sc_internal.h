@@ -24,32 +24,35 @@ constexpr int kSmallPanel = 32; // panels up to this width are prepared by one w
 // Leading dimension (in doubles) of a staged block holding `rows` rows: the smallest value
 // >= rows that is == 4 (mod 16), so DMMA fragment loads (4 consecutive k x 8 consecutive rows)
 // hit 16 distinct 8-byte bank pairs.
-SC_HD constexpr int block_ld(int rows) { return rows <= 4 ? 4 : 4 + 16 * ((rows - 4 + 15) / 16); }
+// (ld == 4 (mod 8) suffices: for t = 0..3 and 4 consecutive rows, ld*t + row covers 16 banks.)
+SC_HD constexpr int block_ld(int rows) { return rows <= 4 ? 4 : 4 + 8 * ((rows - 4 + 7) / 8); }
 
 constexpr int kLdC = 68;                        // block_ld(kChunk): ld of a full 64-row chunk
 constexpr size_t kSmemBudget = 232448;          // B200 max dynamic shared memory per block (227 KB)
-constexpr int kSlots = 8;                       // TRSM L-block pipeline depth (mbarrier pairs)
-constexpr int kRingBytes = 73728;               // TRSM L-block ring (holds >= 2 full 68x64 blocks)
+constexpr int kSlots = 16;                      // TRSM L-block pipeline depth (mbarrier pairs)
+constexpr int kRingMaxBytes = 163840;           // TRSM L-block ring: at most 160 KB ...
+constexpr int kBlockMaxBytes = kLdC * kMaxPanel * 8;  // ... and at least 2 of the largest blocks
 constexpr int kTrsmThreads = kThreads + 32;     // 8 consumer warps + 1 TMA producer warp
 
 // Byte offsets of the TRSM kernel's dynamic shared memory: full/empty mbarriers and ring offsets
 // of the L-block pipeline, per-slot strip rows of a chunk's R_p rows (uint16, copied with the
-// block), the byte ring of L blocks, the solved panel Y (64 x T+4) and the X strip
-// ((strip_cap + 4) rows of T + 4 doubles).
+// block), the byte ring of L blocks (ring_bytes, sized by the planner from what the strip leaves
+// free), the solved panel Y (64 x ld) and the X strip ((strip_cap + 4) rows of ld doubles).
 struct TrsmSmem {
   size_t full, empty, off, srow, ring, ys, strip, total;
 };
-SC_HD inline TrsmSmem trsm_smem_layout(int T, int max_n, int strip_cap) {
-  (void)max_n;
+// Row stride of the shared-memory strip: T (column-swizzled) for T >= 16, T + 4 for T = 8.
+SC_HD constexpr int strip_ld(int T) { return T >= 16 ? T : T + 4; }
+SC_HD inline TrsmSmem trsm_smem_layout(int T, int ring_bytes, int strip_cap) {
   TrsmSmem s{};
   s.full = 0;
   s.empty = 8 * kSlots;
   s.off = 16 * kSlots;
-  s.srow = 256;
+  s.srow = 512;
   s.ring = s.srow + sizeof(uint16_t) * kSlots * kChunk;
-  s.ys = s.ring + (size_t)kRingBytes;
-  s.strip = s.ys + sizeof(double) * (size_t)kMaxPanel * (size_t)(T + 4);
-  s.total = s.strip + sizeof(double) * (size_t)(strip_cap + 4) * (size_t)(T + 4);
+  s.ys = s.ring + (size_t)ring_bytes;
+  s.strip = s.ys + sizeof(double) * (size_t)kMaxPanel * (size_t)strip_ld(T);
+  s.total = s.strip + sizeof(double) * (size_t)(strip_cap + 4) * (size_t)strip_ld(T);
   return s;
 }
 
@@ -64,6 +67,7 @@ struct Panel {
   int32_t R_off, nchunk, ldD, ldLast;   // ldLast = ld of the last chunk
   int64_t buf_off;                      // doubles from the subdomain's panel-buffer base
   int64_t csc_begin, csc_end;           // L entries of columns [a, a+kw) in CSC order
+  int32_t relaxed, pad;                 // relaxed: merged supernodes (structural zeros inside)
 };
 
 // One RHS column tile of TRSM width T of one pattern class: stepped columns [col0, col0+width)
@@ -124,8 +128,10 @@ struct I2 {
   int32_t x, y;
 };
 
+// Apply: one 64 x 64 tile (row block rb >= column block cb) of the lower F' of subdomain sub.
+constexpr int kApplyTile = 64;
 struct ApplyTask {
-  int32_t sub, b0;                 // columns [b0, b0+32) of subdomain sub
+  int32_t sub, rb, cb, pad;
 };
 
 // Symbolic plan of one pattern class (subdomains with identical L pattern, perm and B~^T).
@@ -196,11 +202,12 @@ struct DevPlan {
   double* part;
   unsigned long long* err;         // sticky device error: ((sub+1) << 32) | col
   int32_t nsub, max_n, T, G, strip_cap;  // strip_cap: rows of the shared-memory strip
+  int32_t ring_bytes;                    // TRSM L-block ring size
 };
 
 struct Plan {
   sc_options opt{};
-  int32_t T = 32, G = 64, PW = 64;
+  int32_t T = 32, G = 64, PW = 64, ring_bytes = 0;
   int32_t nsub = 0;
   std::vector<ClassPlan> classes;
   std::vector<int32_t> sub_cls;
