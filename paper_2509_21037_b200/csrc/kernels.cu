@@ -89,6 +89,37 @@ constexpr int kLdT = kMaxPanel + 4;  // smem triangle, column-major [col][row]
 
 constexpr size_t kPrepSmem = 2 * sizeof(double) * kMaxPanel * kLdT;
 
+// Scatter the CSC values of a panel's columns: diagonal-block entries into the smem triangle D
+// (column-major, stride LDD), pruned rows into the panel buffer.  Four loads in flight per thread.
+template <int LDD>
+__device__ __forceinline__ void scatter_panel(const double* __restrict__ Lv, const int32_t* __restrict__ dest,
+                                              double* __restrict__ PB, double* D, const Panel& pn, int t, int nthr) {
+  constexpr int U = 4;
+  for (int64_t q0 = pn.csc_begin + t; q0 < pn.csc_end; q0 += (int64_t)U * nthr) {
+    double v[U];
+    int32_t d[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      const int64_t q = q0 + (int64_t)u * nthr;
+      d[u] = INT32_MIN;
+      if (q < pn.csc_end) {
+        v[u] = __ldg(Lv + q);
+        d[u] = __ldg(dest + q);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+      if (d[u] == INT32_MIN) continue;
+      if (d[u] < 0) {
+        const int idx = -1 - d[u];
+        D[(idx >> 6) * LDD + (idx & 63)] = v[u];
+      } else {
+        PB[d[u]] = v[u];
+      }
+    }
+  }
+}
+
 // Zero the entries of a panel's chunk region that the CSC scatter will not write: everything for
 // a relaxed panel (structural zeros of merged supernodes), only the padding (rows past nR in the
 // last chunk, columns past kw) for a single-supernode panel, whose pruned rows are all present in
@@ -143,16 +174,7 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
   }
   zero_chunk_gaps(PB, pn, tid, kThreads);
   __syncthreads();
-  for (int64_t q = pn.csc_begin + tid; q < pn.csc_end; q += kThreads) {
-    const double v = Lv[q];
-    const int32_t d = dest[q];
-    if (d < 0) {
-      const int idx = -1 - d;
-      D[(idx >> 6) * kLdT + (idx & 63)] = v;
-    } else {
-      PB[d] = v;
-    }
-  }
+  scatter_panel<kLdT>(Lv, dest, PB, D, pn, tid, kThreads);
   // unit diagonal in the padding (its inverse stays the identity)
   for (int i = kw + tid; i < npad; i += kThreads) D[i * kLdT + i] = 1.0;
   __syncthreads();
@@ -244,16 +266,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps) prep_small_kernel(DevPlan P)
   for (int q = lane; q < npad * kLdS / 2; q += 32) reinterpret_cast<double2*>(D)[q] = make_double2(0.0, 0.0);
   zero_chunk_gaps(PB, pn, lane, 32);
   __syncwarp();
-  for (int64_t q = pn.csc_begin + lane; q < pn.csc_end; q += 32) {
-    const double v = Lv[q];
-    const int32_t d = dest[q];
-    if (d < 0) {
-      const int idx = -1 - d;
-      D[(idx >> 6) * kLdS + (idx & 63)] = v;
-    } else {
-      PB[d] = v;
-    }
-  }
+  scatter_panel<kLdS>(Lv, dest, PB, D, pn, lane, 32);
   for (int i = kw + lane; i < npad; i += 32) D[i * kLdS + i] = 1.0;
   __syncwarp();
   {  // level 0: lane -> (8x8 block lane/8, column lane%8)
@@ -321,7 +334,9 @@ template <int T>
 struct TileCfg {
   static constexpr int LDX = strip_ld(T);       // strip / Y row stride in doubles
   static constexpr int NB = T / 8;              // 8-wide column blocks
-  static constexpr int WN = NB < 2 ? NB : 2;    // column blocks per warp
+  // column blocks per warp: 1 for T <= 16 (keeps the register-resident Y fragments small; the
+  // 288-thread CTA is register-allocated as 384 threads, i.e. at most 168 registers per thread)
+  static constexpr int WN = (T <= 16) ? 1 : 2;
   static constexpr int NWC = NB / WN;           // warps along the columns
   static constexpr int WM = NWC;                // row blocks per warp: (8/NWC) warp rows x WM = 8
   // Column swizzle of the unpadded strip (T >= 16): word (row, col) lives at row*T + (col ^ swz(row))
@@ -487,6 +502,11 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
       const double* A = reinterpret_cast<const double*>(ring + off[slot]);
       const int ld = pn.ldD;
       const int kend = min(kw4, (br0 + WM) * 8);
+      // rows row0 + 4 ks + t4 all share (row & 3), hence one swizzled column per j
+      const double* xb = Xs + (row0 + t4) * LDX;
+      int xcol[WN];
+#pragma unroll
+      for (int j = 0; j < WN; j++) xcol[j] = Cfg::idx(row0 + t4, (bc0 + j) * 8 + g) - (row0 + t4) * LDX;
       if (br0 * 8 < kw4) {
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) {
@@ -495,7 +515,7 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
 #pragma unroll
             for (int i = 0; i < WM; i++) a[i] = A[(4 * ks + t4) * ld + (br0 + i) * 8 + g];
 #pragma unroll
-            for (int j = 0; j < WN; j++) bb[j] = Xs[Cfg::idx(row0 + 4 * ks + t4, (bc0 + j) * 8 + g)];
+            for (int j = 0; j < WN; j++) bb[j] = xb[(4 * ks) * LDX + xcol[j]];
 #pragma unroll
             for (int i = 0; i < WM; i++)
 #pragma unroll
@@ -524,9 +544,11 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
     // Y fragments stay in registers for all chunks of the panel: only L is read from shared memory.
     double yf[KS][WN];
 #pragma unroll
-    for (int ks = 0; ks < KS; ks++)
+    for (int j = 0; j < WN; j++) {
+      const double* yb = Ys + Cfg::idx(t4, (bc0 + j) * 8 + g);  // rows 4 ks + t4 share the swizzle
 #pragma unroll
-      for (int j = 0; j < WN; j++) yf[ks][j] = (4 * ks < kw4) ? Ys[Cfg::idx(4 * ks + t4, (bc0 + j) * 8 + g)] : 0.0;
+      for (int ks = 0; ks < KS; ks++) yf[ks][j] = (4 * ks < kw4) ? yb[4 * ks * LDX] : 0.0;
+    }
     for (int c = 0; c < pn.nchunk; c++) {
       b++;
       const int rows_c = min(kChunk, pn.nR - c * kChunk);
