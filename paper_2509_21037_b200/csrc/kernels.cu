@@ -334,11 +334,15 @@ template <int T>
 struct TileCfg {
   static constexpr int LDX = strip_ld(T);       // strip / Y row stride in doubles
   static constexpr int NB = T / 8;              // 8-wide column blocks
-  // column blocks per warp: 1 for T <= 16 (keeps the register-resident Y fragments small; the
-  // 288-thread CTA is register-allocated as 384 threads, i.e. at most 168 registers per thread)
-  static constexpr int WN = (T <= 16) ? 1 : 2;
+  // 8 consumer warps (16 measured slower: 3.0 vs 2.6 ms cfg2, 17.2 vs 15.5 ms cfg3), one column
+  // block each (keeps the register-resident Y fragments small); a 64 x T chunk product is
+  // (8 / warp rows) row blocks per warp
+  static constexpr int NCW = 8;
+  static constexpr int CT = NCW * 32;           // consumer threads
+  static constexpr int WN = 1;                  // column blocks per warp
   static constexpr int NWC = NB / WN;           // warps along the columns
-  static constexpr int WM = NWC;                // row blocks per warp: (8/NWC) warp rows x WM = 8
+  static constexpr int WM = 8 * NWC / NCW;      // row blocks per warp
+  static_assert(WM >= 1 && (NCW / NWC) * WM == 8, "warp tiling must cover 64 rows");
   // Column swizzle of the unpadded strip (T >= 16): word (row, col) lives at row*T + (col ^ swz(row))
   // with swz = 0, 8, 4, 12 for row & 3 = 0..3.  DMMA B-fragment loads (rows k..k+3 x 8 columns)
   // and the 16-byte C-fragment stores (rows g, g+1 x 8 columns) are then bank-conflict free.
@@ -355,8 +359,9 @@ struct TileCfg {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-__device__ __forceinline__ void consumer_sync() {  // named barrier over the 8 consumer warps
-  asm volatile("bar.sync 1, %0;\n" ::"n"(kThreads) : "memory");
+template <int NT>
+__device__ __forceinline__ void consumer_sync() {  // named barrier over the NT consumer threads
+  asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
 }
 
 // Producer (one lane): walks the tile's block stream [inv(L_pp), chunk 0, chunk 1, ...] per step,
@@ -425,9 +430,9 @@ __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, c
 }
 
 template <int T>
-__global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
+__global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPlan P) {
   using Cfg = TileCfg<T>;
-  constexpr int LDX = Cfg::LDX, WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC;
+  constexpr int LDX = Cfg::LDX, WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC, CT = Cfg::CT;
   constexpr int KS = kMaxPanel / 4;  // k steps of 4 in a full panel
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const TrsmSmem L = trsm_smem_layout(T, P.ring_bytes, P.strip_cap);
@@ -448,12 +453,12 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
   if (tid == 0) {
     for (int k = 0; k < kSlots; k++) {
       mbar_init(&full[k], 1);
-      mbar_init(&empty[k], kThreads / 32);
+      mbar_init(&empty[k], Cfg::NCW);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == kThreads / 32) {  // ---- TMA producer warp
+  if (warp == Cfg::NCW) {  // ---- TMA producer warp
     if (lane == 0) trsm_producer(P, tile, PB, ring, full, empty, off, srow);
     return;
   }
@@ -464,14 +469,14 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
   {
     double2* X2 = reinterpret_cast<double2*>(Xs);
     const int nvec = (tile.strip_rows + 4) * LDX / 2;
-    for (int q = tid; q < nvec; q += kThreads) X2[q] = make_double2(0.0, 0.0);
+    for (int q = tid; q < nvec; q += CT) X2[q] = make_double2(0.0, 0.0);
   }
-  consumer_sync();
-  for (int q = tile.binit_begin + tid; q < tile.binit_end; q += kThreads) {
+  consumer_sync<CT>();
+  for (int q = tile.binit_begin + tid; q < tile.binit_end; q += CT) {
     const BInit bi = P.binit[q];
     Xs[Cfg::idx(bi.strip_row, bi.col)] = bi.val;
   }
-  consumer_sync();
+  consumer_sync<CT>();
 
   // ---- stepped supernodal TRSM (row a3); two consumer barriers per factor panel
   int b = 0;  // block counter (same order as the producer)
@@ -537,7 +542,7 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
                 make_double2(yacc[i][j][0], yacc[i][j][1]);
         }
       }
-      consumer_sync();  // Y visible to every warp
+      consumer_sync<CT>();  // Y visible to every warp
     }
     // X[R_p] -= L[R_p, p] Y, one 64-row chunk (one ring block) at a time; chunks update disjoint
     // rows and each warp releases its ring slot itself, so no barrier between chunks.  The warp's
@@ -618,7 +623,7 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
               make_double2(yacc[i][j][0], yacc[i][j][1]);
       }
     }
-    consumer_sync();  // strip updates visible before the next panel reads its rows; Ys reusable
+    consumer_sync<CT>();  // strip updates visible before the next panel reads its rows; Ys reusable
   }
 
   // ---- write the strip into the group strip (row-major, G columns) for the SYRK
@@ -626,7 +631,7 @@ __global__ void __launch_bounds__(kTrsmThreads, 1) trsm_smem_kernel(DevPlan P) {
   double* __restrict__ Xg = P.X + P.sub_X_base[sub] + G.x_off + tile.col_in_group;
   for (int w = tile.wseg_begin; w < tile.wseg_end; w++) {
     const WSeg ws = P.wsegs[w];
-    for (int q = tid; q < ws.len * (T / 2); q += kThreads) {
+    for (int q = tid; q < ws.len * (T / 2); q += CT) {
       const int r = q / (T / 2), j = 2 * (q - r * (T / 2));
       double2 v = make_double2(0.0, 0.0);
       if (ws.src >= 0) v = *reinterpret_cast<const double2*>(Xs + Cfg::idx(ws.src + r, j));
@@ -1015,10 +1020,10 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
   if (P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
   if (ntr > 0) {
     switch (P.T) {
-      case 8: trsm_smem_kernel<8><<<ntr, kTrsmThreads, P.smem_trsm, stream>>>(P.dev); break;
-      case 16: trsm_smem_kernel<16><<<ntr, kTrsmThreads, P.smem_trsm, stream>>>(P.dev); break;
-      case 32: trsm_smem_kernel<32><<<ntr, kTrsmThreads, P.smem_trsm, stream>>>(P.dev); break;
-      default: trsm_smem_kernel<64><<<ntr, kTrsmThreads, P.smem_trsm, stream>>>(P.dev); break;
+      case 8: trsm_smem_kernel<8><<<ntr, TileCfg<8>::CT + 32, P.smem_trsm, stream>>>(P.dev); break;
+      case 16: trsm_smem_kernel<16><<<ntr, TileCfg<16>::CT + 32, P.smem_trsm, stream>>>(P.dev); break;
+      case 32: trsm_smem_kernel<32><<<ntr, TileCfg<32>::CT + 32, P.smem_trsm, stream>>>(P.dev); break;
+      default: trsm_smem_kernel<64><<<ntr, TileCfg<64>::CT + 32, P.smem_trsm, stream>>>(P.dev); break;
     }
     CUDA_TRY(cudaGetLastError());
   }

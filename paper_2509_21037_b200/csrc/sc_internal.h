@@ -32,7 +32,6 @@ constexpr size_t kSmemBudget = 232448;          // B200 max dynamic shared memor
 constexpr int kSlots = 16;                      // TRSM L-block pipeline depth (mbarrier pairs)
 constexpr int kRingMaxBytes = 163840;           // TRSM L-block ring: at most 160 KB ...
 constexpr int kBlockMaxBytes = kLdC * kMaxPanel * 8;  // ... and at least 2 of the largest blocks
-constexpr int kTrsmThreads = kThreads + 32;     // 8 consumer warps + 1 TMA producer warp
 
 // Byte offsets of the TRSM kernel's dynamic shared memory: full/empty mbarriers and ring offsets
 // of the L-block pipeline, per-slot strip rows of a chunk's R_p rows (uint16, copied with the
