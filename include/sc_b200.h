@@ -74,15 +74,21 @@ enum { SC_SKIP_NONE = 0,      /* no B~ sparsity: every column solved from row 0 
        SC_SKIP_EXACT = 2 };   /* elimination-tree reach of each tile's pivots (default; beyond the
                                  paper's envelope, exact structural zeros of L^{-1} B~^T)          */
 
+enum { SC_STRIP_AUTO = 0, SC_STRIP_SHARED = 1, SC_STRIP_GLOBAL = 2 };
+
 typedef struct {
   int32_t precision;         /* 64 (FP64).  Other values -> SC_ERR_INVALID_ARG in this version     */
   int32_t skip;              /* SC_SKIP_*                                                          */
   int32_t tile_cols;         /* T: RHS column-tile width 8, 16, 32 or 64; 0 = automatic (widest whose
-                                X strip fits in shared memory)                                      */
+                                X strip fits in shared memory; 16 for global strips)                */
   int32_t panel_cols;        /* max factor panel width (factor-splitting block), <= 64; 0 = 64      */
   int64_t n_lambda_global;   /* length of the global dual vector used by sc_apply                   */
   int32_t device;            /* CUDA device ordinal; -1 = host-only plan (symbolic + stats only)    */
-  int32_t reserved[7];       /* must be zero                                                        */
+  int32_t x_strip;           /* where a TRSM tile keeps its X strip while it solves: SC_STRIP_AUTO
+                                (shared memory when the largest strip fits next to the L-block
+                                ring, else global), SC_STRIP_SHARED, SC_STRIP_GLOBAL (in place in the
+                                SYRK group strip in HBM/L2; large subdomains, e.g. cfg5)             */
+  int32_t reserved[6];       /* must be zero                                                        */
 } sc_options;
 
 /* Work and size counters (SURVEY.md Appendix A definitions).  flops: 2 per multiply-add, 1 per
@@ -105,7 +111,8 @@ typedef struct {
   double bytes_apply;        /* algorithmic bytes of one sc_apply (F lower read once + vectors)    */
   double bytes_panels;       /* panel buffers (inverted diagonal blocks + pruned row chunks)        */
   int64_t panels;            /* factor panels, summed over subdomains                               */
-  int32_t group_cols, pad0;  /* SYRK output tile width G                                            */
+  int32_t group_cols;        /* SYRK output tile width G                                            */
+  int32_t x_strip;           /* SC_STRIP_SHARED or SC_STRIP_GLOBAL: the mode the plan chose         */
 } sc_stats;
 
 /* Fill `opt` with defaults: precision 64, skip EXACT, tile/panel auto, device 0. */

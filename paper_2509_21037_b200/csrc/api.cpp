@@ -187,7 +187,9 @@ sc_status sc_set_timing_events(sc_plan_t p, void* const* events, int32_t n) {
 
 int32_t sc_launches_per_assemble(sc_plan_t p) {
   if (!p) return 0;
-  return (p->P.prep_tasks.empty() ? 0 : 1) + (p->P.prep_small_tasks.empty() ? 0 : 1) +
+  int small = 0;
+  for (int b = 0; b < 3; b++) small += p->P.small_begin[b + 1] > p->P.small_begin[b] ? 1 : 0;
+  return (p->P.prep_tasks.empty() ? 0 : 1) + small +
          (p->P.trsm_tasks.empty() ? 0 : 1) + (p->P.syrk_tasks.empty() ? 0 : 1);
 }
 

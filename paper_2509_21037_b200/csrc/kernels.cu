@@ -242,18 +242,27 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
 }
 
 
-// Panels of <= kSmallPanel columns: one warp per panel (no CTA barriers), same algorithm.
-constexpr int kLdS = kSmallPanel + 4;              // 36 == 4 (mod 16)
-constexpr int kSmallWarps = 4;
-constexpr size_t kPrepSmallSmem = 2 * sizeof(double) * kSmallPanel * kLdS * kSmallWarps;
+// Panels of <= kSmallPanel columns: one warp per panel (no CTA barriers), same algorithm.  One
+// instantiation per padded width NPAD = 8 / 16 / 32 (the planner buckets the tasks), so the
+// shared memory per warp is sized to the panel and many more warps stay resident.
+template <int NPAD>
+struct SmallCfg {
+  static constexpr int WARPS = NPAD <= 16 ? 8 : 4;  // warps (panels) per CTA
+  static constexpr int LD = NPAD + 4;               // == 4 (mod 8): conflict-free fragment loads
+  static constexpr size_t kWarpDoubles = 2 * (size_t)NPAD * LD;
+  static constexpr size_t kSmem = sizeof(double) * kWarpDoubles * WARPS;
+};
 
-__global__ void __launch_bounds__(32 * kSmallWarps) prep_small_kernel(DevPlan P) {
+template <int NPAD>
+__global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(DevPlan P, int t_begin, int t_end) {
+  using Cfg = SmallCfg<NPAD>;
+  constexpr int LD = Cfg::LD;
   extern __shared__ __align__(16) unsigned char prep_smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int t = blockIdx.x * kSmallWarps + warp;
-  if (t >= P.n_prep_small) return;
-  double* D = reinterpret_cast<double*>(prep_smem) + (size_t)warp * 2 * kSmallPanel * kLdS;
-  double* W = D + kSmallPanel * kLdS;
+  const int t = t_begin + blockIdx.x * Cfg::WARPS + warp;
+  if (t >= t_end) return;
+  double* D = reinterpret_cast<double*>(prep_smem) + (size_t)warp * Cfg::kWarpDoubles;
+  double* W = D + NPAD * LD;
   const I2 task = P.prep_small_tasks[t];
   const int sub = task.x;
   const Panel pn = P.panels[task.y];
@@ -261,58 +270,57 @@ __global__ void __launch_bounds__(32 * kSmallWarps) prep_small_kernel(DevPlan P)
   const double* __restrict__ Lv = P.Lptr[sub];
   double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
   const int kw = pn.kw, kw4 = pn.kw4;
-  int npad = 8;
-  while (npad < kw) npad *= 2;
-  for (int q = lane; q < npad * kLdS / 2; q += 32) reinterpret_cast<double2*>(D)[q] = make_double2(0.0, 0.0);
+  for (int q = lane; q < NPAD * LD / 2; q += 32) reinterpret_cast<double2*>(D)[q] = make_double2(0.0, 0.0);
   zero_chunk_gaps(PB, pn, lane, 32);
   __syncwarp();
-  scatter_panel<kLdS>(Lv, dest, PB, D, pn, lane, 32);
-  for (int i = kw + lane; i < npad; i += 32) D[i * kLdS + i] = 1.0;
+  scatter_panel<LD>(Lv, dest, PB, D, pn, lane, 32);
+  for (int i = kw + lane; i < NPAD; i += 32) D[i * LD + i] = 1.0;
   __syncwarp();
   {  // level 0: lane -> (8x8 block lane/8, column lane%8)
     const int base = (lane >> 3) * 8, j = lane & 7;
-    if (base < npad) {
+    if (base < NPAD) {
       double x[8];
 #pragma unroll
       for (int i = 0; i < 8; i++) {
         double s = (i == j) ? 1.0 : 0.0;
 #pragma unroll
-        for (int k = 0; k < i; k++) s -= (k >= j) ? D[(base + k) * kLdS + base + i] * x[k] : 0.0;
-        const double dii = D[(base + i) * kLdS + base + i];
+        for (int k = 0; k < i; k++) s -= (k >= j) ? D[(base + k) * LD + base + i] * x[k] : 0.0;
+        const double dii = D[(base + i) * LD + base + i];
         if (j == 0 && base + i < kw && (!(dii > 0.0) || !isfinite(dii)))
           atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + base + i));
         x[i] = (i >= j) ? s / dii : 0.0;
       }
 #pragma unroll
-      for (int i = 0; i < 8; i++) W[(base + j) * kLdS + base + i] = x[i];
+      for (int i = 0; i < 8; i++) W[(base + j) * LD + base + i] = x[i];
     }
   }
   __syncwarp();
   const int g = lane >> 2, t4 = lane & 3;
-  for (int b = 16; b <= npad; b *= 2) {
-    const int h = b / 2, nbh = h / 8, npairs = npad / b;
+#pragma unroll
+  for (int b = 16; b <= NPAD; b *= 2) {
+    const int h = b / 2, nbh = h / 8, npairs = NPAD / b;
     for (int blk = 0; blk < npairs * nbh * nbh; blk++) {
       const int pr = blk / (nbh * nbh), rem = blk - pr * nbh * nbh, bi = rem % nbh, bj = rem / nbh;
       const int base = pr * b;
-      const double* Cm = D + base * kLdS + base + h;
-      const double* Ai = W + base * kLdS + base;
+      const double* Cm = D + base * LD + base + h;
+      const double* Ai = W + base * LD + base;
       double c0 = 0.0, c1 = 0.0;
-      for (int k = bj * 8; k < h; k += 4) dmma(c0, c1, Cm[(k + t4) * kLdS + bi * 8 + g], Ai[(bj * 8 + g) * kLdS + k + t4]);
-      double* Tt = D + base * kLdS + base;
-      Tt[(bj * 8 + 2 * t4) * kLdS + bi * 8 + g] = c0;
-      Tt[(bj * 8 + 2 * t4 + 1) * kLdS + bi * 8 + g] = c1;
+      for (int k = bj * 8; k < h; k += 4) dmma(c0, c1, Cm[(k + t4) * LD + bi * 8 + g], Ai[(bj * 8 + g) * LD + k + t4]);
+      double* Tt = D + base * LD + base;
+      Tt[(bj * 8 + 2 * t4) * LD + bi * 8 + g] = c0;
+      Tt[(bj * 8 + 2 * t4 + 1) * LD + bi * 8 + g] = c1;
     }
     __syncwarp();
     for (int blk = 0; blk < npairs * nbh * nbh; blk++) {
       const int pr = blk / (nbh * nbh), rem = blk - pr * nbh * nbh, bi = rem % nbh, bj = rem / nbh;
       const int base = pr * b;
-      const double* Bi = W + (base + h) * kLdS + base + h;
-      const double* Tt = D + base * kLdS + base;
+      const double* Bi = W + (base + h) * LD + base + h;
+      const double* Tt = D + base * LD + base;
       double c0 = 0.0, c1 = 0.0;
-      for (int k = 0; k < (bi + 1) * 8; k += 4) dmma(c0, c1, Bi[(k + t4) * kLdS + bi * 8 + g], Tt[(bj * 8 + g) * kLdS + k + t4]);
-      double* Wo = W + base * kLdS + base + h;
-      Wo[(bj * 8 + 2 * t4) * kLdS + bi * 8 + g] = -c0;
-      Wo[(bj * 8 + 2 * t4 + 1) * kLdS + bi * 8 + g] = -c1;
+      for (int k = 0; k < (bi + 1) * 8; k += 4) dmma(c0, c1, Bi[(k + t4) * LD + bi * 8 + g], Tt[(bj * 8 + g) * LD + k + t4]);
+      double* Wo = W + base * LD + base + h;
+      Wo[(bj * 8 + 2 * t4) * LD + bi * 8 + g] = -c0;
+      Wo[(bj * 8 + 2 * t4 + 1) * LD + bi * 8 + g] = -c1;
     }
     __syncwarp();
   }
@@ -320,7 +328,7 @@ __global__ void __launch_bounds__(32 * kSmallWarps) prep_small_kernel(DevPlan P)
   const int ldD = pn.ldD;
   for (int q = lane; q < ldD * kw4; q += 32) {
     const int j = q / ldD, i = q - j * ldD;
-    Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * kLdS + i] : 0.0;
+    Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * LD + i] : 0.0;
   }
 }
 
@@ -429,26 +437,46 @@ __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, c
   }
 }
 
-template <int T>
+// GS = false: the X strip lives in shared memory (swizzled, written out into the group strip at
+// the end).  GS = true ("global strip", subdomains whose strips do not fit on chip, e.g. cfg5): the
+// tile solves in place in its T columns of the SYRK group strip in global memory (row-major, G
+// wide, L2-resident while the tile runs); the strip rows of the plan are then group-strip rows.
+template <int T, bool GS>
 __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPlan P) {
   using Cfg = TileCfg<T>;
-  constexpr int LDX = Cfg::LDX, WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC, CT = Cfg::CT;
+  constexpr int WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC, CT = Cfg::CT;
   constexpr int KS = kMaxPanel / 4;  // k steps of 4 in a full panel
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const TrsmSmem L = trsm_smem_layout(T, P.ring_bytes, P.strip_cap);
+  const TrsmSmem L = trsm_smem_layout(T, P.ring_bytes, P.strip_cap, GS);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem_raw + L.empty);
   int32_t* off = reinterpret_cast<int32_t*>(smem_raw + L.off);
   uint16_t* srow = reinterpret_cast<uint16_t*>(smem_raw + L.srow);
   unsigned char* ring = smem_raw + L.ring;
   double* Ys = reinterpret_cast<double*>(smem_raw + L.ys);
-  double* Xs = reinterpret_cast<double*>(smem_raw + L.strip);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const I2 task = P.trsm_tasks[blockIdx.x];
   const int sub = task.x;
   const Tile tile = P.tiles[task.y];
   const double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
+  double* Xs;
+  int LDX;
+  if constexpr (GS) {
+    Xs = P.X + P.sub_X_base[sub] + P.groups[tile.group].x_off + tile.col_in_group;
+    LDX = P.G;
+  } else {
+    Xs = reinterpret_cast<double*>(smem_raw + L.strip);
+    LDX = Cfg::LDX;
+  }
+  // element (row, col) of the strip
+  auto xi = [&](int row, int col) -> int {
+    if constexpr (GS) {
+      return row * LDX + col;
+    } else {
+      return Cfg::idx(row, col);
+    }
+  };
 
   if (tid == 0) {
     for (int k = 0; k < kSlots; k++) {
@@ -466,7 +494,12 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
   // ---- consumers.  X init (row a2): zero the strip (+4 pad rows), scatter B~^T
   const int g = lane >> 2, t4 = lane & 3;
   const int br0 = (warp / NWC) * WM, bc0 = (warp % NWC) * WN;
-  {
+  if constexpr (GS) {  // the tile's T columns of every group-strip row
+    for (int q = tid; q < tile.strip_rows * (T / 2); q += CT) {
+      const int r = q / (T / 2), j = 2 * (q - r * (T / 2));
+      *reinterpret_cast<double2*>(Xs + (int64_t)r * LDX + j) = make_double2(0.0, 0.0);
+    }
+  } else {
     double2* X2 = reinterpret_cast<double2*>(Xs);
     const int nvec = (tile.strip_rows + 4) * LDX / 2;
     for (int q = tid; q < nvec; q += CT) X2[q] = make_double2(0.0, 0.0);
@@ -474,7 +507,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
   consumer_sync<CT>();
   for (int q = tile.binit_begin + tid; q < tile.binit_end; q += CT) {
     const BInit bi = P.binit[q];
-    Xs[Cfg::idx(bi.strip_row, bi.col)] = bi.val;
+    Xs[xi(bi.strip_row, bi.col)] = bi.val;
   }
   consumer_sync<CT>();
 
@@ -511,7 +544,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
       const double* xb = Xs + (row0 + t4) * LDX;
       int xcol[WN];
 #pragma unroll
-      for (int j = 0; j < WN; j++) xcol[j] = Cfg::idx(row0 + t4, (bc0 + j) * 8 + g) - (row0 + t4) * LDX;
+      for (int j = 0; j < WN; j++) xcol[j] = xi(row0 + t4, (bc0 + j) * 8 + g) - (row0 + t4) * LDX;
       if (br0 * 8 < kw4) {
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) {
@@ -520,7 +553,8 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
 #pragma unroll
             for (int i = 0; i < WM; i++) a[i] = A[(4 * ks + t4) * ld + (br0 + i) * 8 + g];
 #pragma unroll
-            for (int j = 0; j < WN; j++) bb[j] = xb[(4 * ks) * LDX + xcol[j]];
+            for (int j = 0; j < WN; j++)  // a global strip has no zero pad rows past the last panel
+              bb[j] = (!GS || 4 * ks + t4 < kw) ? xb[(4 * ks) * LDX + xcol[j]] : 0.0;
 #pragma unroll
             for (int i = 0; i < WM; i++)
 #pragma unroll
@@ -552,7 +586,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
     for (int j = 0; j < WN; j++) {
       const double* yb = Ys + Cfg::idx(t4, (bc0 + j) * 8 + g);  // rows 4 ks + t4 share the swizzle
 #pragma unroll
-      for (int ks = 0; ks < KS; ks++) yf[ks][j] = (4 * ks < kw4) ? yb[4 * ks * LDX] : 0.0;
+      for (int ks = 0; ks < KS; ks++) yf[ks][j] = (4 * ks < kw4) ? yb[4 * ks * Cfg::LDX] : 0.0;
     }
     for (int c = 0; c < pn.nchunk; c++) {
       b++;
@@ -564,6 +598,18 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
       int sr[WM];
 #pragma unroll
       for (int i = 0; i < WM; i++) sr[i] = (int)srow[slot * kChunk + (br0 + i) * 8 + g];
+      // global strip: fetch the rows to update before the products (L2 latency under the DMMAs)
+      double2 xold[WM][WN];
+      if constexpr (GS) {
+        if (br0 * 8 < rows_c) {
+#pragma unroll
+          for (int i = 0; i < WM; i++)
+#pragma unroll
+            for (int j = 0; j < WN; j++)
+              xold[i][j] = (sr[i] == 0xFFFF) ? make_double2(0.0, 0.0)
+                                             : *reinterpret_cast<const double2*>(Xs + xi(sr[i], (bc0 + j) * 8 + 2 * t4));
+        }
+      }
       // KSPLIT independent accumulators per output block (k steps round-robin) keep enough DMMA
       // chains in flight per warp
       constexpr int KSPLIT = (WM * WN <= 2) ? 4 : 2;
@@ -603,8 +649,13 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
               s0 += acc[h][i][j][0];
               s1 += acc[h][i][j][1];
             }
-            double2* p = reinterpret_cast<double2*>(Xs + Cfg::idx(sr[i], (bc0 + j) * 8 + 2 * t4));
-            double2 v = *p;
+            double2* p = reinterpret_cast<double2*>(Xs + xi(sr[i], (bc0 + j) * 8 + 2 * t4));
+            double2 v;
+            if constexpr (GS) {
+              v = xold[i][j];
+            } else {
+              v = *p;
+            }
             v.x -= s0;
             v.y -= s1;
             *p = v;
@@ -619,13 +670,14 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
       if (r < kw) {
 #pragma unroll
         for (int j = 0; j < WN; j++)
-          *reinterpret_cast<double2*>(Xs + Cfg::idx(row0 + r, (bc0 + j) * 8 + 2 * t4)) =
+          *reinterpret_cast<double2*>(Xs + xi(row0 + r, (bc0 + j) * 8 + 2 * t4)) =
               make_double2(yacc[i][j][0], yacc[i][j][1]);
       }
     }
     consumer_sync<CT>();  // strip updates visible before the next panel reads its rows; Ys reusable
   }
 
+  if constexpr (GS) return;  // solved in place
   // ---- write the strip into the group strip (row-major, G columns) for the SYRK
   const Group G = P.groups[tile.group];
   double* __restrict__ Xg = P.X + P.sub_X_base[sub] + G.x_off + tile.col_in_group;
@@ -634,7 +686,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
     for (int q = tid; q < ws.len * (T / 2); q += CT) {
       const int r = q / (T / 2), j = 2 * (q - r * (T / 2));
       double2 v = make_double2(0.0, 0.0);
-      if (ws.src >= 0) v = *reinterpret_cast<const double2*>(Xs + Cfg::idx(ws.src + r, j));
+      if (ws.src >= 0) v = *reinterpret_cast<const double2*>(Xs + xi(ws.src + r, j));
       *reinterpret_cast<double2*>(Xg + (int64_t)(ws.dst + r) * P.G + j) = v;
     }
   }
@@ -828,6 +880,16 @@ __global__ void __launch_bounds__(kThreads) apply_scatter_kernel(DevPlan P, doub
 // ------------------------------------------------------------------------------------------------
 namespace {
 
+using TrsmFn = void (*)(DevPlan);
+TrsmFn trsm_kernel_ptr(int T, bool gs) {
+  switch (T) {
+    case 8: return gs ? trsm_smem_kernel<8, true> : trsm_smem_kernel<8, false>;
+    case 16: return gs ? trsm_smem_kernel<16, true> : trsm_smem_kernel<16, false>;
+    case 32: return gs ? trsm_smem_kernel<32, true> : trsm_smem_kernel<32, false>;
+    default: return gs ? trsm_smem_kernel<64, true> : trsm_smem_kernel<64, false>;
+  }
+}
+
 template <typename V>
 sc_status upload(Plan& P, const std::vector<V>& v, const V** dst, std::string& err) {
   void* d = nullptr;
@@ -910,7 +972,6 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, P.sub_m, &D.sub_m, err));
   TRY(upload(P, P.prep_tasks, &D.prep_tasks, err));
   TRY(upload(P, P.prep_small_tasks, &D.prep_small_tasks, err));
-  D.n_prep_small = (int32_t)P.prep_small_tasks.size();
   TRY(upload(P, P.trsm_tasks, &D.trsm_tasks, err));
   TRY(upload(P, P.syrk_tasks, &D.syrk_tasks, err));
   TRY(upload(P, P.apply_tasks, &D.apply_tasks, err));
@@ -945,7 +1006,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
           " columns leaves no room for the L-block ring in shared memory; use smaller tile_cols";
     return SC_ERR_INVALID_ARG;
   }
-  P.smem_trsm = trsm_smem_layout(P.T, P.ring_bytes, P.max_strip_rows).total;
+  P.smem_trsm = trsm_smem_layout(P.T, P.ring_bytes, P.max_strip_rows, P.gstrip).total;
   int dev_smem = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.opt.device));
   if (P.smem_trsm > (size_t)dev_smem) {
@@ -955,14 +1016,10 @@ sc_status upload_plan(Plan& P, std::string& err) {
     return SC_ERR_INVALID_ARG;
   }
   CUDA_TRY(cudaFuncSetAttribute(prep_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem));
-  CUDA_TRY(cudaFuncSetAttribute(prep_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmallSmem));
+  CUDA_TRY(cudaFuncSetAttribute(prep_small_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg<32>::kSmem));
   CUDA_TRY(cudaFuncSetAttribute(syrk_pair_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)syrk_smem_bytes<64>()));
-  switch (P.T) {
-    case 8: CUDA_TRY(cudaFuncSetAttribute(trsm_smem_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
-    case 16: CUDA_TRY(cudaFuncSetAttribute(trsm_smem_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
-    case 32: CUDA_TRY(cudaFuncSetAttribute(trsm_smem_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
-    default: CUDA_TRY(cudaFuncSetAttribute(trsm_smem_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_trsm)); break;
-  }
+  CUDA_TRY(cudaFuncSetAttribute(trsm_kernel_ptr(P.T, P.gstrip), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)P.smem_trsm));
   double total = 8.0 * (P.X_doubles + P.F_doubles + P.PB_doubles + P.part_doubles);
   total += dest.size() * 4.0 + Rrows.size() * 4.0 + panels.size() * sizeof(Panel) + tiles.size() * sizeof(Tile) +
            steps.size() * sizeof(Step) + wsegs.size() * sizeof(WSeg) + groups.size() * sizeof(Group) +
@@ -1012,19 +1069,24 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
     prep_panel_kernel<<<npr, kThreads, kPrepSmem, stream>>>(P.dev);
     CUDA_TRY(cudaGetLastError());
   }
-  const int nps = (int)P.prep_small_tasks.size();
-  if (nps > 0) {
-    prep_small_kernel<<<(nps + kSmallWarps - 1) / kSmallWarps, 32 * kSmallWarps, kPrepSmallSmem, stream>>>(P.dev);
+  for (int bkt = 0; bkt < 3; bkt++) {  // small panels bucketed by padded width 8 / 16 / 32
+    const int t0 = P.small_begin[bkt], t1 = P.small_begin[bkt + 1], nt = t1 - t0;
+    if (nt <= 0) continue;
+    if (bkt == 0) {
+      using C8 = SmallCfg<8>;
+      prep_small_kernel<8><<<(nt + C8::WARPS - 1) / C8::WARPS, 32 * C8::WARPS, C8::kSmem, stream>>>(P.dev, t0, t1);
+    } else if (bkt == 1) {
+      using C16 = SmallCfg<16>;
+      prep_small_kernel<16><<<(nt + C16::WARPS - 1) / C16::WARPS, 32 * C16::WARPS, C16::kSmem, stream>>>(P.dev, t0, t1);
+    } else {
+      using C32 = SmallCfg<32>;
+      prep_small_kernel<32><<<(nt + C32::WARPS - 1) / C32::WARPS, 32 * C32::WARPS, C32::kSmem, stream>>>(P.dev, t0, t1);
+    }
     CUDA_TRY(cudaGetLastError());
   }
   if (P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
   if (ntr > 0) {
-    switch (P.T) {
-      case 8: trsm_smem_kernel<8><<<ntr, TileCfg<8>::CT + 32, P.smem_trsm, stream>>>(P.dev); break;
-      case 16: trsm_smem_kernel<16><<<ntr, TileCfg<16>::CT + 32, P.smem_trsm, stream>>>(P.dev); break;
-      case 32: trsm_smem_kernel<32><<<ntr, TileCfg<32>::CT + 32, P.smem_trsm, stream>>>(P.dev); break;
-      default: trsm_smem_kernel<64><<<ntr, TileCfg<64>::CT + 32, P.smem_trsm, stream>>>(P.dev); break;
-    }
+    trsm_kernel_ptr(P.T, P.gstrip)<<<ntr, TileCfg<8>::CT + 32, P.smem_trsm, stream>>>(P.dev);
     CUDA_TRY(cudaGetLastError());
   }
   if (P.tev[2]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[2], stream));

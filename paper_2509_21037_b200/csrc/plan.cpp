@@ -21,6 +21,7 @@
 //   7. work counters and memory layout.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <iterator>
@@ -124,7 +125,7 @@ int relax_wsmall() {
 }
 
 // Steps 2-7 for one class.
-sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, int skip, ClassPlan& C,
+sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, int skip, bool gstrip, ClassPlan& C,
                         std::string& err) {
   const int32_t n = d.n, m = d.m;
   C.n = n;
@@ -273,6 +274,20 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     C.fl_prep_exec += (double)p.kw * p.kw * p.kw / 3.0;
   }
   C.pb_doubles = pb;
+  if (std::getenv("SC_DEBUG_PB")) {
+    double inv = 0, chunk = 0, useful = 0, nsmall = 0, nbig = 0;
+    std::vector<int> hist(9, 0);
+    for (auto& p : C.panels) {
+      inv += (double)p.ldD * p.kw4;
+      chunk += (p.nchunk > 0 ? (double)(p.nchunk - 1) * kLdC * p.kw4 + (double)p.ldLast * p.kw4 : 0);
+      useful += (double)p.kw * (p.kw + 1) / 2 + (double)p.kw * p.nR;
+      (p.kw > kSmallPanel ? nbig : nsmall) += 1;
+      hist[std::min(8, (p.kw + 7) / 8)]++;
+    }
+    fprintf(stderr, "PB: panels %zu (small %g big %g) inv %g chunk %g useful-trapezoid %g nnzL %lld pb %lld | kw/8 hist", C.panels.size(), nsmall, nbig, inv, chunk, useful, (long long)cp[n], (long long)pb);
+    for (int h : hist) fprintf(stderr, " %d", h);
+    fprintf(stderr, "\n");
+  }
 
   // --- 3. permuted B~^T, pivots, stepped order
   std::vector<int32_t> iperm((size_t)n);
@@ -325,7 +340,7 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     C.fl_trsm_sparse = (double)m * (2.0 * (double)cp[n] - (double)n);
   }
 
-  // --- 4/5. TRSM tiles: reach at panel granularity, steps (panels in order), B scatter
+  // --- 4. TRSM tiles and their reach at panel granularity
   const int32_t np = (int32_t)C.panels.size();
   const int32_t ntiles = (m + T - 1) / T;
   std::vector<int32_t> inreach((size_t)np, -1), stamp((size_t)n, -1), strip_base((size_t)np, -1),
@@ -354,99 +369,114 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
       for (int32_t p = 0; p < np; p++)
         if (C.panels[(size_t)p].a + C.panels[(size_t)p].kw > from) tp.push_back(p);
     }
-    t.step_begin = (int32_t)C.steps.size();
-    int32_t rows = 0;
-    for (int32_t p : tp) {
-      strip_base[(size_t)p] = rows;
-      in_tile[(size_t)p] = J;
-      C.steps.push_back({p, rows, 0});
-      const Panel& P = C.panels[(size_t)p];
-      // GEMM1 skips the zero blocks above the diagonal of inv(L_pp)
-      C.fl_trsm_exec += 2.0 * T * P.kw4 * (0.5 * (double)P.kw4 + 4.0 + (double)P.nR);
-      rows += P.kw;
-    }
-    t.step_end = (int32_t)C.steps.size();
-    // strip rows of each step's pruned rows R_p, 64 per chunk (0xFFFF: not in this tile's strip)
-    for (int32_t s = t.step_begin; s < t.step_end; s++) {
-      Step& st = C.steps[(size_t)s];
-      const Panel& P = C.panels[(size_t)st.panel];
-      st.srow_off = (int64_t)C.srows.size();
-      for (int32_t k = 0; k < P.nchunk * kChunk; k++) {
-        uint16_t v = 0xFFFF;
-        if (k < P.nR) {
-          const int32_t r = C.Rrows[(size_t)(P.R_off + k)];
-          const int32_t q = panel_of_col[(size_t)r];
-          if (in_tile[(size_t)q] == J) v = (uint16_t)(strip_base[(size_t)q] + (r - C.panels[(size_t)q].a));
-        }
-        C.srows.push_back(v);
-      }
-    }
-    t.strip_rows = rows;
-    C.max_strip_rows = std::max(C.max_strip_rows, rows);
-    t.binit_begin = (int32_t)C.binit.size();
-    for (int32_t a = t.col0; a < t.col0 + t.width; a++)
-      for (auto& e : bcol[(size_t)C.sigma[(size_t)a]]) {
-        const int32_t p = panel_of_col[(size_t)e.first];
-        C.binit.push_back({strip_base[(size_t)p] + (e.first - C.panels[(size_t)p].a), a - t.col0, e.second});
-      }
-    t.binit_end = (int32_t)C.binit.size();
     C.tiles.push_back(t);
   }
 
-  // --- SYRK groups (kGroup columns): union of member tiles' panels; tile write-out segments
+  // --- 5/6. SYRK groups (kGroup columns: union of the member tiles' panels), and per tile the
+  // ordered factor panels it applies (steps), the strip rows of their pruned rows and the B~^T
+  // scatter.  Strip rows are tile-local (shared-memory strip, written out into the group strip at
+  // the end) or, for global strips, the rows of the group strip itself (solved in place).
   const int32_t ngroups = (m + kGroup - 1) / kGroup;
   int64_t xoff = 0;
+  int32_t J0 = 0;
   for (int32_t g = 0; g < ngroups; g++) {
     Group G{};
     G.col0 = g * kGroup;
     G.width = std::min(kGroup, m - g * kGroup);
+    int32_t J1 = J0;
+    while (J1 < ntiles && C.tiles[(size_t)J1].group == g) J1++;
     std::vector<int32_t> gp;
-    for (int32_t J = 0; J < ntiles; J++)
-      if (C.tiles[(size_t)J].group == g) {
-        std::vector<int32_t> u;
-        std::set_union(gp.begin(), gp.end(), tile_panels[(size_t)J].begin(), tile_panels[(size_t)J].end(),
-                       std::back_inserter(u));
-        gp.swap(u);
-      }
+    for (int32_t J = J0; J < J1; J++) {
+      std::vector<int32_t> u;
+      std::set_union(gp.begin(), gp.end(), tile_panels[(size_t)J].begin(), tile_panels[(size_t)J].end(),
+                     std::back_inserter(u));
+      gp.swap(u);
+    }
     G.reach_begin = (int32_t)C.greach.size();
-    int32_t rows = 0;
+    int32_t grows = 0;
     for (int32_t p : gp) {
-      C.greach.push_back({p, rows});
-      rows += C.panels[(size_t)p].kw;
+      C.greach.push_back({p, grows});
+      grows += C.panels[(size_t)p].kw;
     }
     G.reach_end = (int32_t)C.greach.size();
-    G.strip_rows = rows;
+    G.strip_rows = grows;
     G.x_off = xoff;
-    xoff += (int64_t)rows * kGroup;
-    for (int32_t J = 0; J < ntiles; J++) {
+    xoff += (int64_t)grows * kGroup;
+    for (int32_t J = J0; J < J1; J++) {
       Tile& t = C.tiles[(size_t)J];
-      if (t.group != g) continue;
-      t.wseg_begin = (int32_t)C.wsegs.size();
-      const auto& tpn = tile_panels[(size_t)J];
+      const auto& tp = tile_panels[(size_t)J];
+      t.step_begin = (int32_t)C.steps.size();
+      int32_t rows = 0;
+      size_t q = (size_t)G.reach_begin;
+      for (int32_t p : tp) {
+        if (gstrip) {
+          while (C.greach[q].panel != p) q++;
+          strip_base[(size_t)p] = C.greach[q].off;
+        } else {
+          strip_base[(size_t)p] = rows;
+        }
+        in_tile[(size_t)p] = J;
+        C.steps.push_back({p, strip_base[(size_t)p], 0});
+        const Panel& P = C.panels[(size_t)p];
+        // GEMM1 skips the zero blocks above the diagonal of inv(L_pp)
+        C.fl_trsm_exec += 2.0 * T * P.kw4 * (0.5 * (double)P.kw4 + 4.0 + (double)P.nR);
+        rows += P.kw;
+      }
+      t.step_end = (int32_t)C.steps.size();
+      // strip rows of each step's pruned rows R_p, 64 per chunk (0xFFFF: not in this tile's strip)
+      for (int32_t s = t.step_begin; s < t.step_end; s++) {
+        Step& st = C.steps[(size_t)s];
+        const Panel& P = C.panels[(size_t)st.panel];
+        st.srow_off = (int64_t)C.srows.size();
+        for (int32_t k = 0; k < P.nchunk * kChunk; k++) {
+          uint16_t v = 0xFFFF;
+          if (k < P.nR) {
+            const int32_t r = C.Rrows[(size_t)(P.R_off + k)];
+            const int32_t qq = panel_of_col[(size_t)r];
+            if (in_tile[(size_t)qq] == J) v = (uint16_t)(strip_base[(size_t)qq] + (r - C.panels[(size_t)qq].a));
+          }
+          C.srows.push_back(v);
+        }
+      }
+      // global strips are zeroed over all rows of the group strip (rows outside this tile's reach
+      // stay exactly zero in its columns)
+      t.strip_rows = gstrip ? grows : rows;
+      C.max_strip_rows = std::max(C.max_strip_rows, rows);
+      t.binit_begin = (int32_t)C.binit.size();
+      for (int32_t a = t.col0; a < t.col0 + t.width; a++)
+        for (auto& e : bcol[(size_t)C.sigma[(size_t)a]]) {
+          const int32_t p = panel_of_col[(size_t)e.first];
+          C.binit.push_back({strip_base[(size_t)p] + (e.first - C.panels[(size_t)p].a), a - t.col0, e.second});
+        }
+      t.binit_end = (int32_t)C.binit.size();
+      // write-out segments of a shared-memory strip into the group strip
+      t.wseg_begin = t.wseg_end = (int32_t)C.wsegs.size();
+      if (gstrip) continue;
       size_t k = 0;
       int32_t src = 0;
-      for (int32_t q = G.reach_begin; q < G.reach_end; q++) {
-        const Reach& R = C.greach[(size_t)q];
+      for (int32_t qg = G.reach_begin; qg < G.reach_end; qg++) {
+        const Reach& R = C.greach[(size_t)qg];
         const int32_t kw = C.panels[(size_t)R.panel].kw;
-        int32_t s = -1;
-        if (k < tpn.size() && tpn[k] == R.panel) {
-          s = src;
+        int32_t sidx = -1;
+        if (k < tp.size() && tp[k] == R.panel) {
+          sidx = src;
           src += kw;
           k++;
         }
         if ((int32_t)C.wsegs.size() > t.wseg_begin) {
           WSeg& last = C.wsegs.back();
           const bool contig_dst = last.dst + last.len == R.off;
-          if (contig_dst && ((s < 0 && last.src < 0) || (s >= 0 && last.src >= 0 && last.src + last.len == s))) {
+          if (contig_dst && ((sidx < 0 && last.src < 0) || (sidx >= 0 && last.src >= 0 && last.src + last.len == sidx))) {
             last.len += kw;
             continue;
           }
         }
-        C.wsegs.push_back({s, R.off, kw, 0});
+        C.wsegs.push_back({sidx, R.off, kw, 0});
       }
       t.wseg_end = (int32_t)C.wsegs.size();
     }
     C.groups.push_back(G);
+    J0 = J1;
   }
   C.x_doubles = xoff;
 
@@ -500,7 +530,8 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   if (!(opt.tile_cols == 0 || opt.tile_cols == 8 || opt.tile_cols == 16 || opt.tile_cols == 32 || opt.tile_cols == 64))
     FAIL(SC_ERR_INVALID_ARG, "tile_cols must be 0, 8, 16, 32 or 64");
   if (opt.panel_cols < 0 || opt.panel_cols > kMaxPanel) FAIL(SC_ERR_INVALID_ARG, "panel_cols must be in [0, 64]");
-  for (int k = 0; k < 7; k++)
+  if (opt.x_strip < 0 || opt.x_strip > 2) FAIL(SC_ERR_INVALID_ARG, "x_strip must be 0, 1 or 2");
+  for (int k = 0; k < 6; k++)
     if (opt.reserved[k] != 0) FAIL(SC_ERR_INVALID_ARG, "reserved options must be zero");
   P.opt = opt;
   P.nsub = nsub;
@@ -544,14 +575,15 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   int32_t G0 = max_m > 512 ? 64 : 32;
   if (const char* e = std::getenv("SC_GROUP")) G0 = std::atoi(e);
   if (!(G0 == 16 || G0 == 32 || G0 == 64)) FAIL(SC_ERR_INVALID_ARG, "SC_GROUP must be 16, 32 or 64");
-  auto analyse_all = [&](int T) -> sc_status {
+  auto analyse_all = [&](int T, bool gstrip) -> sc_status {
     P.T = T;
     P.G = std::max(G0, T);
+    P.gstrip = gstrip;
     for (size_t c = 0; c < P.classes.size(); c++) {
       uint64_t h = P.classes[c].hash;
       P.classes[c] = ClassPlan();
       P.classes[c].hash = h;
-      sc_status st = analyse_class(sd[rep[c]], T, P.G, P.PW, opt.skip, P.classes[c], err);
+      sc_status st = analyse_class(sd[rep[c]], T, P.G, P.PW, opt.skip, gstrip, P.classes[c], err);
       if (st != SC_OK) {
         err = "subdomain " + std::to_string(rep[c]) + ": " + err;
         return st;
@@ -561,7 +593,8 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   };
   // TRSM tile width: the widest of 32 / 16 / 8 whose largest X strip fits in shared memory next to
   // an L-block ring of at least two of the plan's largest blocks; the ring gets what is left (up
-  // to 160 KB) so the producer can run ahead
+  // to 160 KB) so the producer can run ahead.  A global strip (solved in place in the group strip,
+  // through L2) needs no strip space: the ring gets up to 160 KB.
   auto ring_for = [&](int T) -> int64_t {
     int32_t mx = 0;
     int64_t maxblk = 16;
@@ -572,19 +605,32 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
         if (p.nchunk > 0) maxblk = std::max<int64_t>(maxblk, (int64_t)(p.nchunk > 1 ? kLdC : p.ldLast) * p.kw4 * 8);
       }
     }
-    const int64_t fixed = (int64_t)trsm_smem_layout(T, 0, mx).total;
+    const int64_t fixed = (int64_t)trsm_smem_layout(T, 0, mx, P.gstrip).total;
     int64_t ring = std::min<int64_t>(kRingMaxBytes, (int64_t)kSmemBudget - fixed) & ~(int64_t)127;
     return ring >= 2 * maxblk ? ring : -1;
   };
-  if (opt.tile_cols) {
-    sc_status st = analyse_all(opt.tile_cols);
+  const int Tg = opt.tile_cols ? opt.tile_cols : 16;  // global-strip tile width
+  if (opt.x_strip == SC_STRIP_GLOBAL) {
+    sc_status st = analyse_all(Tg, true);
     if (st != SC_OK) return st;
+  } else if (opt.tile_cols) {
+    sc_status st = analyse_all(opt.tile_cols, false);
+    if (st != SC_OK) return st;
+    if (opt.x_strip == SC_STRIP_AUTO && ring_for(opt.tile_cols) < 0) {
+      st = analyse_all(Tg, true);
+      if (st != SC_OK) return st;
+    }
   } else {
     const int cand[3] = {32, 16, 8};
-    for (int k = 0; k < 3; k++) {
-      sc_status st = analyse_all(cand[k]);
+    bool fits = false;
+    for (int k = 0; k < 3 && !fits; k++) {
+      sc_status st = analyse_all(cand[k], false);
       if (st != SC_OK) return st;
-      if (ring_for(cand[k]) > 0) break;
+      fits = ring_for(cand[k]) > 0;
+    }
+    if (!fits && opt.x_strip == SC_STRIP_AUTO) {
+      sc_status st = analyse_all(Tg, true);
+      if (st != SC_OK) return st;
     }
   }
   for (auto& C : P.classes) P.max_strip_rows = std::max(P.max_strip_rows, C.max_strip_rows);
@@ -648,6 +694,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   S.tile_cols = P.T;
   S.panel_cols = P.PW;
   std::vector<int64_t> qcount((size_t)std::max<int64_t>(opt.n_lambda_global, 0) + 1, 0);
+  std::vector<I2> small_bkt[3];
   for (int32_t i = 0; i < nsub; i++) {
     const int32_t cls = P.sub_cls[(size_t)i];
     const ClassPlan& C = P.classes[(size_t)cls];
@@ -664,9 +711,12 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     P.sub_part_off.push_back(P.part_doubles);
     const int32_t nab = (C.m + kApplyTile - 1) / kApplyTile;  // apply tiles: nab (nab + 1) / 2
     P.part_doubles += (int64_t)nab * (nab + 1) / 2 * 2 * kApplyTile;
-    for (size_t q = 0; q < C.panels.size(); q++)
-      (C.panels[q].kw > kSmallPanel ? P.prep_tasks : P.prep_small_tasks)
-          .push_back({i, P.cls_panel_begin[(size_t)cls] + (int32_t)q});
+    for (size_t q = 0; q < C.panels.size(); q++) {
+      const I2 tk{i, P.cls_panel_begin[(size_t)cls] + (int32_t)q};
+      const int32_t kw = C.panels[q].kw;
+      if (kw > kSmallPanel) P.prep_tasks.push_back(tk);
+      else small_bkt[kw <= 8 ? 0 : (kw <= 16 ? 1 : 2)].push_back(tk);
+    }
     for (size_t t = 0; t < C.tiles.size(); t++)
       if (C.tiles[t].width > 0) P.trsm_tasks.push_back({i, P.cls_tile_begin[(size_t)cls] + (int32_t)t});
     for (size_t q = 0; q < C.pairs.size(); q++) P.syrk_tasks.push_back({i, P.cls_pair_begin[(size_t)cls] + (int32_t)q});
@@ -703,7 +753,13 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     S.bytes_panels += 8.0 * (double)C.pb_doubles;
     S.panels += (int64_t)C.panels.size();
   }
+  for (int b = 0; b < 3; b++) {
+    P.small_begin[b] = (int32_t)P.prep_small_tasks.size();
+    P.prep_small_tasks.insert(P.prep_small_tasks.end(), small_bkt[b].begin(), small_bkt[b].end());
+  }
+  P.small_begin[3] = (int32_t)P.prep_small_tasks.size();
   S.group_cols = P.G;
+  S.x_strip = P.gstrip ? SC_STRIP_GLOBAL : SC_STRIP_SHARED;
   S.trsm_tasks = (int64_t)P.trsm_tasks.size();
   S.syrk_tasks = (int64_t)P.syrk_tasks.size();
   S.bytes_X = 8.0 * (double)P.X_doubles;

@@ -42,7 +42,7 @@ struct TrsmSmem {
 };
 // Row stride of the shared-memory strip: T (column-swizzled) for T >= 16, T + 4 for T = 8.
 SC_HD constexpr int strip_ld(int T) { return T >= 16 ? T : T + 4; }
-SC_HD inline TrsmSmem trsm_smem_layout(int T, int ring_bytes, int strip_cap) {
+SC_HD inline TrsmSmem trsm_smem_layout(int T, int ring_bytes, int strip_cap, bool global_strip) {
   TrsmSmem s{};
   s.full = 0;
   s.empty = 8 * kSlots;
@@ -51,7 +51,7 @@ SC_HD inline TrsmSmem trsm_smem_layout(int T, int ring_bytes, int strip_cap) {
   s.ring = s.srow + sizeof(uint16_t) * kSlots * kChunk;
   s.ys = s.ring + (size_t)ring_bytes;
   s.strip = s.ys + sizeof(double) * (size_t)kMaxPanel * (size_t)strip_ld(T);
-  s.total = s.strip + sizeof(double) * (size_t)(strip_cap + 4) * (size_t)strip_ld(T);
+  s.total = s.strip + (global_strip ? 0 : sizeof(double) * (size_t)(strip_cap + 4) * (size_t)strip_ld(T));
   return s;
 }
 
@@ -185,8 +185,8 @@ struct DevPlan {
   const int32_t* sub_m;
   const double* const* Lptr;       // per subdomain L values (device)
   const I2* prep_tasks;            // (sub, global panel), panels wider than kSmallPanel
-  const I2* prep_small_tasks;      // (sub, global panel), panels of <= kSmallPanel columns
-  int32_t n_prep_small;
+  const I2* prep_small_tasks;      // (sub, global panel), panels of <= kSmallPanel columns, bucketed
+                                   //   by padded width 8 / 16 / 32 (Plan::small_begin)
   const I2* trsm_tasks;            // (sub, global tile)
   const I2* syrk_tasks;            // (sub, global pair)
   const ApplyTask* apply_tasks;
@@ -207,6 +207,7 @@ struct DevPlan {
 struct Plan {
   sc_options opt{};
   int32_t T = 32, G = 64, PW = 64, ring_bytes = 0;
+  bool gstrip = false;             // X strips solved in place in the group strips (global memory)
   int32_t nsub = 0;
   std::vector<ClassPlan> classes;
   std::vector<int32_t> sub_cls;
@@ -215,6 +216,7 @@ struct Plan {
   // global (concatenated) arrays
   std::vector<int32_t> cls_tile_begin, cls_pair_begin, cls_panel_begin, cls_group_begin;
   std::vector<I2> prep_tasks, prep_small_tasks, trsm_tasks, syrk_tasks;
+  int32_t small_begin[4] = {0, 0, 0, 0};  // prep_small_tasks buckets: npad 8 | 16 | 32
   std::vector<ApplyTask> apply_tasks;
   std::vector<int64_t> sub_X_base, sub_F_base, sub_PB_base, sub_part_off, sub_slm_off;
   std::vector<int64_t> slm, qg_ptr, qg_sub_a;

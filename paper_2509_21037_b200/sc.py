@@ -17,6 +17,7 @@ LIB_PATH = os.path.join(HERE, "libsc_b200.so")
 
 SC_OK, SC_ERR_INVALID_ARG, SC_ERR_PATTERN, SC_ERR_ZERO_PIVOT, SC_ERR_OOM, SC_ERR_CUDA, SC_ERR_STATE = range(7)
 SKIP_NONE, SKIP_ENVELOPE, SKIP_EXACT = 0, 1, 2
+STRIP_AUTO, STRIP_SHARED, STRIP_GLOBAL = 0, 1, 2
 _STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARG", 2: "SC_ERR_PATTERN", 3: "SC_ERR_ZERO_PIVOT", 4: "SC_ERR_OOM",
            5: "SC_ERR_CUDA", 6: "SC_ERR_STATE"}
 
@@ -37,7 +38,7 @@ class SubdomainDesc(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("skip", ctypes.c_int32), ("tile_cols", ctypes.c_int32),
                 ("panel_cols", ctypes.c_int32), ("n_lambda_global", ctypes.c_int64), ("device", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 7)]
+                ("x_strip", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
 
 
 class Stats(ctypes.Structure):
@@ -49,7 +50,7 @@ class Stats(ctypes.Structure):
                                                "flops_trsm_sparse_orig", "flops_trsm_executed",
                                                "flops_syrk_executed", "bytes_L_values", "bytes_F_lower", "bytes_X",
                                                "device_bytes", "bytes_apply", "bytes_panels")] + \
-               [("panels", ctypes.c_int64), ("group_cols", ctypes.c_int32), ("pad0", ctypes.c_int32)]
+               [("panels", ctypes.c_int64), ("group_cols", ctypes.c_int32), ("x_strip", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -122,7 +123,7 @@ class SCPlan:
     Bt_colptr, Bt_rowidx, Bt_values, lambda_map (numpy arrays, e.g. synth.Subdomain)."""
 
     def __init__(self, subdomains: Sequence, *, n_lambda: int = 0, skip: int = SKIP_EXACT, tile_cols: int = 0,
-                 panel_cols: int = 0, device: int = 0):
+                 panel_cols: int = 0, device: int = 0, x_strip: int = STRIP_AUTO):
         L = lib()
         keep: List[np.ndarray] = []
 
@@ -152,7 +153,7 @@ class SCPlan:
             self.nnz.append(int(sd.L_colptr[-1]))
         opt = Options()
         L.sc_options_default(ctypes.byref(opt))
-        opt.skip, opt.tile_cols, opt.panel_cols = skip, tile_cols, panel_cols
+        opt.skip, opt.tile_cols, opt.panel_cols, opt.x_strip = skip, tile_cols, panel_cols, x_strip
         opt.n_lambda_global, opt.device = int(n_lambda), int(device)
         self.device = device
         self.n_lambda = int(n_lambda)

@@ -173,6 +173,27 @@ def test_invalid_inputs_rejected():
     with pytest.raises(ScError) as e:
         SCPlan([sd], n_lambda=P.n_lambda, tile_cols=48, device=-1)
     assert e.value.status == scmod.SC_ERR_INVALID_ARG
+    # bad strip mode
+    with pytest.raises(ScError) as e:
+        SCPlan([sd], n_lambda=P.n_lambda, x_strip=3, device=-1)
+    assert e.value.status == scmod.SC_ERR_INVALID_ARG
+
+
+def test_global_strip_plan_same_reach_and_work():
+    """The global-strip variant (tiles solved in place in the SYRK group strip) visits the same
+    panels as the shared-memory variant: identical strip rows, executed and useful work."""
+    P = config_problem("t3e")
+    subs = P.subdomains[:6]
+    a = SCPlan(subs, n_lambda=P.n_lambda, tile_cols=16, x_strip=scmod.STRIP_SHARED, device=-1)
+    b = SCPlan(subs, n_lambda=P.n_lambda, tile_cols=16, x_strip=scmod.STRIP_GLOBAL, device=-1)
+    sa, sb = a.stats(), b.stats()
+    assert sa["x_strip"] == scmod.STRIP_SHARED and sb["x_strip"] == scmod.STRIP_GLOBAL
+    for k in ("flops_trsm_useful", "flops_syrk_useful", "flops_trsm_executed", "flops_syrk_executed", "bytes_X",
+              "trsm_steps", "syrk_tasks"):
+        assert sa[k] == sb[k], k
+    for i, sd in enumerate(subs):
+        for col in range(0, sd.m, 16):
+            assert np.array_equal(a.strip_rows(i, col), b.strip_rows(i, col))
 
 
 def test_not_fill_closed_pattern_rejected():
