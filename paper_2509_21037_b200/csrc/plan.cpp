@@ -26,6 +26,8 @@
 #include <cstring>
 #include <iterator>
 #include <numeric>
+#include <atomic>
+#include <thread>
 #include <unordered_map>
 
 #include "sc_internal.h"
@@ -125,8 +127,8 @@ int relax_wsmall() {
 }
 
 // Steps 2-7 for one class.
-sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, int skip, bool gstrip, ClassPlan& C,
-                        std::string& err) {
+sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, int skip, bool gstrip,
+                        int32_t strip_limit, ClassPlan& C, std::string& err) {
   const int32_t n = d.n, m = d.m;
   C.n = n;
   C.m = m;
@@ -369,7 +371,16 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
       for (int32_t p = 0; p < np; p++)
         if (C.panels[(size_t)p].a + C.panels[(size_t)p].kw > from) tp.push_back(p);
     }
+    int32_t rows = 0;
+    for (int32_t p : tp) rows += C.panels[(size_t)p].kw;
+    C.max_strip_rows = std::max(C.max_strip_rows, rows);
     C.tiles.push_back(t);
+  }
+  // a shared-memory strip that cannot fit: stop here (the planner picks another tile width or
+  // the global strip; the rest of the analysis would be discarded)
+  if (strip_limit >= 0 && C.max_strip_rows > strip_limit) {
+    C.too_big = true;
+    return SC_OK;
   }
 
   // --- 5/6. SYRK groups (kGroup columns: union of the member tiles' panels), and per tile the
@@ -379,6 +390,8 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
   const int32_t ngroups = (m + kGroup - 1) / kGroup;
   int64_t xoff = 0;
   int32_t J0 = 0;
+  std::vector<int32_t> gmark((size_t)np, -1);
+  std::vector<int64_t> gsrow_off((size_t)np, -1);
   for (int32_t g = 0; g < ngroups; g++) {
     Group G{};
     G.col0 = g * kGroup;
@@ -396,10 +409,30 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     int32_t grows = 0;
     for (int32_t p : gp) {
       C.greach.push_back({p, grows});
+      gmark[(size_t)p] = g;
       grows += C.panels[(size_t)p].kw;
     }
     G.reach_end = (int32_t)C.greach.size();
     G.strip_rows = grows;
+    // global strip: one row map per (group, panel), shared by the group's tiles.  R_p rows outside
+    // a tile's own reach but inside the group's receive exact-zero updates (Y vanishes on columns
+    // outside the reach, whose L rows hit only reach rows), so mapping them is harmless.
+    if (gstrip) {
+      for (int32_t q = G.reach_begin; q < G.reach_end; q++) strip_base[(size_t)C.greach[(size_t)q].panel] = C.greach[(size_t)q].off;
+      for (int32_t q = G.reach_begin; q < G.reach_end; q++) {
+        const Panel& P = C.panels[(size_t)C.greach[(size_t)q].panel];
+        gsrow_off[(size_t)C.greach[(size_t)q].panel] = (int64_t)C.srows.size();
+        for (int32_t k = 0; k < P.nchunk * kChunk; k++) {
+          uint16_t v = 0xFFFF;
+          if (k < P.nR) {
+            const int32_t r = C.Rrows[(size_t)(P.R_off + k)];
+            const int32_t qq = panel_of_col[(size_t)r];
+            if (gmark[(size_t)qq] == g) v = (uint16_t)(strip_base[(size_t)qq] + (r - C.panels[(size_t)qq].a));
+          }
+          C.srows.push_back(v);
+        }
+      }
+    }
     G.x_off = xoff;
     xoff += (int64_t)grows * kGroup;
     for (int32_t J = J0; J < J1; J++) {
@@ -427,6 +460,10 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
       for (int32_t s = t.step_begin; s < t.step_end; s++) {
         Step& st = C.steps[(size_t)s];
         const Panel& P = C.panels[(size_t)st.panel];
+        if (gstrip) {
+          st.srow_off = gsrow_off[(size_t)st.panel];
+          continue;
+        }
         st.srow_off = (int64_t)C.srows.size();
         for (int32_t k = 0; k < P.nchunk * kChunk; k++) {
           uint16_t v = 0xFFFF;
@@ -441,7 +478,6 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
       // global strips are zeroed over all rows of the group strip (rows outside this tile's reach
       // stay exactly zero in its columns)
       t.strip_rows = gstrip ? grows : rows;
-      C.max_strip_rows = std::max(C.max_strip_rows, rows);
       t.binit_begin = (int32_t)C.binit.size();
       for (int32_t a = t.col0; a < t.col0 + t.width; a++)
         for (auto& e : bcol[(size_t)C.sigma[(size_t)a]]) {
@@ -479,6 +515,10 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     J0 = J1;
   }
   C.x_doubles = xoff;
+  if (std::getenv("SC_DEBUG_PLAN"))
+    fprintf(stderr, "class n=%d m=%d T=%d gstrip=%d: panels %d tiles %zu steps %zu srows %zu Rrows %zu greach %zu binit %zu\n",
+            n, m, T, (int)gstrip, np, C.tiles.size(), C.steps.size(), C.srows.size(), C.Rrows.size(), C.greach.size(),
+            C.binit.size());
 
   // --- 6. SYRK output tiles I >= J over groups with their common-row segments
   for (int32_t I = 0; I < ngroups; I++)
@@ -575,21 +615,47 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   int32_t G0 = max_m > 512 ? 64 : 32;
   if (const char* e = std::getenv("SC_GROUP")) G0 = std::atoi(e);
   if (!(G0 == 16 || G0 == 32 || G0 == 64)) FAIL(SC_ERR_INVALID_ARG, "SC_GROUP must be 16, 32 or 64");
-  auto analyse_all = [&](int T, bool gstrip) -> sc_status {
+  // classes are independent: analysed on all host cores
+  auto analyse_all = [&](int T, bool gstrip, int32_t strip_limit) -> sc_status {
     P.T = T;
     P.G = std::max(G0, T);
     P.gstrip = gstrip;
-    for (size_t c = 0; c < P.classes.size(); c++) {
-      uint64_t h = P.classes[c].hash;
-      P.classes[c] = ClassPlan();
-      P.classes[c].hash = h;
-      sc_status st = analyse_class(sd[rep[c]], T, P.G, P.PW, opt.skip, gstrip, P.classes[c], err);
-      if (st != SC_OK) {
-        err = "subdomain " + std::to_string(rep[c]) + ": " + err;
-        return st;
+    const size_t nc = P.classes.size();
+    std::vector<sc_status> st(nc, SC_OK);
+    std::vector<std::string> errs(nc);
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+      for (size_t c = next++; c < nc; c = next++) {
+        uint64_t h = P.classes[c].hash;
+        P.classes[c] = ClassPlan();
+        P.classes[c].hash = h;
+        st[c] = analyse_class(sd[rep[c]], T, P.G, P.PW, opt.skip, gstrip, strip_limit, P.classes[c], errs[c]);
       }
-    }
+    };
+    const size_t nthr = std::min<size_t>(nc, std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (size_t k = 1; k < nthr; k++) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    for (size_t c = 0; c < nc; c++)
+      if (st[c] != SC_OK) {
+        err = "subdomain " + std::to_string(rep[c]) + ": " + errs[c];
+        return st[c];
+      }
     return SC_OK;
+  };
+  auto too_big = [&]() {
+    for (auto& C : P.classes)
+      if (C.too_big) return true;
+    return false;
+  };
+  // largest shared-memory strip (rows) that fits next to a ring of two of the largest L blocks a
+  // panel width of PW can produce
+  auto strip_limit_for = [&](int T) -> int32_t {
+    const int64_t kw4 = (P.PW + 3) & ~3;
+    const int64_t maxblk = std::max<int64_t>(block_ld(P.PW), kLdC) * kw4 * 8;
+    const int64_t fixed = (int64_t)trsm_smem_layout(T, (int)(2 * maxblk), 0, false).total;
+    return (int32_t)std::max<int64_t>(-1, ((int64_t)kSmemBudget - fixed) / (8 * strip_ld(T)));
   };
   // TRSM tile width: the widest of 32 / 16 / 8 whose largest X strip fits in shared memory next to
   // an L-block ring of at least two of the plan's largest blocks; the ring gets what is left (up
@@ -611,25 +677,25 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   };
   const int Tg = opt.tile_cols ? opt.tile_cols : 16;  // global-strip tile width
   if (opt.x_strip == SC_STRIP_GLOBAL) {
-    sc_status st = analyse_all(Tg, true);
+    sc_status st = analyse_all(Tg, true, -1);
     if (st != SC_OK) return st;
-  } else if (opt.tile_cols) {
-    sc_status st = analyse_all(opt.tile_cols, false);
-    if (st != SC_OK) return st;
-    if (opt.x_strip == SC_STRIP_AUTO && ring_for(opt.tile_cols) < 0) {
-      st = analyse_all(Tg, true);
-      if (st != SC_OK) return st;
-    }
   } else {
-    const int cand[3] = {32, 16, 8};
+    const int cand_auto[3] = {32, 16, 8};
+    const int* cand = opt.tile_cols ? &opt.tile_cols : cand_auto;
+    const int ncand = opt.tile_cols ? 1 : 3;
     bool fits = false;
-    for (int k = 0; k < 3 && !fits; k++) {
-      sc_status st = analyse_all(cand[k], false);
+    for (int k = 0; k < ncand && !fits; k++) {
+      // SC_STRIP_SHARED with an explicit tile width analyses fully and reports the misfit below
+      const bool force = opt.x_strip == SC_STRIP_SHARED && opt.tile_cols;
+      sc_status st = analyse_all(cand[k], false, force ? -1 : strip_limit_for(cand[k]));
       if (st != SC_OK) return st;
-      fits = ring_for(cand[k]) > 0;
+      fits = !too_big() && ring_for(cand[k]) > 0;
     }
     if (!fits && opt.x_strip == SC_STRIP_AUTO) {
-      sc_status st = analyse_all(Tg, true);
+      sc_status st = analyse_all(Tg, true, -1);
+      if (st != SC_OK) return st;
+    } else if (!fits) {
+      sc_status st = analyse_all(cand[ncand - 1], false, -1);  // full analysis for the error report
       if (st != SC_OK) return st;
     }
   }

@@ -157,6 +157,7 @@ struct ClassPlan {
   int64_t x_doubles = 0;           // X region (group strips) per subdomain
   int64_t pb_doubles = 0;          // panel buffer per subdomain
   int32_t max_strip_rows = 0;      // over TRSM tiles
+  bool too_big = false;            // analysis stopped: a strip exceeds the shared-memory limit
   // counters (per subdomain of this class)
   double fl_trsm_useful = 0, fl_syrk_useful = 0, fl_trsm_env = 0, fl_syrk_env = 0;
   double fl_trsm_dense = 0, fl_syrk_dense = 0, fl_trsm_sparse = 0;
