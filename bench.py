@@ -161,6 +161,8 @@ def main():
     ap.add_argument("--skip", default="exact", choices=["none", "envelope", "exact"])
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--panel", type=int, default=0)
+    ap.add_argument("--strip", default="auto", choices=["auto", "shared", "global"],
+                    help="where TRSM tiles keep their X strip (sc_options.x_strip)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -190,7 +192,7 @@ def main():
     P = config_problem(args.config, seed=rank)
     skip = {"none": 0, "envelope": 1, "exact": 2}[args.skip]
     plan = SCPlan(P.subdomains, n_lambda=P.n_lambda, skip=skip, tile_cols=args.tile, panel_cols=args.panel,
-                  device=local)
+                  device=local, x_strip={"auto": 0, "shared": 1, "global": 2}[args.strip])
     t_plan = time.perf_counter() - t_plan0
     st = plan.stats()
     Ls = [torch.from_numpy(np.ascontiguousarray(sd.L_values)).cuda() for sd in P.subdomains]
@@ -343,6 +345,7 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CFG_DESC[args.config], "name": args.config, "subdomains_per_gpu": nsub,
                    "skip": args.skip, "tile_cols": st["tile_cols"], "panel_cols": st["panel_cols"],
+                   "x_strip": {1: "shared", 2: "global"}.get(st["x_strip"], "?"),
                    "parallelism": f"subdomain-sharded x{world} (no collective in assembly)",
                    "l2": f"inputs larger than L2: L values {st['bytes_L_values'] / 1e9:.2f} GB, "
                          f"X {st['bytes_X'] / 1e9:.2f} GB, F {8 * sum(m * m for m in plan.m) / 1e9:.2f} GB per GPU"},

@@ -80,7 +80,7 @@ typedef struct {
   int32_t precision;         /* 64 (FP64).  Other values -> SC_ERR_INVALID_ARG in this version     */
   int32_t skip;              /* SC_SKIP_*                                                          */
   int32_t tile_cols;         /* T: RHS column-tile width 8, 16, 32 or 64; 0 = automatic (widest whose
-                                X strip fits in shared memory; 16 for global strips)                */
+                                X strip fits in shared memory, 32 or 16; 32 for global strips)       */
   int32_t panel_cols;        /* max factor panel width (factor-splitting block), <= 64; 0 = 64      */
   int64_t n_lambda_global;   /* length of the global dual vector used by sc_apply                   */
   int32_t device;            /* CUDA device ordinal; -1 = host-only plan (symbolic + stats only)    */

@@ -545,9 +545,12 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
       int xcol[WN];
 #pragma unroll
       for (int j = 0; j < WN; j++) xcol[j] = xi(row0 + t4, (bc0 + j) * 8 + g) - (row0 + t4) * LDX;
+      // k steps in warp-uniform groups of 4 (16 columns): a narrow panel issues only the DMMAs of
+      // its own width (per-k-step predication alone would issue all 16 k steps of a full panel)
       if (br0 * 8 < kw4) {
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) {
+          if (ks % 4 == 0 && 4 * ks >= kend) break;
           if (4 * ks < kend) {
             double a[WM], bb[WN];
 #pragma unroll
@@ -623,6 +626,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
             for (int j = 0; j < WN; j++) acc[h][i][j][0] = acc[h][i][j][1] = 0.0;
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) {
+          if (ks % 4 == 0 && 4 * ks >= kw4) break;  // warp-uniform exit per group of 4 k steps
           if (4 * ks < kw4) {
             double a[WM];
 #pragma unroll

@@ -119,7 +119,7 @@ sc_status validate_desc(const sc_subdomain_desc& d, int32_t i, std::string& err)
 // environment variables SC_RELAX_ZMAX / SC_RELAX_WSMALL for tuning experiments.
 double relax_zmax() {
   const char* e = std::getenv("SC_RELAX_ZMAX");
-  return e ? std::atof(e) : 0.5;
+  return e ? std::atof(e) : 0.2;
 }
 int relax_wsmall() {
   const char* e = std::getenv("SC_RELAX_WSMALL");
@@ -515,6 +515,60 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     J0 = J1;
   }
   C.x_doubles = xoff;
+  if (std::getenv("SC_DEBUG_LIVE") && !gstrip) {
+    // frontal-stack experiment: max rows live at once per tile, B injected upfront / at own step
+    std::vector<int32_t> first((size_t)np), ownstep((size_t)np);
+    double sum_up = 0, sum_own = 0, sum_all = 0;
+    int mx_up = 0, mx_own = 0;
+    for (auto& t : C.tiles) {
+      if (t.step_end <= t.step_begin) continue;
+      for (int32_t s2 = t.step_begin; s2 < t.step_end; s2++) {
+        first[(size_t)C.steps[(size_t)s2].panel] = s2;
+        ownstep[(size_t)C.steps[(size_t)s2].panel] = s2;
+      }
+      std::vector<int32_t> firstB = first;
+      for (int32_t q = t.binit_begin; q < t.binit_end; q++) {
+        // B entry row -> panel: find the step whose strip rows contain it
+        const int32_t sr = C.binit[(size_t)q].strip_row;
+        for (int32_t s2 = t.step_begin; s2 < t.step_end; s2++) {
+          const Step& st = C.steps[(size_t)s2];
+          if (sr >= st.strip_row && sr < st.strip_row + C.panels[(size_t)st.panel].kw) firstB[(size_t)st.panel] = t.step_begin;
+        }
+      }
+      for (int32_t s2 = t.step_begin; s2 < t.step_end; s2++) {
+        const Step& st = C.steps[(size_t)s2];
+        const Panel& P = C.panels[(size_t)st.panel];
+        for (int32_t k = 0; k < P.nR; k++) {
+          const uint16_t v = C.srows[(size_t)(st.srow_off + k)];
+          if (v == 0xFFFF) continue;
+          for (int32_t s3 = s2; s3 < t.step_end; s3++) {
+            const Step& st3 = C.steps[(size_t)s3];
+            if (v >= st3.strip_row && v < st3.strip_row + C.panels[(size_t)st3.panel].kw) {
+              first[(size_t)st3.panel] = std::min(first[(size_t)st3.panel], s2);
+              firstB[(size_t)st3.panel] = std::min(firstB[(size_t)st3.panel], s2);
+              break;
+            }
+          }
+        }
+      }
+      int m_up = 0, m_own = 0;
+      for (int32_t s2 = t.step_begin; s2 < t.step_end; s2++) {
+        int l_up = 0, l_own = 0;
+        for (int32_t s3 = t.step_begin; s3 < t.step_end; s3++) {
+          const int32_t q = C.steps[(size_t)s3].panel;
+          const int kw = C.panels[(size_t)q].kw;
+          if (firstB[(size_t)q] <= s2 && s2 <= ownstep[(size_t)q]) l_up += kw;
+          if (first[(size_t)q] <= s2 && s2 <= ownstep[(size_t)q]) l_own += kw;
+        }
+        m_up = std::max(m_up, l_up);
+        m_own = std::max(m_own, l_own);
+      }
+      sum_up += m_up; sum_own += m_own; sum_all += t.strip_rows;
+      mx_up = std::max(mx_up, m_up); mx_own = std::max(mx_own, m_own);
+    }
+    fprintf(stderr, "live rows: strip mean %.0f max %d | live(B upfront) mean %.0f max %d | live(B at own step) mean %.0f max %d\n",
+            sum_all / C.tiles.size(), C.max_strip_rows, sum_up / C.tiles.size(), mx_up, sum_own / C.tiles.size(), mx_own);
+  }
   if (std::getenv("SC_DEBUG_PLAN"))
     fprintf(stderr, "class n=%d m=%d T=%d gstrip=%d: panels %d tiles %zu steps %zu srows %zu Rrows %zu greach %zu binit %zu\n",
             n, m, T, (int)gstrip, np, C.tiles.size(), C.steps.size(), C.srows.size(), C.Rrows.size(), C.greach.size(),
@@ -584,7 +638,6 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
         if (sd[i].lambda_map[a] < 0 || sd[i].lambda_map[a] >= opt.n_lambda_global)
           FAIL(SC_ERR_INVALID_ARG, "subdomain " + std::to_string(i) + ": lambda_map entry outside [0, n_lambda_global)");
   }
-  P.PW = opt.panel_cols ? opt.panel_cols : kMaxPanel;
 
   // --- classes (dedup identical patterns); the TRSM tile width is chosen so the largest X strip
   // fits in shared memory (T = 32 when possible, else 16; tile_cols forces a width)
@@ -613,6 +666,9 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   int32_t max_m = 0;
   for (int32_t i = 0; i < nsub; i++) max_m = std::max(max_m, sd[i].m);
   int32_t G0 = max_m > 512 ? 64 : 32;
+  // factor panel width: 64 for large operators (3D: wide separators, DMMA-bound); 32 for small ones
+  // (2D: narrow supernodes, latency-bound; narrower L blocks leave shared memory for T = 32 strips)
+  P.PW = opt.panel_cols ? opt.panel_cols : (max_m > 512 ? kMaxPanel : 32);
   if (const char* e = std::getenv("SC_GROUP")) G0 = std::atoi(e);
   if (!(G0 == 16 || G0 == 32 || G0 == 64)) FAIL(SC_ERR_INVALID_ARG, "SC_GROUP must be 16, 32 or 64");
   // classes are independent: analysed on all host cores
@@ -675,14 +731,18 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     int64_t ring = std::min<int64_t>(kRingMaxBytes, (int64_t)kSmemBudget - fixed) & ~(int64_t)127;
     return ring >= 2 * maxblk ? ring : -1;
   };
-  const int Tg = opt.tile_cols ? opt.tile_cols : 16;  // global-strip tile width
+  // global-strip tile width: 32 (measured on cfg4 / cfg5: 16 and 64 are slower)
+  const int Tg = opt.tile_cols ? opt.tile_cols : 32;
   if (opt.x_strip == SC_STRIP_GLOBAL) {
     sc_status st = analyse_all(Tg, true, -1);
     if (st != SC_OK) return st;
   } else {
+    // automatic: a shared-memory strip of 32 or 16 columns if it fits, else (AUTO) the global strip
+    // at T = 32, which beats a shared strip of only 8 columns (cfg4: TRSM 67 vs 81 ms); an explicit
+    // SC_STRIP_SHARED request still falls back to T = 8
     const int cand_auto[3] = {32, 16, 8};
     const int* cand = opt.tile_cols ? &opt.tile_cols : cand_auto;
-    const int ncand = opt.tile_cols ? 1 : 3;
+    const int ncand = opt.tile_cols ? 1 : (opt.x_strip == SC_STRIP_SHARED ? 3 : 2);
     bool fits = false;
     for (int k = 0; k < ncand && !fits; k++) {
       // SC_STRIP_SHARED with an explicit tile width analyses fully and reports the misfit below
