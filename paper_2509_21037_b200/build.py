@@ -22,11 +22,15 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str = "", defines=()) -> str:
+    """out/defines: variant builds for A/B measurements (e.g. libsc_b200_wn2.so with -DSC_WN16=2)."""
+    global LIB
+    if out:
+        LIB = os.path.join(HERE, out)
     if not force and not _stale():
         return LIB
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC,-O3",
-           "-I", os.path.join(ROOT, "include"), "-I", CSRC, "-Xptxas", "-v" if verbose else "-O3",
+           "-I", os.path.join(ROOT, "include"), "-I", CSRC, *[f"-D{d}" for d in defines], "-Xptxas", "-v" if verbose else "-O3",
            "-o", LIB + ".tmp", *[os.path.join(CSRC, s) for s in SOURCES], "-lcudart", "-lpthread"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
@@ -39,5 +43,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
+    # python build.py [-v] [out=libname.so] [NAME=VALUE ...]  (defines for variant builds)
+    extra = [a for a in sys.argv[1:] if a != "-v"]
+    outs = [a[4:] for a in extra if a.startswith("out=")]
+    build(force=True, verbose="-v" in sys.argv, out=outs[0] if outs else "",
+          defines=[a for a in extra if not a.startswith("out=")])
     print(LIB)

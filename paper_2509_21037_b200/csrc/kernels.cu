@@ -338,6 +338,12 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
 // ------------------------------------------------------------------------------------------------
 static_assert(kLdC == block_ld(kChunk), "chunk ld");
 
+#ifndef SC_WN16
+#define SC_WN16 1
+#endif
+#ifndef SC_WN32
+#define SC_WN32 1
+#endif
 template <int T>
 struct TileCfg {
   static constexpr int LDX = strip_ld(T);       // strip / Y row stride in doubles
@@ -347,7 +353,7 @@ struct TileCfg {
   // (8 / warp rows) row blocks per warp
   static constexpr int NCW = 8;
   static constexpr int CT = NCW * 32;           // consumer threads
-  static constexpr int WN = 1;                  // column blocks per warp
+  static constexpr int WN = T >= 32 ? SC_WN32 : (T == 16 ? SC_WN16 : 1);  // column blocks per warp
   static constexpr int NWC = NB / WN;           // warps along the columns
   static constexpr int WM = 8 * NWC / NCW;      // row blocks per warp
   static_assert(WM >= 1 && (NCW / NWC) * WM == 8, "warp tiling must cover 64 rows");

@@ -13,7 +13,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsc_b200.so")
+# SC_B200_LIB: alternative in-tree build for A/B measurements (tools/); default the in-tree library
+LIB_PATH = os.environ.get("SC_B200_LIB") or os.path.join(HERE, "libsc_b200.so")
 
 SC_OK, SC_ERR_INVALID_ARG, SC_ERR_PATTERN, SC_ERR_ZERO_PIVOT, SC_ERR_OOM, SC_ERR_CUDA, SC_ERR_STATE = range(7)
 SKIP_NONE, SKIP_ENVELOPE, SKIP_EXACT = 0, 1, 2
