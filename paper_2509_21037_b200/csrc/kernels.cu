@@ -153,6 +153,52 @@ __device__ __forceinline__ void zero_chunk_gaps(double* PB, const Panel& pn, int
   }
 }
 
+
+// W_p = L[R_p, p] inv(L_pp), in place on the panel's chunks (called after the scatter and the
+// inversion, with the scatter's global writes visible to the calling threads): one 8-row block of
+// one chunk per warp item; the whole row block is loaded before it is overwritten.  Winv: inverse
+// in shared memory, column-major with stride LDW (zero above the diagonal, unit padding).
+template <int LDW, int NPAD>
+__device__ __forceinline__ void chunks_times_inverse(double* __restrict__ PB, const Panel& pn, const double* Winv,
+                                                     int item0, int nitem_step, int lane) {
+  if (pn.nchunk == 0) return;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int kw4 = pn.kw4;
+  double* c0 = PB + pn.buf_off + (int64_t)pn.ldD * kw4;
+  constexpr int KSN = NPAD / 4;
+  for (int item = item0; item < pn.nchunk * 8; item += nitem_step) {
+    const int c = item >> 3, rb = item & 7;
+    const int rows_c = min(kChunk, pn.nR - c * kChunk);
+    if (rb * 8 >= rows_c) continue;
+    const int ld = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
+    double* blk = c0 + (int64_t)c * kLdC * kw4;
+    const int row = rb * 8 + g;
+    const bool ok = row < rows_c;
+    double a[KSN];
+#pragma unroll
+    for (int ks = 0; ks < KSN; ks++) a[ks] = (ok && 4 * ks < kw4) ? blk[(4 * ks + t4) * ld + row] : 0.0;
+    __syncwarp();
+#pragma unroll
+    for (int cb = 0; cb < NPAD / 8; cb++) {
+      if (cb * 8 >= kw4) break;
+      double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
+#pragma unroll
+      for (int ks = 2 * cb; ks < KSN; ks++) {  // inv lower triangular: k >= 8 cb
+        if (ks % 4 == 0 && 4 * ks >= kw4) break;
+        if (4 * ks < kw4) {
+          const double bv = Winv[(cb * 8 + g) * LDW + 4 * ks + t4];
+          if (ks & 1) dmma(o0, o1, a[ks], bv);
+          else dmma(e0, e1, a[ks], bv);
+        }
+      }
+      if (ok && cb * 8 + 2 * t4 < kw4) {  // kw4 is a multiple of 4, not of 8
+        blk[(cb * 8 + 2 * t4) * ld + row] = e0 + o0;
+        blk[(cb * 8 + 2 * t4 + 1) * ld + row] = e1 + o1;
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
   extern __shared__ __align__(16) unsigned char prep_smem[];
   double* D = reinterpret_cast<double*>(prep_smem);  // triangle, then temporaries
@@ -239,6 +285,8 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
     const int j = q / ldD, i = q - j * ldD;
     Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * kLdT + i] : 0.0;
   }
+  // chunks: L[R_p, p] -> W_p = L[R_p, p] inv(L_pp) (the TRSM's update operand)
+  chunks_times_inverse<kLdT, kMaxPanel>(PB, pn, W, warp, kThreads / 32, lane);
 }
 
 
@@ -330,6 +378,7 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
     const int j = q / ldD, i = q - j * ldD;
     Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * LD + i] : 0.0;
   }
+  chunks_times_inverse<LD, NPAD>(PB, pn, W, 0, 1, lane);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -378,67 +427,103 @@ __device__ __forceinline__ void consumer_sync() {  // named barrier over the NT 
   asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
 }
 
-// Producer (one lane): walks the tile's block stream [inv(L_pp), chunk 0, chunk 1, ...] per step,
-// issues each block with cp.async.bulk into the ring as soon as a slot and the bytes are free; a
-// chunk block travels with its 64 precomputed strip rows (128 B, same mbarrier).
+// Per-slot record written by the producer before it arms the slot's full barrier (the consumers
+// read it after their wait): ring offset of the block and, for a step's first block (inv(L_pp)),
+// the step's panel geometry, so the consumers never fetch descriptors from global memory.
+struct SlotRec {
+  int32_t off, kw, kw4, ldD, nchunk, nR, ldLast, strip_row, grow, pad[3];
+};
+static_assert(sizeof(SlotRec) == 48, "slot record");
+
+// Producer (the whole warp): walks the tile's block stream [inv(L_pp), chunk 0, chunk 1, ...] per
+// step.  Step / panel descriptors are fetched 32 steps at a time (lane l loads step s0 + l, so the
+// dependent global loads overlap) and broadcast with shuffles; lane 0 issues each block with
+// cp.async.bulk into the byte ring as soon as a slot and the bytes are free.  A chunk block travels
+// with its 64 precomputed strip rows (128 B, same mbarrier).
 __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, const double* PB, unsigned char* ring,
-                                           uint64_t* full, uint64_t* empty, int32_t* off, uint16_t* srow) {
-  int q_slot[kSlots], q_start[kSlots];  // FIFO of in-flight blocks
+                                           uint64_t* full, uint64_t* empty, SlotRec* rec, uint16_t* srow, int lane) {
+  int q_slot[kSlots], q_start[kSlots];  // FIFO of in-flight blocks (identical in every lane)
   int q_head = 0, inflight = 0, ring_head = 0, ring_tail = 0;
   int b = 0;
-  for (int s = tile.step_begin; s < tile.step_end; s++) {
-    const Step st = P.steps[s];
-    const Panel pn = P.panels[st.panel];
-    for (int c = -1; c < pn.nchunk; c++, b++) {
-      const double* src;
-      int bytes;
-      if (c < 0) {
-        src = PB + pn.buf_off;
-        bytes = pn.ldD * pn.kw4 * 8;
-      } else {
-        src = PB + pn.buf_off + (int64_t)pn.ldD * pn.kw4 + (int64_t)c * kLdC * pn.kw4;
-        bytes = ((c == pn.nchunk - 1) ? pn.ldLast : kLdC) * pn.kw4 * 8;
-      }
-      // wait until a slot and `bytes` contiguous ring bytes are free (pop oldest in-flight blocks)
-      int start = 0;
-      while (true) {
-        bool ok = false;
-        if (inflight == 0) {
-          ring_head = ring_tail = 0;
-          start = 0;
-          ok = true;
-        } else if (inflight < kSlots) {
-          if (ring_tail > ring_head) {
-            if (P.ring_bytes - ring_tail >= bytes) {
+  for (int s0 = tile.step_begin; s0 < tile.step_end; s0 += 32) {
+    Step stl{};
+    Panel pnl{};
+    if (s0 + lane < tile.step_end) {
+      stl = P.steps[s0 + lane];
+      pnl = P.panels[stl.panel];
+    }
+    const int cnt = min(32, tile.step_end - s0);
+    for (int k = 0; k < cnt; k++) {
+      const int64_t buf_off = __shfl_sync(0xffffffffu, pnl.buf_off, k);
+      const int64_t srow_off = __shfl_sync(0xffffffffu, stl.srow_off, k);
+      const int kw = __shfl_sync(0xffffffffu, pnl.kw, k), kw4 = __shfl_sync(0xffffffffu, pnl.kw4, k);
+      const int ldD = __shfl_sync(0xffffffffu, pnl.ldD, k), nchunk = __shfl_sync(0xffffffffu, pnl.nchunk, k);
+      const int nR = __shfl_sync(0xffffffffu, pnl.nR, k), ldLast = __shfl_sync(0xffffffffu, pnl.ldLast, k);
+      const int strip_row = __shfl_sync(0xffffffffu, stl.strip_row, k), grow = __shfl_sync(0xffffffffu, stl.grow, k);
+      for (int c = -1; c < nchunk; c++, b++) {
+        const double* src;
+        int bytes;
+        if (c < 0) {
+          src = PB + buf_off;
+          bytes = ldD * kw4 * 8;
+        } else {
+          src = PB + buf_off + (int64_t)ldD * kw4 + (int64_t)c * kLdC * kw4;
+          bytes = ((c == nchunk - 1) ? ldLast : kLdC) * kw4 * 8;
+        }
+        // wait until a slot and `bytes` contiguous ring bytes are free (pop oldest in-flight blocks)
+        int start = 0;
+        while (true) {
+          bool ok = false;
+          if (inflight == 0) {
+            ring_head = ring_tail = 0;
+            start = 0;
+            ok = true;
+          } else if (inflight < kSlots) {
+            if (ring_tail > ring_head) {
+              if (P.ring_bytes - ring_tail >= bytes) {
+                start = ring_tail;
+                ok = true;
+              } else if (ring_head >= bytes) {
+                start = 0;
+                ok = true;
+              }
+            } else if (ring_tail < ring_head && ring_head - ring_tail >= bytes) {
               start = ring_tail;
               ok = true;
-            } else if (ring_head >= bytes) {
-              start = 0;
-              ok = true;
             }
-          } else if (ring_tail < ring_head && ring_head - ring_tail >= bytes) {
-            start = ring_tail;
-            ok = true;
           }
+          if (ok) break;
+          const int os = q_slot[q_head];
+          mbar_wait(&empty[os], (uint32_t)((b - inflight) / kSlots) & 1u);
+          q_head = (q_head + 1) % kSlots;
+          inflight--;
+          ring_head = inflight ? q_start[q_head] : ring_tail;
         }
-        if (ok) break;
-        const int os = q_slot[q_head];
-        mbar_wait(&empty[os], (uint32_t)((b - inflight) / kSlots) & 1u);
-        q_head = (q_head + 1) % kSlots;
-        inflight--;
-        ring_head = inflight ? q_start[q_head] : ring_tail;
+        const int slot = b % kSlots;
+        const int qi = (q_head + inflight) % kSlots;
+        q_slot[qi] = slot;
+        q_start[qi] = start;
+        inflight++;
+        ring_tail = start + bytes;
+        if (lane == 0) {
+          SlotRec& r = rec[slot];
+          r.off = start;
+          if (c < 0) {
+            r.kw = kw;
+            r.kw4 = kw4;
+            r.ldD = ldD;
+            r.nchunk = nchunk;
+            r.nR = nR;
+            r.ldLast = ldLast;
+            r.strip_row = strip_row;
+            r.grow = grow;
+          }
+          const uint32_t rb = (c >= 0) ? (uint32_t)(kChunk * sizeof(uint16_t)) : 0u;
+          mbar_expect_tx(&full[slot], (uint32_t)bytes + rb);
+          bulk_g2s(ring + start, src, (uint32_t)bytes, &full[slot]);
+          if (c >= 0) bulk_g2s(srow + slot * kChunk, P.srows + srow_off + (int64_t)c * kChunk, rb, &full[slot]);
+        }
       }
-      const int slot = b % kSlots;
-      const int qi = (q_head + inflight) % kSlots;
-      q_slot[qi] = slot;
-      q_start[qi] = start;
-      inflight++;
-      ring_tail = start + bytes;
-      off[slot] = start;
-      const uint32_t rb = (c >= 0) ? (uint32_t)(kChunk * sizeof(uint16_t)) : 0u;
-      mbar_expect_tx(&full[slot], (uint32_t)bytes + rb);
-      bulk_g2s(ring + start, src, (uint32_t)bytes, &full[slot]);
-      if (c >= 0) bulk_g2s(srow + slot * kChunk, P.srows + st.srow_off + (int64_t)c * kChunk, rb, &full[slot]);
     }
   }
 }
@@ -456,10 +541,9 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
   const TrsmSmem L = trsm_smem_layout(T, P.ring_bytes, P.strip_cap, GS);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem_raw + L.empty);
-  int32_t* off = reinterpret_cast<int32_t*>(smem_raw + L.off);
+  SlotRec* rec = reinterpret_cast<SlotRec*>(smem_raw + L.off);
   uint16_t* srow = reinterpret_cast<uint16_t*>(smem_raw + L.srow);
   unsigned char* ring = smem_raw + L.ring;
-  double* Ys = reinterpret_cast<double*>(smem_raw + L.ys);
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const I2 task = P.trsm_tasks[blockIdx.x];
@@ -493,7 +577,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
   }
   __syncthreads();
   if (warp == Cfg::NCW) {  // ---- TMA producer warp
-    if (lane == 0) trsm_producer(P, tile, PB, ring, full, empty, off, srow);
+    trsm_producer(P, tile, PB, ring, full, empty, rec, srow, lane);
     return;
   }
 
@@ -517,22 +601,45 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
   }
   consumer_sync<CT>();
 
-  // ---- stepped supernodal TRSM (row a3); two consumer barriers per factor panel
+  // ---- stepped supernodal TRSM (row a3).  With W_p = L[R_p, p] inv(L_pp) prepared once per
+  // subdomain, step p is two independent products of the SAME operand X_p (final after the earlier
+  // steps):  X_p <- inv(L_pp) X_p  and  X[R_p] -= W_p X_p.  No barrier separates them; the solved
+  // rows go straight to the group strip in HBM (they are never read again by this tile), and one
+  // barrier per step among the warps of a column block orders the R_p updates before the next
+  // panel reads its rows.
+  const int cgrp = warp % NWC;  // column-block group: the warps that touch these T / NWC columns
+  Group Gt;
+  double* Xg = nullptr;         // this tile's columns of its group strip (shared-strip mode)
+  if constexpr (!GS) {
+    Gt = P.groups[tile.group];
+    Xg = P.X + P.sub_X_base[sub] + Gt.x_off + tile.col_in_group;
+  }
   int b = 0;  // block counter (same order as the producer)
-  Step st_next = P.steps[tile.step_begin < tile.step_end ? tile.step_begin : 0];
-  Panel pn_next = P.panels[st_next.panel];
   for (int s = tile.step_begin; s < tile.step_end; s++, b++) {
-    const Step st = st_next;
-    const Panel pn = pn_next;
-    if (s + 1 < tile.step_end) {  // descriptors of the next panel, off the critical path
-      st_next = P.steps[s + 1];
-      pn_next = P.panels[st_next.panel];
-    }
+    // the step's geometry arrives with its first block (inv(L_pp))
+    const int slot0 = b % kSlots;
+    mbar_wait(&full[slot0], (uint32_t)(b / kSlots) & 1u);
+    const SlotRec pn = rec[slot0];
     const int kw = pn.kw, kw4 = pn.kw4;
-    const int row0 = st.strip_row;
-    // Y = inv(L_pp) X_p  (inv(L_pp) lower triangular: row block i needs k < 8 (i + 1)); two
-    // accumulators per output block (even / odd k steps) for DMMA latency hiding
-    double yacc[WM][WN][2];
+    const int row0 = pn.strip_row;
+    // B operand: X_p (rows row0 + 4 ks + t4 share (row & 3), hence one swizzled column per j).  A
+    // global strip has no zero pad rows past the last panel: rows >= kw are read as 0.
+    double yf[KS][WN];
+    {
+      const double* xb = Xs + (row0 + t4) * LDX;
+#pragma unroll
+      for (int j = 0; j < WN; j++) {
+        const int xcol = xi(row0 + t4, (bc0 + j) * 8 + g) - (row0 + t4) * LDX;
+#pragma unroll
+        for (int ks = 0; ks < KS; ks++) {
+          if (ks % 4 == 0 && 4 * ks >= kw4) break;
+          yf[ks][j] = (4 * ks < kw4 && (!GS || 4 * ks + t4 < kw)) ? xb[(4 * ks) * LDX + xcol] : 0.0;
+        }
+      }
+    }
+    // X_p <- inv(L_pp) X_p for this warp's row blocks (inv lower triangular: row block i needs
+    // k < 8 (i + 1)); kept in registers until the step's barrier
+    double yn[WM][WN][2];
     {
       double ya[2][WM][WN][2];
 #pragma unroll
@@ -541,69 +648,44 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
         for (int i = 0; i < WM; i++)
 #pragma unroll
           for (int j = 0; j < WN; j++) ya[h][i][j][0] = ya[h][i][j][1] = 0.0;
-      const int slot = b % kSlots;
-      mbar_wait(&full[slot], (uint32_t)(b / kSlots) & 1u);
-      const double* A = reinterpret_cast<const double*>(ring + off[slot]);
+      const int slot = slot0;
+      const double* A = reinterpret_cast<const double*>(ring + pn.off);
       const int ld = pn.ldD;
       const int kend = min(kw4, (br0 + WM) * 8);
-      // rows row0 + 4 ks + t4 all share (row & 3), hence one swizzled column per j
-      const double* xb = Xs + (row0 + t4) * LDX;
-      int xcol[WN];
-#pragma unroll
-      for (int j = 0; j < WN; j++) xcol[j] = xi(row0 + t4, (bc0 + j) * 8 + g) - (row0 + t4) * LDX;
-      // k steps in warp-uniform groups of 4 (16 columns): a narrow panel issues only the DMMAs of
-      // its own width (per-k-step predication alone would issue all 16 k steps of a full panel)
       if (br0 * 8 < kw4) {
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) {
           if (ks % 4 == 0 && 4 * ks >= kend) break;
           if (4 * ks < kend) {
-            double a[WM], bb[WN];
+            double a[WM];
 #pragma unroll
             for (int i = 0; i < WM; i++) a[i] = A[(4 * ks + t4) * ld + (br0 + i) * 8 + g];
 #pragma unroll
-            for (int j = 0; j < WN; j++)  // a global strip has no zero pad rows past the last panel
-              bb[j] = (!GS || 4 * ks + t4 < kw) ? xb[(4 * ks) * LDX + xcol[j]] : 0.0;
-#pragma unroll
             for (int i = 0; i < WM; i++)
 #pragma unroll
-              for (int j = 0; j < WN; j++) dmma(ya[ks & 1][i][j][0], ya[ks & 1][i][j][1], a[i], bb[j]);
+              for (int j = 0; j < WN; j++) dmma(ya[ks & 1][i][j][0], ya[ks & 1][i][j][1], a[i], yf[ks][j]);
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
 #pragma unroll
-      for (int i = 0; i < WM; i++) {
-        const int r = (br0 + i) * 8 + g;
+      for (int i = 0; i < WM; i++)
 #pragma unroll
         for (int j = 0; j < WN; j++) {
-          yacc[i][j][0] = ya[0][i][j][0] + ya[1][i][j][0];
-          yacc[i][j][1] = ya[0][i][j][1] + ya[1][i][j][1];
-          if (r < kw4)
-            *reinterpret_cast<double2*>(Ys + Cfg::idx(r, (bc0 + j) * 8 + 2 * t4)) =
-                make_double2(yacc[i][j][0], yacc[i][j][1]);
+          yn[i][j][0] = ya[0][i][j][0] + ya[1][i][j][0];
+          yn[i][j][1] = ya[0][i][j][1] + ya[1][i][j][1];
         }
-      }
-      consumer_sync<CT>();  // Y visible to every warp
     }
-    // X[R_p] -= L[R_p, p] Y, one 64-row chunk (one ring block) at a time; chunks update disjoint
-    // rows and each warp releases its ring slot itself, so no barrier between chunks.  The warp's
-    // Y fragments stay in registers for all chunks of the panel: only L is read from shared memory.
-    double yf[KS][WN];
-#pragma unroll
-    for (int j = 0; j < WN; j++) {
-      const double* yb = Ys + Cfg::idx(t4, (bc0 + j) * 8 + g);  // rows 4 ks + t4 share the swizzle
-#pragma unroll
-      for (int ks = 0; ks < KS; ks++) yf[ks][j] = (4 * ks < kw4) ? yb[4 * ks * Cfg::LDX] : 0.0;
-    }
+    // X[R_p] -= W_p X_p, one 64-row chunk (one ring block) at a time; chunks update disjoint rows
+    // and each warp releases its ring slot itself
     for (int c = 0; c < pn.nchunk; c++) {
       b++;
       const int rows_c = min(kChunk, pn.nR - c * kChunk);
       const int ld = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
       const int slot = b % kSlots;
       mbar_wait(&full[slot], (uint32_t)(b / kSlots) & 1u);
-      const double* A = reinterpret_cast<const double*>(ring + off[slot]);
+      const double* A = reinterpret_cast<const double*>(ring + rec[slot].off);
       int sr[WM];
 #pragma unroll
       for (int i = 0; i < WM; i++) sr[i] = (int)srow[slot * kChunk + (br0 + i) * 8 + g];
@@ -673,31 +755,28 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
         }
       }
     }
-    // the panel's rows are final: X_p = Y (GEMM1's reads of X_p finished before the barrier above)
+    // the column-block group's R_p updates are visible before the next panel reads its rows, and
+    // every warp of the group has read X_p: store the solved rows (final) into the group strip
+    if constexpr (NWC == 1) {
+      consumer_sync<CT>();
+    } else {
+      asm volatile("bar.sync %0, %1;\n" ::"r"(2 + cgrp), "n"(CT / NWC) : "memory");  // ids 2..9
+    }
 #pragma unroll
     for (int i = 0; i < WM; i++) {
       const int r = (br0 + i) * 8 + g;
       if (r < kw) {
 #pragma unroll
-        for (int j = 0; j < WN; j++)
-          *reinterpret_cast<double2*>(Xs + xi(row0 + r, (bc0 + j) * 8 + 2 * t4)) =
-              make_double2(yacc[i][j][0], yacc[i][j][1]);
+        for (int j = 0; j < WN; j++) {
+          double* dst;
+          if constexpr (GS) {
+            dst = Xs + xi(row0 + r, (bc0 + j) * 8 + 2 * t4);
+          } else {
+            dst = Xg + (int64_t)(pn.grow + r) * P.G + (bc0 + j) * 8 + 2 * t4;
+          }
+          *reinterpret_cast<double2*>(dst) = make_double2(yn[i][j][0], yn[i][j][1]);
+        }
       }
-    }
-    consumer_sync<CT>();  // strip updates visible before the next panel reads its rows; Ys reusable
-  }
-
-  if constexpr (GS) return;  // solved in place
-  // ---- write the strip into the group strip (row-major, G columns) for the SYRK
-  const Group G = P.groups[tile.group];
-  double* __restrict__ Xg = P.X + P.sub_X_base[sub] + G.x_off + tile.col_in_group;
-  for (int w = tile.wseg_begin; w < tile.wseg_end; w++) {
-    const WSeg ws = P.wsegs[w];
-    for (int q = tid; q < ws.len * (T / 2); q += CT) {
-      const int r = q / (T / 2), j = 2 * (q - r * (T / 2));
-      double2 v = make_double2(0.0, 0.0);
-      if (ws.src >= 0) v = *reinterpret_cast<const double2*>(Xs + xi(ws.src + r, j));
-      *reinterpret_cast<double2*>(Xg + (int64_t)(ws.dst + r) * P.G + j) = v;
     }
   }
 }

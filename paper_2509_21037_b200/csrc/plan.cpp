@@ -442,14 +442,10 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
       int32_t rows = 0;
       size_t q = (size_t)G.reach_begin;
       for (int32_t p : tp) {
-        if (gstrip) {
-          while (C.greach[q].panel != p) q++;
-          strip_base[(size_t)p] = C.greach[q].off;
-        } else {
-          strip_base[(size_t)p] = rows;
-        }
+        while (C.greach[q].panel != p) q++;
+        strip_base[(size_t)p] = gstrip ? C.greach[q].off : rows;
         in_tile[(size_t)p] = J;
-        C.steps.push_back({p, strip_base[(size_t)p], 0});
+        C.steps.push_back({p, strip_base[(size_t)p], C.greach[q].off, 0, 0});
         const Panel& P = C.panels[(size_t)p];
         // GEMM1 skips the zero blocks above the diagonal of inv(L_pp)
         C.fl_trsm_exec += 2.0 * T * P.kw4 * (0.5 * (double)P.kw4 + 4.0 + (double)P.nR);

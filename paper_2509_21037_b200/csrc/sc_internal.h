@@ -46,11 +46,13 @@ SC_HD inline TrsmSmem trsm_smem_layout(int T, int ring_bytes, int strip_cap, boo
   TrsmSmem s{};
   s.full = 0;
   s.empty = 8 * kSlots;
-  s.off = 16 * kSlots;
-  s.srow = 512;
+  s.off = 16 * kSlots;            // per-slot records (48 B each, kernels.cu SlotRec)
+  s.srow = s.off + 48 * kSlots;
   s.ring = s.srow + sizeof(uint16_t) * kSlots * kChunk;
-  s.ys = s.ring + (size_t)ring_bytes;
-  s.strip = s.ys + sizeof(double) * (size_t)kMaxPanel * (size_t)strip_ld(T);
+  // 512 B guard after the ring: a warp's 8-row fragment loads of a block whose ld is below 64 may
+  // read up to 60 doubles past its end (rows that are never used)
+  s.ys = s.ring + (size_t)ring_bytes + 512;  // (no Y buffer: the solved panel stays in registers)
+  s.strip = s.ys;
   s.total = s.strip + (global_strip ? 0 : sizeof(double) * (size_t)(strip_cap + 4) * (size_t)strip_ld(T));
   return s;
 }
@@ -80,11 +82,13 @@ struct Tile {
   int32_t col_in_group, pad;
 };
 
-// TRSM step: tile visits panel `panel` (global index) whose rows start at `strip_row`.
+// TRSM step: tile visits panel `panel` (global index) whose rows start at `strip_row` (tile strip in
+// shared memory, or the group strip itself for global strips).
 // srow_off: offset (uint16 units, 64 per chunk) of the strip rows of R_p for this tile in srows[]
 // (0xFFFF = row outside the tile's reach, whose update is exactly zero).
 struct Step {
   int32_t panel, strip_row;
+  int32_t grow, pad;               // row of the panel in the tile's group strip (solved rows go there)
   int64_t srow_off;
 };
 
