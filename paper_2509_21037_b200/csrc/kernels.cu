@@ -162,38 +162,56 @@ template <int LDW, int NPAD>
 __device__ __forceinline__ void chunks_times_inverse(double* __restrict__ PB, const Panel& pn, const double* Winv,
                                                      int item0, int nitem_step, int lane) {
   if (pn.nchunk == 0) return;
+  // RB row blocks per pass (their loads in flight together); k outer, column blocks inner (NPAD / 8
+  // independent accumulator chains)
+  constexpr int RB = NPAD == 64 ? 1 : 4;
+  constexpr int KSN = NPAD / 4, NCB = NPAD / 8;
   const int g = lane >> 2, t4 = lane & 3;
   const int kw4 = pn.kw4;
   double* c0 = PB + pn.buf_off + (int64_t)pn.ldD * kw4;
-  constexpr int KSN = NPAD / 4;
-  for (int item = item0; item < pn.nchunk * 8; item += nitem_step) {
-    const int c = item >> 3, rb = item & 7;
-    const int rows_c = min(kChunk, pn.nR - c * kChunk);
-    if (rb * 8 >= rows_c) continue;
-    const int ld = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
-    double* blk = c0 + (int64_t)c * kLdC * kw4;
-    const int row = rb * 8 + g;
-    const bool ok = row < rows_c;
-    double a[KSN];
+  const int nitems = pn.nchunk * 8;
+  for (int base = item0; base < nitems; base += RB * nitem_step) {
+    double a[RB][KSN];
+    double* blk[RB];
+    int ld[RB], row[RB];
+    bool ok[RB];
 #pragma unroll
-    for (int ks = 0; ks < KSN; ks++) a[ks] = (ok && 4 * ks < kw4) ? blk[(4 * ks + t4) * ld + row] : 0.0;
-    __syncwarp();
+    for (int r = 0; r < RB; r++) {
+      const int item = base + r * nitem_step;
+      const int c = item >> 3, rb = item & 7;
+      const int rows_c = item < nitems ? min(kChunk, pn.nR - c * kChunk) : 0;
+      ld[r] = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
+      blk[r] = c0 + (int64_t)c * kLdC * kw4;
+      row[r] = rb * 8 + g;
+      ok[r] = row[r] < rows_c;
 #pragma unroll
-    for (int cb = 0; cb < NPAD / 8; cb++) {
-      if (cb * 8 >= kw4) break;
-      double e0 = 0.0, e1 = 0.0, o0 = 0.0, o1 = 0.0;
+      for (int ks = 0; ks < KSN; ks++) a[r][ks] = (ok[r] && 4 * ks < kw4) ? blk[r][(4 * ks + t4) * ld[r] + row[r]] : 0.0;
+    }
+    __syncwarp();  // every lane's loads of these rows precede any store into them
 #pragma unroll
-      for (int ks = 2 * cb; ks < KSN; ks++) {  // inv lower triangular: k >= 8 cb
+    for (int r = 0; r < RB; r++) {
+      if (!__any_sync(0xffffffffu, ok[r])) continue;
+      double acc[NCB][2];
+#pragma unroll
+      for (int cb = 0; cb < NCB; cb++) acc[cb][0] = acc[cb][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < KSN; ks++) {
         if (ks % 4 == 0 && 4 * ks >= kw4) break;
         if (4 * ks < kw4) {
-          const double bv = Winv[(cb * 8 + g) * LDW + 4 * ks + t4];
-          if (ks & 1) dmma(o0, o1, a[ks], bv);
-          else dmma(e0, e1, a[ks], bv);
+#pragma unroll
+          for (int cb = 0; cb <= ks / 2 && cb < NCB; cb++)  // inv lower triangular: k >= 8 cb
+            dmma(acc[cb][0], acc[cb][1], a[r][ks], Winv[(cb * 8 + g) * LDW + 4 * ks + t4]);
         }
       }
-      if (ok && cb * 8 + 2 * t4 < kw4) {  // kw4 is a multiple of 4, not of 8
-        blk[(cb * 8 + 2 * t4) * ld + row] = e0 + o0;
-        blk[(cb * 8 + 2 * t4 + 1) * ld + row] = e1 + o1;
+      if (ok[r]) {
+#pragma unroll
+        for (int cb = 0; cb < NCB; cb++) {
+          const int col = cb * 8 + 2 * t4;
+          if (col < kw4) {  // kw4 is a multiple of 4, not of 8
+            blk[r][col * ld[r] + row[r]] = acc[cb][0];
+            blk[r][(col + 1) * ld[r] + row[r]] = acc[cb][1];
+          }
+        }
       }
     }
   }
@@ -286,7 +304,7 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
     Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * kLdT + i] : 0.0;
   }
   // chunks: L[R_p, p] -> W_p = L[R_p, p] inv(L_pp) (the TRSM's update operand)
-  chunks_times_inverse<kLdT, kMaxPanel>(PB, pn, W, warp, kThreads / 32, lane);
+  if (P.wmode) chunks_times_inverse<kLdT, kMaxPanel>(PB, pn, W, warp, kThreads / 32, lane);
 }
 
 
@@ -378,7 +396,7 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
     const int j = q / ldD, i = q - j * ldD;
     Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * LD + i] : 0.0;
   }
-  chunks_times_inverse<LD, NPAD>(PB, pn, W, 0, 1, lane);
+  if (P.wmode) chunks_times_inverse<LD, NPAD>(PB, pn, W, 0, 1, lane);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -532,13 +550,13 @@ __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, c
 // the end).  GS = true ("global strip", subdomains whose strips do not fit on chip, e.g. cfg5): the
 // tile solves in place in its T columns of the SYRK group strip in global memory (row-major, G
 // wide, L2-resident while the tile runs); the strip rows of the plan are then group-strip rows.
-template <int T, bool GS>
+template <int T, bool GS, bool YM>
 __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPlan P) {
   using Cfg = TileCfg<T>;
   constexpr int WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC, CT = Cfg::CT;
   constexpr int KS = kMaxPanel / 4;  // k steps of 4 in a full panel
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const TrsmSmem L = trsm_smem_layout(T, P.ring_bytes, P.strip_cap, GS);
+  const TrsmSmem L = trsm_smem_layout(T, P.ring_bytes, P.strip_cap, GS, YM);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem_raw + L.empty);
   SlotRec* rec = reinterpret_cast<SlotRec*>(smem_raw + L.off);
@@ -608,6 +626,14 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
   // barrier per step among the warps of a column block orders the R_p updates before the next
   // panel reads its rows.
   const int cgrp = warp % NWC;  // column-block group: the warps that touch these T / NWC columns
+  auto group_sync = [&]() {
+    if constexpr (NWC == 1) {
+      consumer_sync<CT>();
+    } else {
+      asm volatile("bar.sync %0, %1;\n" ::"r"(2 + cgrp), "n"(CT / NWC) : "memory");  // ids 2..9
+    }
+  };
+  double* Ys = reinterpret_cast<double*>(smem_raw + L.ys);  // Y mode only: 64 x LDX, swizzled
   Group Gt;
   double* Xg = nullptr;         // this tile's columns of its group strip (shared-strip mode)
   if constexpr (!GS) {
@@ -677,8 +703,30 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
           yn[i][j][1] = ya[0][i][j][1] + ya[1][i][j][1];
         }
     }
-    // X[R_p] -= W_p X_p, one 64-row chunk (one ring block) at a time; chunks update disjoint rows
-    // and each warp releases its ring slot itself
+    if constexpr (YM) {
+      // Y mode: the update operand is L[R_p, p] itself, so the chunks need the solved Y = X_p(new):
+      // exchanged through Ys among the warps of the column-block group, then held as B fragments
+#pragma unroll
+      for (int i = 0; i < WM; i++) {
+        const int r = (br0 + i) * 8 + g;
+#pragma unroll
+        for (int j = 0; j < WN; j++)
+          if (r < kw4)
+            *reinterpret_cast<double2*>(Ys + Cfg::idx(r, (bc0 + j) * 8 + 2 * t4)) = make_double2(yn[i][j][0], yn[i][j][1]);
+      }
+      group_sync();
+#pragma unroll
+      for (int j = 0; j < WN; j++) {
+        const double* yb = Ys + Cfg::idx(t4, (bc0 + j) * 8 + g);  // rows 4 ks + t4 share the swizzle
+#pragma unroll
+        for (int ks = 0; ks < KS; ks++) {
+          if (ks % 4 == 0 && 4 * ks >= kw4) break;
+          yf[ks][j] = (4 * ks < kw4) ? yb[4 * ks * Cfg::LDX] : 0.0;
+        }
+      }
+    }
+    // X[R_p] -= W_p X_p (W mode) or L[R_p, p] Y (Y mode), one 64-row chunk (one ring block) at a
+    // time; chunks update disjoint rows and each warp releases its ring slot itself
     for (int c = 0; c < pn.nchunk; c++) {
       b++;
       const int rows_c = min(kChunk, pn.nR - c * kChunk);
@@ -757,11 +805,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
     }
     // the column-block group's R_p updates are visible before the next panel reads its rows, and
     // every warp of the group has read X_p: store the solved rows (final) into the group strip
-    if constexpr (NWC == 1) {
-      consumer_sync<CT>();
-    } else {
-      asm volatile("bar.sync %0, %1;\n" ::"r"(2 + cgrp), "n"(CT / NWC) : "memory");  // ids 2..9
-    }
+    group_sync();
 #pragma unroll
     for (int i = 0; i < WM; i++) {
       const int r = (br0 + i) * 8 + g;
@@ -970,13 +1014,17 @@ __global__ void __launch_bounds__(kThreads) apply_scatter_kernel(DevPlan P, doub
 namespace {
 
 using TrsmFn = void (*)(DevPlan);
-TrsmFn trsm_kernel_ptr(int T, bool gs) {
+template <bool YM>
+TrsmFn trsm_kernel_ptr_m(int T, bool gs) {
   switch (T) {
-    case 8: return gs ? trsm_smem_kernel<8, true> : trsm_smem_kernel<8, false>;
-    case 16: return gs ? trsm_smem_kernel<16, true> : trsm_smem_kernel<16, false>;
-    case 32: return gs ? trsm_smem_kernel<32, true> : trsm_smem_kernel<32, false>;
-    default: return gs ? trsm_smem_kernel<64, true> : trsm_smem_kernel<64, false>;
+    case 8: return gs ? trsm_smem_kernel<8, true, YM> : trsm_smem_kernel<8, false, YM>;
+    case 16: return gs ? trsm_smem_kernel<16, true, YM> : trsm_smem_kernel<16, false, YM>;
+    case 32: return gs ? trsm_smem_kernel<32, true, YM> : trsm_smem_kernel<32, false, YM>;
+    default: return gs ? trsm_smem_kernel<64, true, YM> : trsm_smem_kernel<64, false, YM>;
   }
+}
+TrsmFn trsm_kernel_ptr(int T, bool gs, bool wmode) {
+  return wmode ? trsm_kernel_ptr_m<false>(T, gs) : trsm_kernel_ptr_m<true>(T, gs);
 }
 
 template <typename V>
@@ -1090,12 +1138,13 @@ sc_status upload_plan(Plan& P, std::string& err) {
   D.strip_cap = P.max_strip_rows;
   D.G = P.G;
   D.ring_bytes = P.ring_bytes;
+  D.wmode = P.wmode ? 1 : 0;
   if (P.ring_bytes <= 0) {
     err = "X strip of " + std::to_string(P.max_strip_rows) + " rows x " + std::to_string(P.T) +
           " columns leaves no room for the L-block ring in shared memory; use smaller tile_cols";
     return SC_ERR_INVALID_ARG;
   }
-  P.smem_trsm = trsm_smem_layout(P.T, P.ring_bytes, P.max_strip_rows, P.gstrip).total;
+  P.smem_trsm = trsm_smem_layout(P.T, P.ring_bytes, P.max_strip_rows, P.gstrip, !P.wmode).total;
   int dev_smem = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.opt.device));
   if (P.smem_trsm > (size_t)dev_smem) {
@@ -1107,7 +1156,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   CUDA_TRY(cudaFuncSetAttribute(prep_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem));
   CUDA_TRY(cudaFuncSetAttribute(prep_small_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg<32>::kSmem));
   CUDA_TRY(cudaFuncSetAttribute(syrk_pair_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)syrk_smem_bytes<64>()));
-  CUDA_TRY(cudaFuncSetAttribute(trsm_kernel_ptr(P.T, P.gstrip), cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CUDA_TRY(cudaFuncSetAttribute(trsm_kernel_ptr(P.T, P.gstrip, P.wmode), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)P.smem_trsm));
   double total = 8.0 * (P.X_doubles + P.F_doubles + P.PB_doubles + P.part_doubles);
   total += dest.size() * 4.0 + Rrows.size() * 4.0 + panels.size() * sizeof(Panel) + tiles.size() * sizeof(Tile) +
@@ -1175,7 +1224,7 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
   }
   if (P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
   if (ntr > 0) {
-    trsm_kernel_ptr(P.T, P.gstrip)<<<ntr, TileCfg<8>::CT + 32, P.smem_trsm, stream>>>(P.dev);
+    trsm_kernel_ptr(P.T, P.gstrip, P.wmode)<<<ntr, TileCfg<8>::CT + 32, P.smem_trsm, stream>>>(P.dev);
     CUDA_TRY(cudaGetLastError());
   }
   if (P.tev[2]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[2], stream));

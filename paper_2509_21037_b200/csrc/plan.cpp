@@ -665,6 +665,12 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   // factor panel width: 64 for large operators (3D: wide separators, DMMA-bound); 32 for small ones
   // (2D: narrow supernodes, latency-bound; narrower L blocks leave shared memory for T = 32 strips)
   P.PW = opt.panel_cols ? opt.panel_cols : (max_m > 512 ? kMaxPanel : 32);
+  // TRSM update operand: Y mode (default: L[R_p,p] times the solved panel Y, exchanged through
+  // shared memory within each column-block group) or W mode (W_p = L[R_p,p] inv(L_pp) prepared once
+  // per subdomain in prep: no intra-step barrier, but the prep transform costs more than the
+  // barrier saves: cfg2-5 measured equal or slower in total, e.g. cfg4 3649 vs 3730 subdomains/s)
+  P.wmode = false;
+  if (const char* e = std::getenv("SC_TRSM_MODE")) P.wmode = e[0] == 'W';
   if (const char* e = std::getenv("SC_GROUP")) G0 = std::atoi(e);
   if (!(G0 == 16 || G0 == 32 || G0 == 64)) FAIL(SC_ERR_INVALID_ARG, "SC_GROUP must be 16, 32 or 64");
   // classes are independent: analysed on all host cores
@@ -706,7 +712,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   auto strip_limit_for = [&](int T) -> int32_t {
     const int64_t kw4 = (P.PW + 3) & ~3;
     const int64_t maxblk = std::max<int64_t>(block_ld(P.PW), kLdC) * kw4 * 8;
-    const int64_t fixed = (int64_t)trsm_smem_layout(T, (int)(2 * maxblk), 0, false).total;
+    const int64_t fixed = (int64_t)trsm_smem_layout(T, (int)(2 * maxblk), 0, false, !P.wmode).total;
     return (int32_t)std::max<int64_t>(-1, ((int64_t)kSmemBudget - fixed) / (8 * strip_ld(T)));
   };
   // TRSM tile width: the widest of 32 / 16 / 8 whose largest X strip fits in shared memory next to
@@ -723,7 +729,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
         if (p.nchunk > 0) maxblk = std::max<int64_t>(maxblk, (int64_t)(p.nchunk > 1 ? kLdC : p.ldLast) * p.kw4 * 8);
       }
     }
-    const int64_t fixed = (int64_t)trsm_smem_layout(T, 0, mx, P.gstrip).total;
+    const int64_t fixed = (int64_t)trsm_smem_layout(T, 0, mx, P.gstrip, !P.wmode).total;
     int64_t ring = std::min<int64_t>(kRingMaxBytes, (int64_t)kSmemBudget - fixed) & ~(int64_t)127;
     return ring >= 2 * maxblk ? ring : -1;
   };

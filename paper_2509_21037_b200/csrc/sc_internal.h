@@ -42,7 +42,7 @@ struct TrsmSmem {
 };
 // Row stride of the shared-memory strip: T (column-swizzled) for T >= 16, T + 4 for T = 8.
 SC_HD constexpr int strip_ld(int T) { return T >= 16 ? T : T + 4; }
-SC_HD inline TrsmSmem trsm_smem_layout(int T, int ring_bytes, int strip_cap, bool global_strip) {
+SC_HD inline TrsmSmem trsm_smem_layout(int T, int ring_bytes, int strip_cap, bool global_strip, bool ybuf) {
   TrsmSmem s{};
   s.full = 0;
   s.empty = 8 * kSlots;
@@ -51,8 +51,9 @@ SC_HD inline TrsmSmem trsm_smem_layout(int T, int ring_bytes, int strip_cap, boo
   s.ring = s.srow + sizeof(uint16_t) * kSlots * kChunk;
   // 512 B guard after the ring: a warp's 8-row fragment loads of a block whose ld is below 64 may
   // read up to 60 doubles past its end (rows that are never used)
-  s.ys = s.ring + (size_t)ring_bytes + 512;  // (no Y buffer: the solved panel stays in registers)
-  s.strip = s.ys;
+  s.ys = s.ring + (size_t)ring_bytes + 512;
+  // Y buffer (Y mode: 64 x strip_ld(T)); in W mode the solved panel stays in registers
+  s.strip = s.ys + (ybuf ? sizeof(double) * (size_t)kMaxPanel * (size_t)strip_ld(T) : 0);
   s.total = s.strip + (global_strip ? 0 : sizeof(double) * (size_t)(strip_cap + 4) * (size_t)strip_ld(T));
   return s;
 }
@@ -207,12 +208,14 @@ struct DevPlan {
   unsigned long long* err;         // sticky device error: ((sub+1) << 32) | col
   int32_t nsub, max_n, T, G, strip_cap;  // strip_cap: rows of the shared-memory strip
   int32_t ring_bytes;                    // TRSM L-block ring size
+  int32_t wmode;                         // 1: chunks hold W_p = L[R_p,p] inv(L_pp) (W mode), 0: L (Y mode)
 };
 
 struct Plan {
   sc_options opt{};
   int32_t T = 32, G = 64, PW = 64, ring_bytes = 0;
   bool gstrip = false;             // X strips solved in place in the group strips (global memory)
+  bool wmode = true;               // TRSM update operand W_p = L[R_p,p] inv(L_pp) (wide panels) or L (Y mode)
   int32_t nsub = 0;
   std::vector<ClassPlan> classes;
   std::vector<int32_t> sub_cls;
