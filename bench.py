@@ -346,6 +346,7 @@ def main():
         "config": {"workload": CFG_DESC[args.config], "name": args.config, "subdomains_per_gpu": nsub,
                    "skip": args.skip, "tile_cols": st["tile_cols"], "panel_cols": st["panel_cols"],
                    "x_strip": {1: "shared", 2: "global"}.get(st["x_strip"], "?"),
+                   "trsm_tasks_2cta": st["trsm_tasks_2cta"],
                    "parallelism": f"subdomain-sharded x{world} (no collective in assembly)",
                    "l2": f"inputs larger than L2: L values {st['bytes_L_values'] / 1e9:.2f} GB, "
                          f"X {st['bytes_X'] / 1e9:.2f} GB, F {8 * sum(m * m for m in plan.m) / 1e9:.2f} GB per GPU"},

@@ -113,6 +113,7 @@ typedef struct {
   int64_t panels;            /* factor panels, summed over subdomains                               */
   int32_t group_cols;        /* SYRK output tile width G                                            */
   int32_t x_strip;           /* SC_STRIP_SHARED or SC_STRIP_GLOBAL: the mode the plan chose         */
+  int64_t trsm_tasks_2cta;   /* TRSM tiles in the small-strip class (own launch, two CTAs per SM)   */
 } sc_stats;
 
 /* Fill `opt` with defaults: precision 64, skip EXACT, tile/panel auto, device 0. */

@@ -459,7 +459,8 @@ static_assert(sizeof(SlotRec) == 48, "slot record");
 // cp.async.bulk into the byte ring as soon as a slot and the bytes are free.  A chunk block travels
 // with its 64 precomputed strip rows (128 B, same mbarrier).
 __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, const double* PB, unsigned char* ring,
-                                           uint64_t* full, uint64_t* empty, SlotRec* rec, uint16_t* srow, int lane) {
+                                           uint64_t* full, uint64_t* empty, SlotRec* rec, uint16_t* srow, int lane,
+                                           int ring_bytes) {
   int q_slot[kSlots], q_start[kSlots];  // FIFO of in-flight blocks (identical in every lane)
   int q_head = 0, inflight = 0, ring_head = 0, ring_tail = 0;
   int b = 0;
@@ -498,7 +499,7 @@ __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, c
             ok = true;
           } else if (inflight < kSlots) {
             if (ring_tail > ring_head) {
-              if (P.ring_bytes - ring_tail >= bytes) {
+              if (ring_bytes - ring_tail >= bytes) {
                 start = ring_tail;
                 ok = true;
               } else if (ring_head >= bytes) {
@@ -550,13 +551,14 @@ __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, c
 // the end).  GS = true ("global strip", subdomains whose strips do not fit on chip, e.g. cfg5): the
 // tile solves in place in its T columns of the SYRK group strip in global memory (row-major, G
 // wide, L2-resident while the tile runs); the strip rows of the plan are then group-strip rows.
-template <int T, bool GS, bool YM>
-__global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPlan P) {
+// MINB: CTAs per SM the launch is built for (2: the small-strip tile class, registers capped)
+template <int T, bool GS, bool YM, int MINB = 1>
+__global__ void __launch_bounds__(TileCfg<T>::CT + 32, MINB) trsm_smem_kernel(DevPlan P, TrsmLaunch Lc) {
   using Cfg = TileCfg<T>;
   constexpr int WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC, CT = Cfg::CT;
   constexpr int KS = kMaxPanel / 4;  // k steps of 4 in a full panel
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const TrsmSmem L = trsm_smem_layout(T, P.ring_bytes, P.strip_cap, GS, YM);
+  const TrsmSmem L = trsm_smem_layout(T, Lc.ring_bytes, Lc.strip_cap, GS, YM);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + L.full);
   uint64_t* empty = reinterpret_cast<uint64_t*>(smem_raw + L.empty);
   SlotRec* rec = reinterpret_cast<SlotRec*>(smem_raw + L.off);
@@ -564,7 +566,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
   unsigned char* ring = smem_raw + L.ring;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const I2 task = P.trsm_tasks[blockIdx.x];
+  const I2 task = P.trsm_tasks[Lc.task0 + blockIdx.x];
   const int sub = task.x;
   const Tile tile = P.tiles[task.y];
   const double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
@@ -595,7 +597,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, 1) trsm_smem_kernel(DevPl
   }
   __syncthreads();
   if (warp == Cfg::NCW) {  // ---- TMA producer warp
-    trsm_producer(P, tile, PB, ring, full, empty, rec, srow, lane);
+    trsm_producer(P, tile, PB, ring, full, empty, rec, srow, lane, Lc.ring_bytes);
     return;
   }
 
@@ -1013,7 +1015,7 @@ __global__ void __launch_bounds__(kThreads) apply_scatter_kernel(DevPlan P, doub
 // ------------------------------------------------------------------------------------------------
 namespace {
 
-using TrsmFn = void (*)(DevPlan);
+using TrsmFn = void (*)(DevPlan, TrsmLaunch);
 template <bool YM>
 TrsmFn trsm_kernel_ptr_m(int T, bool gs) {
   switch (T) {
@@ -1025,6 +1027,13 @@ TrsmFn trsm_kernel_ptr_m(int T, bool gs) {
 }
 TrsmFn trsm_kernel_ptr(int T, bool gs, bool wmode) {
   return wmode ? trsm_kernel_ptr_m<false>(T, gs) : trsm_kernel_ptr_m<true>(T, gs);
+}
+// small-strip class (shared strips, T <= 16 only), two CTAs per SM
+TrsmFn trsm_kernel_ptr2(int T, bool wmode) {
+  switch (T) {
+    case 8: return wmode ? trsm_smem_kernel<8, false, false, 2> : trsm_smem_kernel<8, false, true, 2>;
+    default: return wmode ? trsm_smem_kernel<16, false, false, 2> : trsm_smem_kernel<16, false, true, 2>;
+  }
 }
 
 template <typename V>
@@ -1135,9 +1144,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   D.nsub = P.nsub;
   D.max_n = P.max_n;
   D.T = P.T;
-  D.strip_cap = P.max_strip_rows;
   D.G = P.G;
-  D.ring_bytes = P.ring_bytes;
   D.wmode = P.wmode ? 1 : 0;
   if (P.ring_bytes <= 0) {
     err = "X strip of " + std::to_string(P.max_strip_rows) + " rows x " + std::to_string(P.T) +
@@ -1145,6 +1152,12 @@ sc_status upload_plan(Plan& P, std::string& err) {
     return SC_ERR_INVALID_ARG;
   }
   P.smem_trsm = trsm_smem_layout(P.T, P.ring_bytes, P.max_strip_rows, P.gstrip, !P.wmode).total;
+  if (P.ntrsm_small > 0) {  // small-strip tile class: its own (smaller) launch footprint
+    P.smem_trsm_small = trsm_smem_layout(P.T, P.ring_small, P.strip_small, false, !P.wmode).total;
+    CUDA_TRY(cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&P.side_stream), cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(&P.ev_fork), cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(&P.ev_join), cudaEventDisableTiming));
+  }
   int dev_smem = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.opt.device));
   if (P.smem_trsm > (size_t)dev_smem) {
@@ -1158,6 +1171,9 @@ sc_status upload_plan(Plan& P, std::string& err) {
   CUDA_TRY(cudaFuncSetAttribute(syrk_pair_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)syrk_smem_bytes<64>()));
   CUDA_TRY(cudaFuncSetAttribute(trsm_kernel_ptr(P.T, P.gstrip, P.wmode), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)P.smem_trsm));
+  if (P.ntrsm_small > 0)
+    CUDA_TRY(cudaFuncSetAttribute(trsm_kernel_ptr2(P.T, P.wmode), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)P.smem_trsm_small));
   double total = 8.0 * (P.X_doubles + P.F_doubles + P.PB_doubles + P.part_doubles);
   total += dest.size() * 4.0 + Rrows.size() * 4.0 + panels.size() * sizeof(Panel) + tiles.size() * sizeof(Tile) +
            steps.size() * sizeof(Step) + wsegs.size() * sizeof(WSeg) + groups.size() * sizeof(Group) +
@@ -1178,6 +1194,10 @@ void free_plan_device(Plan& P) {
   P.h_Lptr_pinned = nullptr;
   if (P.lptr_event) cudaEventDestroy((cudaEvent_t)P.lptr_event);
   P.lptr_event = nullptr;
+  if (P.side_stream) cudaStreamDestroy(static_cast<cudaStream_t>(P.side_stream));
+  if (P.ev_fork) cudaEventDestroy(static_cast<cudaEvent_t>(P.ev_fork));
+  if (P.ev_join) cudaEventDestroy(static_cast<cudaEvent_t>(P.ev_join));
+  P.side_stream = P.ev_fork = P.ev_join = nullptr;
   if (P.d_Lstage) cudaFree(P.d_Lstage);
   P.d_Lstage = nullptr;
   P.on_device = false;
@@ -1224,7 +1244,25 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
   }
   if (P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
   if (ntr > 0) {
-    trsm_kernel_ptr(P.T, P.gstrip, P.wmode)<<<ntr, TileCfg<8>::CT + 32, P.smem_trsm, stream>>>(P.dev);
+    // tiles with small strips (2 CTAs per SM) and the rest (1 CTA per SM): two launches, the large
+    // ones on a side stream so both classes share the SMs and neither launch's tail idles them
+    const TrsmFn fn = trsm_kernel_ptr(P.T, P.gstrip, P.wmode), fn2 = trsm_kernel_ptr2(P.T, P.wmode);
+    const int ns = P.ntrsm_small, nl = ntr - ns;
+    if (ns > 0 && nl > 0) {
+      cudaStream_t side = static_cast<cudaStream_t>(P.side_stream);
+      CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_fork), stream));
+      CUDA_TRY(cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(P.ev_fork), 0));
+      fn<<<nl, TileCfg<8>::CT + 32, P.smem_trsm, side>>>(P.dev, TrsmLaunch{ns, P.ring_bytes, P.max_strip_rows, 0});
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_join), side));
+      fn2<<<ns, TileCfg<8>::CT + 32, P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{0, P.ring_small, P.strip_small, 0});
+      CUDA_TRY(cudaGetLastError());
+      CUDA_TRY(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(P.ev_join), 0));
+    } else if (ns > 0) {
+      fn2<<<ns, TileCfg<8>::CT + 32, P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{0, P.ring_small, P.strip_small, 0});
+    } else {
+      fn<<<ntr, TileCfg<8>::CT + 32, P.smem_trsm, stream>>>(P.dev, TrsmLaunch{0, P.ring_bytes, P.max_strip_rows, 0});
+    }
     CUDA_TRY(cudaGetLastError());
   }
   if (P.tev[2]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[2], stream));

@@ -733,6 +733,35 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     int64_t ring = std::min<int64_t>(kRingMaxBytes, (int64_t)kSmemBudget - fixed) & ~(int64_t)127;
     return ring >= 2 * maxblk ? ring : -1;
   };
+  // two-CTAs-per-SM budget for tile width T (after an analysis at T): strip rows that fit next to a
+  // ring of max(2 largest L blocks, 32 KB) in half an SM, and how many tiles qualify
+  struct TwoCta {
+    int32_t rmax = 0, fit_max = 0;
+    int64_t n_all = 0, n_fit = 0, half = 0;
+  };
+  auto two_cta = [&](int T) -> TwoCta {
+    TwoCta r;
+    int64_t maxblk = 16;
+    for (auto& C : P.classes)
+      for (auto& p : C.panels) {
+        maxblk = std::max<int64_t>(maxblk, (int64_t)p.ldD * p.kw4 * 8);
+        if (p.nchunk > 0) maxblk = std::max<int64_t>(maxblk, (int64_t)(p.nchunk > 1 ? kLdC : p.ldLast) * p.kw4 * 8);
+      }
+    const int64_t ring_min = (std::max<int64_t>(2 * maxblk, 32768) + 127) & ~(int64_t)127;
+    r.half = kSmemPerSM / 2 - 1024;  // per-CTA reservation
+    const int64_t fixed = (int64_t)trsm_smem_layout(T, (int)ring_min, 0, false, !P.wmode).total;
+    r.rmax = (int32_t)((r.half - fixed) / (8 * strip_ld(T)));
+    for (auto& C : P.classes)
+      for (auto& t : C.tiles)
+        if (t.width > 0) {
+          r.n_all++;
+          if (t.strip_rows <= r.rmax) {
+            r.n_fit++;
+            r.fit_max = std::max(r.fit_max, t.strip_rows);
+          }
+        }
+    return r;
+  };
   // global-strip tile width: 32 (measured on cfg4 / cfg5: 16 and 64 are slower)
   const int Tg = opt.tile_cols ? opt.tile_cols : 32;
   if (opt.x_strip == SC_STRIP_GLOBAL) {
@@ -746,6 +775,16 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     const int* cand = opt.tile_cols ? &opt.tile_cols : cand_auto;
     const int ncand = opt.tile_cols ? 1 : (opt.x_strip == SC_STRIP_SHARED ? 3 : 2);
     bool fits = false;
+    // small operators (2D): T = 16 at two CTAs per SM beats T = 32 at one when most tiles' strips
+    // fit in half an SM (cfg2 TRSM 1.72 vs 2.01 ms)
+    if (!opt.tile_cols && max_m <= 512) {
+      sc_status st = analyse_all(16, false, strip_limit_for(16));
+      if (st != SC_OK) return st;
+      if (!too_big() && ring_for(16) > 0) {
+        const TwoCta tc = two_cta(16);
+        fits = tc.rmax > 0 && tc.n_fit * 2 >= tc.n_all;
+      }
+    }
     for (int k = 0; k < ncand && !fits; k++) {
       // SC_STRIP_SHARED with an explicit tile width analyses fully and reports the misfit below
       const bool force = opt.x_strip == SC_STRIP_SHARED && opt.tile_cols;
@@ -763,6 +802,34 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   }
   for (auto& C : P.classes) P.max_strip_rows = std::max(P.max_strip_rows, C.max_strip_rows);
   P.ring_bytes = (int32_t)std::max<int64_t>(ring_for(P.T), 0);
+  // small-strip tile class (shared strips): tiles whose strip fits next to a ring of >= 2 of the
+  // largest L blocks (and >= 32 KB) within half of the SM's shared memory run two CTAs per SM
+  // (T <= 16 only: the register cap of two 288-thread CTAs per SM makes wider tiles spill)
+  int32_t split_rows = 0;
+  bool want_split = true;
+  if (const char* e = std::getenv("SC_TRSM_SPLIT")) want_split = std::atoi(e) != 0;
+  if (!P.gstrip && want_split && P.T <= 16) {
+    TwoCta tc = two_cta(P.T);
+    if (const char* e = std::getenv("SC_TRSM_SPLIT_ROWS")) {  // test hook: force the class boundary
+      const int32_t r = std::min(tc.rmax, (int32_t)std::atoi(e));
+      tc.n_fit = 0;
+      tc.fit_max = 0;
+      for (auto& C : P.classes)
+        for (auto& t : C.tiles)
+          if (t.width > 0 && t.strip_rows <= r) {
+            tc.n_fit++;
+            tc.fit_max = std::max(tc.fit_max, t.strip_rows);
+          }
+      tc.n_all = 2 * tc.n_fit;  // accept
+      if (tc.n_fit == 0) tc.rmax = 0;
+    }
+    if (tc.rmax > 0 && tc.n_fit * 2 >= tc.n_all) {  // (all tiles fitting: one launch at two CTAs per SM)
+      split_rows = tc.fit_max;
+      P.strip_small = tc.fit_max;
+      P.ring_small =
+          (int32_t)((tc.half - (int64_t)trsm_smem_layout(P.T, 0, tc.fit_max, false, !P.wmode).total) & ~(int64_t)127);
+    }
+  }
 
   // --- global concatenation: class-local indices -> global
   int64_t srow_base = 0;
@@ -823,6 +890,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   S.panel_cols = P.PW;
   std::vector<int64_t> qcount((size_t)std::max<int64_t>(opt.n_lambda_global, 0) + 1, 0);
   std::vector<I2> small_bkt[3];
+  std::vector<I2> trsm_small;
   for (int32_t i = 0; i < nsub; i++) {
     const int32_t cls = P.sub_cls[(size_t)i];
     const ClassPlan& C = P.classes[(size_t)cls];
@@ -846,7 +914,9 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
       else small_bkt[kw <= 8 ? 0 : (kw <= 16 ? 1 : 2)].push_back(tk);
     }
     for (size_t t = 0; t < C.tiles.size(); t++)
-      if (C.tiles[t].width > 0) P.trsm_tasks.push_back({i, P.cls_tile_begin[(size_t)cls] + (int32_t)t});
+      if (C.tiles[t].width > 0)
+        (split_rows > 0 && C.tiles[t].strip_rows <= split_rows ? trsm_small : P.trsm_tasks)
+            .push_back({i, P.cls_tile_begin[(size_t)cls] + (int32_t)t});
     for (size_t q = 0; q < C.pairs.size(); q++) P.syrk_tasks.push_back({i, P.cls_pair_begin[(size_t)cls] + (int32_t)q});
     for (int32_t rb = 0; rb < nab; rb++)
       for (int32_t cb = 0; cb <= rb; cb++) P.apply_tasks.push_back({i, rb, cb, 0});
@@ -881,6 +951,8 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     S.bytes_panels += 8.0 * (double)C.pb_doubles;
     S.panels += (int64_t)C.panels.size();
   }
+  P.ntrsm_small = (int32_t)trsm_small.size();
+  P.trsm_tasks.insert(P.trsm_tasks.begin(), trsm_small.begin(), trsm_small.end());
   for (int b = 0; b < 3; b++) {
     P.small_begin[b] = (int32_t)P.prep_small_tasks.size();
     P.prep_small_tasks.insert(P.prep_small_tasks.end(), small_bkt[b].begin(), small_bkt[b].end());
@@ -889,6 +961,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   S.group_cols = P.G;
   S.x_strip = P.gstrip ? SC_STRIP_GLOBAL : SC_STRIP_SHARED;
   S.trsm_tasks = (int64_t)P.trsm_tasks.size();
+  S.trsm_tasks_2cta = P.ntrsm_small;
   S.syrk_tasks = (int64_t)P.syrk_tasks.size();
   S.bytes_X = 8.0 * (double)P.X_doubles;
   // CSR over global multipliers of the (sub, stepped position) contributions, in (sub, a) order

@@ -29,6 +29,7 @@ SC_HD constexpr int block_ld(int rows) { return rows <= 4 ? 4 : 4 + 8 * ((rows -
 
 constexpr int kLdC = 68;                        // block_ld(kChunk): ld of a full 64-row chunk
 constexpr size_t kSmemBudget = 232448;          // B200 max dynamic shared memory per block (227 KB)
+constexpr int64_t kSmemPerSM = 233472;          // B200 shared memory per SM (228 KB)
 constexpr int kSlots = 16;                      // TRSM L-block pipeline depth (mbarrier pairs)
 constexpr int kRingMaxBytes = 163840;           // TRSM L-block ring: at most 160 KB ...
 constexpr int kBlockMaxBytes = kLdC * kMaxPanel * 8;  // ... and at least 2 of the largest blocks
@@ -169,6 +170,12 @@ struct ClassPlan {
   double fl_trsm_exec = 0, fl_syrk_exec = 0, fl_prep_exec = 0;
 };
 
+// Per-launch parameters of the TRSM kernel: first task, L-block ring bytes and shared strip capacity
+// (rows) of this launch (tiles are split into a small-strip class at two CTAs per SM and the rest).
+struct TrsmLaunch {
+  int32_t task0, ring_bytes, strip_cap, pad;
+};
+
 // Device-side view passed by value to every kernel.
 struct DevPlan {
   const Panel* panels;             // all classes, concatenated
@@ -206,8 +213,7 @@ struct DevPlan {
   double* PB;                      // panel buffers
   double* part;
   unsigned long long* err;         // sticky device error: ((sub+1) << 32) | col
-  int32_t nsub, max_n, T, G, strip_cap;  // strip_cap: rows of the shared-memory strip
-  int32_t ring_bytes;                    // TRSM L-block ring size
+  int32_t nsub, max_n, T, G;
   int32_t wmode;                         // 1: chunks hold W_p = L[R_p,p] inv(L_pp) (W mode), 0: L (Y mode)
 };
 
@@ -245,6 +251,12 @@ struct Plan {
   void* tev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional timing events (sc_set_timing_events)
   int64_t n_lambda = 0;
   size_t smem_trsm = 0;
+  // small-strip TRSM tile class: trsm_tasks[0, ntrsm_small) at two CTAs per SM
+  int32_t ntrsm_small = 0, ring_small = 0, strip_small = 0;
+  size_t smem_trsm_small = 0;
+  void* side_stream = nullptr;   // cudaStream_t for the large-strip launch
+  void* ev_fork = nullptr;       // cudaEvent_t
+  void* ev_join = nullptr;
 };
 
 // plan.cpp

@@ -51,7 +51,8 @@ class Stats(ctypes.Structure):
                                                "flops_trsm_sparse_orig", "flops_trsm_executed",
                                                "flops_syrk_executed", "bytes_L_values", "bytes_F_lower", "bytes_X",
                                                "device_bytes", "bytes_apply", "bytes_panels")] + \
-               [("panels", ctypes.c_int64), ("group_cols", ctypes.c_int32), ("x_strip", ctypes.c_int32)]
+               [("panels", ctypes.c_int64), ("group_cols", ctypes.c_int32), ("x_strip", ctypes.c_int32),
+                ("trsm_tasks_2cta", ctypes.c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

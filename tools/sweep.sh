@@ -9,7 +9,7 @@ for spec in $SWEEP; do
 import json,sys
 try:
     d=json.load(open('gpurun_out/sw.json'))
-    print('$spec', round(d['value']), {k: round(v,3) for k,v in d['phase_ms'].items()}, d['config'].get('tile_cols'), d['config'].get('x_strip'), round(d['roofline']['frac'],3))
+    print('$spec', round(d['value']), {k: round(v,3) for k,v in d['phase_ms'].items()}, d['config'].get('tile_cols'), d['config'].get('x_strip'), d['config'].get('trsm_tasks_2cta'), round(d['roofline']['frac'],3))
 except Exception as e:
     print('$spec FAILED', open('gpurun_out/sw.err').read()[-600:])
 " >> gpurun_out/sweep.txt
