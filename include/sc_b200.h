@@ -132,8 +132,11 @@ sc_status sc_plan_create(const sc_subdomain_desc* sd, int32_t nsub, const sc_opt
 sc_status sc_assemble_batch(sc_plan_t p, const double* const* L_values, void* stream);
 
 /* Same as sc_assemble_batch but the L values live in HOST memory (ideally pinned): the call copies
-   them to a plan-owned device staging buffer on `stream` (host->device inside the call, the
-   paper's "copies factor L_i to the GPU") and then assembles.  Does not synchronise. */
+   them to a plan-owned device staging buffer (host->device inside the call, the paper's "copies
+   factor L_i to the GPU") and assembles.  Pipelined: the batch is cut into up
+   to 16 chunks of subdomains; chunk k's copies run on a plan-owned copy stream while the kernels of
+   chunk k-1 run on `stream`.  The host arrays must stay valid until `stream` completes.  Does not
+   synchronise. */
 sc_status sc_assemble_batch_host(sc_plan_t p, const double* const* L_values_host, void* stream);
 
 /* Solution stage: q[g] = sum_i sum_{a: lambda_map_i(a) = g} (F_i lambda_i)(a), lambda_i(a) =

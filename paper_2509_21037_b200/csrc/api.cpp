@@ -75,9 +75,7 @@ sc_status sc_assemble_batch_host(sc_plan_t p, const double* const* L_values_host
   if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
   if (!L_values_host && p->P.nsub > 0) return fail(SC_ERR_INVALID_ARG, "NULL L_values_host");
   std::string err;
-  std::vector<const double*> dptrs;
-  sc_status st = sc::stage_host_L(p->P, L_values_host, stream, dptrs, err);
-  if (st == SC_OK) st = sc::launch_assemble(p->P, dptrs.data(), stream, err);
+  sc_status st = sc::assemble_host_pipelined(p->P, L_values_host, stream, err);
   return st == SC_OK ? SC_OK : fail(st, err);
 }
 

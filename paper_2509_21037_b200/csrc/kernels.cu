@@ -217,12 +217,12 @@ __device__ __forceinline__ void chunks_times_inverse(double* __restrict__ PB, co
   }
 }
 
-__global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P) {
+__global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0) {
   extern __shared__ __align__(16) unsigned char prep_smem[];
   double* D = reinterpret_cast<double*>(prep_smem);  // triangle, then temporaries
   double* W = D + kMaxPanel * kLdT;                  // inverse
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const I2 task = P.prep_tasks[blockIdx.x];
+  const I2 task = P.prep_tasks[t0 + blockIdx.x];
   const int sub = task.x;
   const Panel pn = P.panels[task.y];
   const int cls = P.sub_cls[sub];
@@ -857,7 +857,7 @@ constexpr size_t syrk_smem_bytes() {
 }
 
 template <int G>
-__global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P) {
+__global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) {
   constexpr int kLdG = G + 4, kGroup = G;
   extern __shared__ __align__(16) unsigned char syrk_smem[];
   double* Sbuf = reinterpret_cast<double*>(syrk_smem);
@@ -865,7 +865,7 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool active = warp < SyrkCfg<G>::ACTIVE;
   const int g = lane >> 2, t4 = lane & 3;
-  const I2 task = P.syrk_tasks[blockIdx.x];
+  const I2 task = P.syrk_tasks[t0 + blockIdx.x];
   const int sub = task.x;
   const Pair pr = P.pairs[task.y];
   const Group gI = P.groups[pr.I], gJ = P.groups[pr.J];
@@ -1198,37 +1198,56 @@ void free_plan_device(Plan& P) {
   if (P.ev_fork) cudaEventDestroy(static_cast<cudaEvent_t>(P.ev_fork));
   if (P.ev_join) cudaEventDestroy(static_cast<cudaEvent_t>(P.ev_join));
   P.side_stream = P.ev_fork = P.ev_join = nullptr;
+  if (P.copy_stream) cudaStreamDestroy(static_cast<cudaStream_t>(P.copy_stream));
+  if (P.ev_start) cudaEventDestroy(static_cast<cudaEvent_t>(P.ev_start));
+  for (void* e : P.ev_chunk) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  P.ev_chunk.clear();
+  P.copy_stream = P.ev_start = nullptr;
   if (P.d_Lstage) cudaFree(P.d_Lstage);
   P.d_Lstage = nullptr;
   P.on_device = false;
 }
 
-sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_v, std::string& err) {
-  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
-  CUDA_TRY(cudaSetDevice(P.opt.device));
+// first task of subdomain >= sub in a subdomain-major task list
+static int task_lb(const std::vector<I2>& v, int lo, int hi, int32_t sub) {
+  return (int)(std::lower_bound(v.begin() + lo, v.begin() + hi, sub, [](const I2& t, int32_t s) { return t.x < s; }) -
+               v.begin());
+}
+
+static sc_status set_Lptr(Plan& P, const double* const* Lptr_host, cudaStream_t stream, std::string& err) {
   bool same = (int32_t)P.last_Lptr.size() == P.nsub;
   for (int32_t i = 0; same && i < P.nsub; i++) same = (P.last_Lptr[(size_t)i] == Lptr_host[i]);
-  if (!same) {
-    for (int32_t i = 0; i < P.nsub; i++)
-      if (!Lptr_host[i] && P.sub_nnz[(size_t)i] > 0) {
-        err = "L_values[" + std::to_string(i) + "] is NULL";
-        return SC_ERR_INVALID_ARG;
-      }
-    CUDA_TRY(cudaEventSynchronize((cudaEvent_t)P.lptr_event));  // previous upload consumed the buffer
-    for (int32_t i = 0; i < P.nsub; i++) P.h_Lptr_pinned[i] = Lptr_host[i];
-    CUDA_TRY(cudaMemcpyAsync(P.d_Lptr, P.h_Lptr_pinned, sizeof(double*) * (size_t)P.nsub, cudaMemcpyHostToDevice, stream));
-    CUDA_TRY(cudaEventRecord((cudaEvent_t)P.lptr_event, stream));
-    P.last_Lptr.assign(Lptr_host, Lptr_host + P.nsub);
-  }
-  P.last_stream = stream_v;
-  const int npr = (int)P.prep_tasks.size(), ntr = (int)P.trsm_tasks.size(), nsy = (int)P.syrk_tasks.size();
-  if (P.tev[0]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[0], stream));
-  if (npr > 0) {
-    prep_panel_kernel<<<npr, kThreads, kPrepSmem, stream>>>(P.dev);
-    CUDA_TRY(cudaGetLastError());
+  if (same) return SC_OK;
+  for (int32_t i = 0; i < P.nsub; i++)
+    if (!Lptr_host[i] && P.sub_nnz[(size_t)i] > 0) {
+      err = "L_values[" + std::to_string(i) + "] is NULL";
+      return SC_ERR_INVALID_ARG;
+    }
+  CUDA_TRY(cudaEventSynchronize((cudaEvent_t)P.lptr_event));  // previous upload consumed the buffer
+  for (int32_t i = 0; i < P.nsub; i++) P.h_Lptr_pinned[i] = Lptr_host[i];
+  CUDA_TRY(cudaMemcpyAsync(P.d_Lptr, P.h_Lptr_pinned, sizeof(double*) * (size_t)P.nsub, cudaMemcpyHostToDevice, stream));
+  CUDA_TRY(cudaEventRecord((cudaEvent_t)P.lptr_event, stream));
+  P.last_Lptr.assign(Lptr_host, Lptr_host + P.nsub);
+  return SC_OK;
+}
+
+// All phases (prep, TRSM, SYRK) for the subdomains [s0, s1) on `stream`; timing events only for the
+// whole batch.
+static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, bool timing, std::string& err) {
+  const bool all = s0 == 0 && s1 == P.nsub;
+  if (timing && P.tev[0]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[0], stream));
+  {
+    const int npr = (int)P.prep_tasks.size();
+    const int a = all ? 0 : task_lb(P.prep_tasks, 0, npr, s0), b = all ? npr : task_lb(P.prep_tasks, 0, npr, s1);
+    if (b > a) {
+      prep_panel_kernel<<<b - a, kThreads, kPrepSmem, stream>>>(P.dev, a);
+      CUDA_TRY(cudaGetLastError());
+    }
   }
   for (int bkt = 0; bkt < 3; bkt++) {  // small panels bucketed by padded width 8 / 16 / 32
-    const int t0 = P.small_begin[bkt], t1 = P.small_begin[bkt + 1], nt = t1 - t0;
+    const int lo = P.small_begin[bkt], hi = P.small_begin[bkt + 1];
+    const int t0 = all ? lo : task_lb(P.prep_small_tasks, lo, hi, s0);
+    const int t1 = all ? hi : task_lb(P.prep_small_tasks, lo, hi, s1), nt = t1 - t0;
     if (nt <= 0) continue;
     if (bkt == 0) {
       using C8 = SmallCfg<8>;
@@ -1242,46 +1261,70 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
     }
     CUDA_TRY(cudaGetLastError());
   }
-  if (P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
-  if (ntr > 0) {
+  if (timing && P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
+  {
     // tiles with small strips (2 CTAs per SM) and the rest (1 CTA per SM): two launches, the large
     // ones on a side stream so both classes share the SMs and neither launch's tail idles them
+    const int ntr = (int)P.trsm_tasks.size(), nsm = P.ntrsm_small;
     const TrsmFn fn = trsm_kernel_ptr(P.T, P.gstrip, P.wmode), fn2 = trsm_kernel_ptr2(P.T, P.wmode);
-    const int ns = P.ntrsm_small, nl = ntr - ns;
+    const int sa = all ? 0 : task_lb(P.trsm_tasks, 0, nsm, s0), sb = all ? nsm : task_lb(P.trsm_tasks, 0, nsm, s1);
+    const int la = all ? nsm : task_lb(P.trsm_tasks, nsm, ntr, s0), lb = all ? ntr : task_lb(P.trsm_tasks, nsm, ntr, s1);
+    const int ns = sb - sa, nl = lb - la;
     if (ns > 0 && nl > 0) {
       cudaStream_t side = static_cast<cudaStream_t>(P.side_stream);
       CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_fork), stream));
       CUDA_TRY(cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(P.ev_fork), 0));
-      fn<<<nl, TileCfg<8>::CT + 32, P.smem_trsm, side>>>(P.dev, TrsmLaunch{ns, P.ring_bytes, P.max_strip_rows, 0});
+      fn<<<nl, TileCfg<8>::CT + 32, P.smem_trsm, side>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_join), side));
-      fn2<<<ns, TileCfg<8>::CT + 32, P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{0, P.ring_small, P.strip_small, 0});
+      fn2<<<ns, TileCfg<8>::CT + 32, P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(P.ev_join), 0));
     } else if (ns > 0) {
-      fn2<<<ns, TileCfg<8>::CT + 32, P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{0, P.ring_small, P.strip_small, 0});
-    } else {
-      fn<<<ntr, TileCfg<8>::CT + 32, P.smem_trsm, stream>>>(P.dev, TrsmLaunch{0, P.ring_bytes, P.max_strip_rows, 0});
+      fn2<<<ns, TileCfg<8>::CT + 32, P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
+    } else if (nl > 0) {
+      fn<<<nl, TileCfg<8>::CT + 32, P.smem_trsm, stream>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
     }
     CUDA_TRY(cudaGetLastError());
   }
-  if (P.tev[2]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[2], stream));
-  if (nsy > 0) {
-    switch (P.G) {
-      case 16: syrk_pair_kernel<16><<<nsy, kThreads, syrk_smem_bytes<16>(), stream>>>(P.dev); break;
-      case 32: syrk_pair_kernel<32><<<nsy, kThreads, syrk_smem_bytes<32>(), stream>>>(P.dev); break;
-      default: syrk_pair_kernel<64><<<nsy, kThreads, syrk_smem_bytes<64>(), stream>>>(P.dev); break;
+  if (timing && P.tev[2]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[2], stream));
+  {
+    const int nsy = (int)P.syrk_tasks.size();
+    const int a = all ? 0 : task_lb(P.syrk_tasks, 0, nsy, s0), b = all ? nsy : task_lb(P.syrk_tasks, 0, nsy, s1);
+    if (b > a) {
+      switch (P.G) {
+        case 16: syrk_pair_kernel<16><<<b - a, kThreads, syrk_smem_bytes<16>(), stream>>>(P.dev, a); break;
+        case 32: syrk_pair_kernel<32><<<b - a, kThreads, syrk_smem_bytes<32>(), stream>>>(P.dev, a); break;
+        default: syrk_pair_kernel<64><<<b - a, kThreads, syrk_smem_bytes<64>(), stream>>>(P.dev, a); break;
+      }
+      CUDA_TRY(cudaGetLastError());
     }
-    CUDA_TRY(cudaGetLastError());
   }
-  if (P.tev[3]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[3], stream));
+  if (timing && P.tev[3]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[3], stream));
   return SC_OK;
 }
 
-sc_status stage_host_L(Plan& P, const double* const* Lhost, void* stream_v, std::vector<const double*>& dptrs,
-                       std::string& err) {
+sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_v, std::string& err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   CUDA_TRY(cudaSetDevice(P.opt.device));
+  sc_status st = set_Lptr(P, Lptr_host, stream, err);
+  if (st != SC_OK) return st;
+  P.last_stream = stream_v;
+  return launch_range(P, 0, P.nsub, stream, true, err);
+}
+
+// Host-resident L (row f1 "host-fed pipeline"): the batch is cut into chunks of
+// subdomains; chunk k's pinned-host -> device copies run on a plan-owned copy stream while the
+// kernels of chunk k-1 run on `stream` (one event per chunk), so the H2D transfer (PCIe-bound) hides
+// the assembly.
+sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* stream_v, std::string& err) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  CUDA_TRY(cudaSetDevice(P.opt.device));
+  for (int32_t i = 0; i < P.nsub; i++)
+    if (P.sub_nnz[(size_t)i] > 0 && !Lhost[i]) {
+      err = "L_values_host[" + std::to_string(i) + "] is NULL";
+      return SC_ERR_INVALID_ARG;
+    }
   if (!P.d_Lstage) {
     P.Lstage_off.assign((size_t)P.nsub + 1, 0);
     for (int32_t i = 0; i < P.nsub; i++) P.Lstage_off[(size_t)i + 1] = P.Lstage_off[(size_t)i] + P.sub_nnz[(size_t)i];
@@ -1289,17 +1332,36 @@ sc_status stage_host_L(Plan& P, const double* const* Lhost, void* stream_v, std:
     CUDA_TRY(cudaMalloc(&d, std::max<size_t>(8 * (size_t)P.Lstage_off.back(), 16)));
     P.d_Lstage = static_cast<double*>(d);
   }
-  dptrs.resize((size_t)P.nsub);
-  for (int32_t i = 0; i < P.nsub; i++) {
-    double* dst = P.d_Lstage + P.Lstage_off[(size_t)i];
-    if (P.sub_nnz[(size_t)i] > 0) {
-      if (!Lhost[i]) {
-        err = "L_values_host[" + std::to_string(i) + "] is NULL";
-        return SC_ERR_INVALID_ARG;
-      }
-      CUDA_TRY(cudaMemcpyAsync(dst, Lhost[i], 8 * (size_t)P.sub_nnz[(size_t)i], cudaMemcpyHostToDevice, stream));
-    }
-    dptrs[(size_t)i] = dst;
+  if (!P.copy_stream) {
+    CUDA_TRY(cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&P.copy_stream), cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(&P.ev_start), cudaEventDisableTiming));
+  }
+  const int32_t nchunk = std::max<int32_t>(1, std::min<int32_t>(16, P.nsub / 64));
+  while ((int32_t)P.ev_chunk.size() < nchunk) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    P.ev_chunk.push_back(e);
+  }
+  std::vector<const double*> dptrs((size_t)P.nsub);
+  for (int32_t i = 0; i < P.nsub; i++) dptrs[(size_t)i] = P.d_Lstage + P.Lstage_off[(size_t)i];
+  sc_status st = set_Lptr(P, dptrs.data(), stream, err);
+  if (st != SC_OK) return st;
+  P.last_stream = stream_v;
+  cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream);
+  // the staging buffer is reused: copies wait for everything enqueued on `stream` before this call
+  CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_start), stream));
+  CUDA_TRY(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(P.ev_start), 0));
+  for (int32_t k = 0; k < nchunk; k++) {
+    const int32_t s0 = (int32_t)((int64_t)P.nsub * k / nchunk), s1 = (int32_t)((int64_t)P.nsub * (k + 1) / nchunk);
+    for (int32_t i = s0; i < s1; i++)
+      if (P.sub_nnz[(size_t)i] > 0)
+        CUDA_TRY(cudaMemcpyAsync(P.d_Lstage + P.Lstage_off[(size_t)i], Lhost[i], 8 * (size_t)P.sub_nnz[(size_t)i],
+                                 cudaMemcpyHostToDevice, cs));
+    cudaEvent_t e = static_cast<cudaEvent_t>(P.ev_chunk[(size_t)k]);
+    CUDA_TRY(cudaEventRecord(e, cs));
+    CUDA_TRY(cudaStreamWaitEvent(stream, e, 0));
+    st = launch_range(P, s0, s1, stream, false, err);
+    if (st != SC_OK) return st;
   }
   return SC_OK;
 }

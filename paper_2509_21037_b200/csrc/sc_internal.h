@@ -257,6 +257,9 @@ struct Plan {
   void* side_stream = nullptr;   // cudaStream_t for the large-strip launch
   void* ev_fork = nullptr;       // cudaEvent_t
   void* ev_join = nullptr;
+  void* copy_stream = nullptr;   // host-fed pipeline (sc_assemble_batch_host): H2D copies
+  void* ev_start = nullptr;
+  std::vector<void*> ev_chunk;
 };
 
 // plan.cpp
@@ -270,7 +273,6 @@ sc_status launch_apply(Plan& P, const double* lambda, double* q, void* stream, s
 sc_status device_check(Plan& P, std::string& err);
 sc_status copy_F_lower(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
 sc_status copy_X_strips(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
-sc_status stage_host_L(Plan& P, const double* const* Lhost, void* stream, std::vector<const double*>& dptrs,
-                       std::string& err);
+sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* stream, std::string& err);
 
 }  // namespace sc
