@@ -1353,10 +1353,22 @@ sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* str
   CUDA_TRY(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(P.ev_start), 0));
   for (int32_t k = 0; k < nchunk; k++) {
     const int32_t s0 = (int32_t)((int64_t)P.nsub * k / nchunk), s1 = (int32_t)((int64_t)P.nsub * (k + 1) / nchunk);
+    // one batched call per chunk (per-copy launch overhead would otherwise cap the PCIe rate)
+    std::vector<void*> dsts, srcs;
+    std::vector<size_t> sizes;
     for (int32_t i = s0; i < s1; i++)
-      if (P.sub_nnz[(size_t)i] > 0)
-        CUDA_TRY(cudaMemcpyAsync(P.d_Lstage + P.Lstage_off[(size_t)i], Lhost[i], 8 * (size_t)P.sub_nnz[(size_t)i],
-                                 cudaMemcpyHostToDevice, cs));
+      if (P.sub_nnz[(size_t)i] > 0) {
+        dsts.push_back(P.d_Lstage + P.Lstage_off[(size_t)i]);
+        srcs.push_back(const_cast<double*>(Lhost[i]));
+        sizes.push_back(8 * (size_t)P.sub_nnz[(size_t)i]);
+      }
+    if (!dsts.empty()) {
+      cudaMemcpyAttributes attr{};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+      size_t attr_idx = 0, fail_idx = 0;
+      CUDA_TRY(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &attr_idx, 1, &fail_idx, cs));
+    }
     cudaEvent_t e = static_cast<cudaEvent_t>(P.ev_chunk[(size_t)k]);
     CUDA_TRY(cudaEventRecord(e, cs));
     CUDA_TRY(cudaStreamWaitEvent(stream, e, 0));
