@@ -2,7 +2,7 @@
 `--set full` captures, the launch lists, and profiles/traffic_<cfg>.json (DRAM bytes per launch of
 each phase's kernel, read by bench.py for roofline.traffic).
 
-    python tools/make_profiles.py r01 gpurun_out
+    python tools/make_profiles.py r01 gpurun_out [dst_dir]
 """
 import csv
 import glob
@@ -19,7 +19,7 @@ from ncu_summary import stalls, summary  # noqa: E402
 tag = sys.argv[1]
 src = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-dst = os.path.join(root, "profiles")
+dst = sys.argv[3] if len(sys.argv) > 3 else os.path.join(root, "profiles")
 os.makedirs(dst, exist_ok=True)
 
 PHASE = {"prep_panel_kernel": "prep", "prep_small_kernel": "prep", "trsm_smem_kernel": "trsm", "syrk_pair_kernel": "syrk"}
