@@ -50,6 +50,8 @@ def load_peaks():
     if "hbm_gbs" not in peaks:
         peaks["hbm_gbs"] = 6650.0
         peaks["hbm_source"] = "fallback (B200_PROFILING.md)"
+    else:
+        peaks.setdefault("hbm_source", "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)")
     return peaks
 
 
@@ -275,8 +277,13 @@ def main():
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel: prep is HBM-bound (algorithmic bytes: L values read once),
-    # TRSM and SYRK are FP64-tensor-bound (algorithmic flops: useful etree-exact flops)
+    # roofline of the dominant kernel.  Algorithmic work per phase, per launch:
+    #   prep: bytes = L values read once;
+    #   trsm: flops = useful (etree-exact) TRSM flops, bytes = L values read once + X strips written once;
+    #   syrk: flops = useful SYRK flops, bytes = X strips read once + F lower written once.
+    # The binding roof is the one the algorithmic intensity (flops/byte) selects against the ridge
+    # point peak_fp64 / peak_hbm: below it the kernel is reported against HBM (GB/s), above it
+    # against the FP64 tensor (DMMA) peak.
     phases = {"prep": ms_prep, "trsm": ms_trsm, "syrk": ms_syrk}
     dom = max(phases, key=phases.get)
     dom_ms = phases[dom]
@@ -286,18 +293,26 @@ def main():
         prof_traffic = json.load(open(tp)).get(dom)
     kernel_names = {"prep": "prep_panel_kernel + prep_small_kernel", "trsm": f"trsm_smem_kernel<{st['tile_cols']}>",
                     "syrk": f"syrk_pair_kernel<{st['group_cols']}>"}
-    if dom == "prep":
-        achieved = st["bytes_L_values"] / (dom_ms / 1e3) / 1e9
+    alg = {"prep": (0.0, st["bytes_L_values"]),
+           "trsm": (st["flops_trsm_useful"], st["bytes_L_values"] + st["bytes_X"]),
+           "syrk": (st["flops_syrk_useful"], st["bytes_X"] + st["bytes_F_lower"])}
+    flops, nbytes = alg[dom]
+    ridge = peaks["fp64_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    intensity = flops / nbytes if nbytes else float("inf")
+    if intensity < ridge:
+        achieved = nbytes / (dom_ms / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                    "algorithmic": "L values read once (8 B / nnz(L)) per launch"}
+                    "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks.get("hbm_source", "MEASURED_PEAKS.json hbm_gbs")}
     else:
-        dom_flops = st["flops_trsm_useful"] if dom == "trsm" else st["flops_syrk_useful"]
-        achieved = dom_flops / (dom_ms / 1e3) / 1e12
+        achieved = flops / (dom_ms / 1e3) / 1e12
         roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
                     "frac": achieved / peaks["fp64_tflops"], "dtype": "f64 (DMMA m8n8k4)",
-                    "peak_source": peaks["fp64_tflops_source"],
-                    "algorithmic": "useful (etree-exact) FP64 flops of the phase per launch"}
+                    "peak_source": peaks["fp64_tflops_source"]}
+    roofline.update({"algorithmic": {"prep": "L values read once (8 B/nnz(L))",
+                                     "trsm": "useful TRSM flops; L values read once + X strips written once",
+                                     "syrk": "useful SYRK flops; X strips read once + F lower written once"}[dom],
+                     "algorithmic_flops": flops, "algorithmic_bytes": nbytes, "intensity_flop_per_byte": intensity,
+                     "ridge_flop_per_byte": ridge})
     roofline.update({"traffic": prof_traffic, "kernel": kernel_names[dom], "share_of_step": dom_ms / ms_step})
     # amortization point: explicit GPU (assembly + apply per
     # iteration) vs implicit CPU apply per iteration on the host cores; the factorization is common
