@@ -217,6 +217,7 @@ __device__ __forceinline__ void chunks_times_inverse(double* __restrict__ PB, co
   }
 }
 
+template <bool WMODE>
 __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0) {
   extern __shared__ __align__(16) unsigned char prep_smem[];
   double* D = reinterpret_cast<double*>(prep_smem);  // triangle, then temporaries
@@ -304,7 +305,7 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0)
     Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * kLdT + i] : 0.0;
   }
   // chunks: L[R_p, p] -> W_p = L[R_p, p] inv(L_pp) (the TRSM's update operand)
-  if (P.wmode) chunks_times_inverse<kLdT, kMaxPanel>(PB, pn, W, warp, kThreads / 32, lane);
+  if constexpr (WMODE) chunks_times_inverse<kLdT, kMaxPanel>(PB, pn, W, warp, kThreads / 32, lane);
 }
 
 
@@ -319,7 +320,7 @@ struct SmallCfg {
   static constexpr size_t kSmem = sizeof(double) * kWarpDoubles * WARPS;
 };
 
-template <int NPAD>
+template <int NPAD, bool WMODE>
 __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(DevPlan P, int t_begin, int t_end) {
   using Cfg = SmallCfg<NPAD>;
   constexpr int LD = Cfg::LD;
@@ -396,7 +397,7 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
     const int j = q / ldD, i = q - j * ldD;
     Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * LD + i] : 0.0;
   }
-  if (P.wmode) chunks_times_inverse<LD, NPAD>(PB, pn, W, 0, 1, lane);
+  if constexpr (WMODE) chunks_times_inverse<LD, NPAD>(PB, pn, W, 0, 1, lane);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1166,14 +1167,26 @@ sc_status upload_plan(Plan& P, std::string& err) {
           " bytes); use smaller tile_cols";
     return SC_ERR_INVALID_ARG;
   }
-  CUDA_TRY(cudaFuncSetAttribute(prep_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kPrepSmem));
-  CUDA_TRY(cudaFuncSetAttribute(prep_small_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SmallCfg<32>::kSmem));
-  CUDA_TRY(cudaFuncSetAttribute(syrk_pair_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)syrk_smem_bytes<64>()));
-  CUDA_TRY(cudaFuncSetAttribute(trsm_kernel_ptr(P.T, P.gstrip, P.wmode), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)P.smem_trsm));
-  if (P.ntrsm_small > 0)
-    CUDA_TRY(cudaFuncSetAttribute(trsm_kernel_ptr2(P.T, P.wmode), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)P.smem_trsm_small));
+  // every kernel: the largest shared-memory carveout (the default left prep_small<16> at 3 CTAs/SM)
+  auto smem_attr = [&](const void* fn, size_t bytes) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e == cudaSuccess)
+      e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+    return e;
+  };
+  CUDA_TRY(smem_attr((const void*)prep_panel_kernel<true>, kPrepSmem));
+  CUDA_TRY(smem_attr((const void*)prep_panel_kernel<false>, kPrepSmem));
+  CUDA_TRY(smem_attr((const void*)prep_small_kernel<8, true>, SmallCfg<8>::kSmem));
+  CUDA_TRY(smem_attr((const void*)prep_small_kernel<8, false>, SmallCfg<8>::kSmem));
+  CUDA_TRY(smem_attr((const void*)prep_small_kernel<16, true>, SmallCfg<16>::kSmem));
+  CUDA_TRY(smem_attr((const void*)prep_small_kernel<16, false>, SmallCfg<16>::kSmem));
+  CUDA_TRY(smem_attr((const void*)prep_small_kernel<32, true>, SmallCfg<32>::kSmem));
+  CUDA_TRY(smem_attr((const void*)prep_small_kernel<32, false>, SmallCfg<32>::kSmem));
+  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<16>, syrk_smem_bytes<16>()));
+  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<32>, syrk_smem_bytes<32>()));
+  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<64>, syrk_smem_bytes<64>()));
+  CUDA_TRY(smem_attr((const void*)trsm_kernel_ptr(P.T, P.gstrip, P.wmode), P.smem_trsm));
+  if (P.ntrsm_small > 0) CUDA_TRY(smem_attr((const void*)trsm_kernel_ptr2(P.T, P.wmode), P.smem_trsm_small));
   double total = 8.0 * (P.X_doubles + P.F_doubles + P.PB_doubles + P.part_doubles);
   total += dest.size() * 4.0 + Rrows.size() * 4.0 + panels.size() * sizeof(Panel) + tiles.size() * sizeof(Tile) +
            steps.size() * sizeof(Step) + wsegs.size() * sizeof(WSeg) + groups.size() * sizeof(Group) +
@@ -1208,6 +1221,21 @@ void free_plan_device(Plan& P) {
   P.on_device = false;
 }
 
+template <bool WMODE>
+static void launch_prep_small(int bkt, int t0, int t1, Plan& P, cudaStream_t stream) {
+  const int nt = t1 - t0;
+  if (bkt == 0) {
+    using C8 = SmallCfg<8>;
+    prep_small_kernel<8, WMODE><<<(nt + C8::WARPS - 1) / C8::WARPS, 32 * C8::WARPS, C8::kSmem, stream>>>(P.dev, t0, t1);
+  } else if (bkt == 1) {
+    using C16 = SmallCfg<16>;
+    prep_small_kernel<16, WMODE><<<(nt + C16::WARPS - 1) / C16::WARPS, 32 * C16::WARPS, C16::kSmem, stream>>>(P.dev, t0, t1);
+  } else {
+    using C32 = SmallCfg<32>;
+    prep_small_kernel<32, WMODE><<<(nt + C32::WARPS - 1) / C32::WARPS, 32 * C32::WARPS, C32::kSmem, stream>>>(P.dev, t0, t1);
+  }
+}
+
 // first task of subdomain >= sub in a subdomain-major task list
 static int task_lb(const std::vector<I2>& v, int lo, int hi, int32_t sub) {
   return (int)(std::lower_bound(v.begin() + lo, v.begin() + hi, sub, [](const I2& t, int32_t s) { return t.x < s; }) -
@@ -1240,7 +1268,8 @@ static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stre
     const int npr = (int)P.prep_tasks.size();
     const int a = all ? 0 : task_lb(P.prep_tasks, 0, npr, s0), b = all ? npr : task_lb(P.prep_tasks, 0, npr, s1);
     if (b > a) {
-      prep_panel_kernel<<<b - a, kThreads, kPrepSmem, stream>>>(P.dev, a);
+      if (P.wmode) prep_panel_kernel<true><<<b - a, kThreads, kPrepSmem, stream>>>(P.dev, a);
+      else prep_panel_kernel<false><<<b - a, kThreads, kPrepSmem, stream>>>(P.dev, a);
       CUDA_TRY(cudaGetLastError());
     }
   }
@@ -1249,15 +1278,10 @@ static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stre
     const int t0 = all ? lo : task_lb(P.prep_small_tasks, lo, hi, s0);
     const int t1 = all ? hi : task_lb(P.prep_small_tasks, lo, hi, s1), nt = t1 - t0;
     if (nt <= 0) continue;
-    if (bkt == 0) {
-      using C8 = SmallCfg<8>;
-      prep_small_kernel<8><<<(nt + C8::WARPS - 1) / C8::WARPS, 32 * C8::WARPS, C8::kSmem, stream>>>(P.dev, t0, t1);
-    } else if (bkt == 1) {
-      using C16 = SmallCfg<16>;
-      prep_small_kernel<16><<<(nt + C16::WARPS - 1) / C16::WARPS, 32 * C16::WARPS, C16::kSmem, stream>>>(P.dev, t0, t1);
+    if (P.wmode) {
+      launch_prep_small<true>(bkt, t0, t1, P, stream);
     } else {
-      using C32 = SmallCfg<32>;
-      prep_small_kernel<32><<<(nt + C32::WARPS - 1) / C32::WARPS, 32 * C32::WARPS, C32::kSmem, stream>>>(P.dev, t0, t1);
+      launch_prep_small<false>(bkt, t0, t1, P, stream);
     }
     CUDA_TRY(cudaGetLastError());
   }
