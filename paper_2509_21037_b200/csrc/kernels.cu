@@ -89,24 +89,30 @@ constexpr int kLdT = kMaxPanel + 4;  // smem triangle, column-major [col][row]
 
 constexpr size_t kPrepSmem = 2 * sizeof(double) * kMaxPanel * kLdT;
 
-// Scatter the CSC values of a panel's columns: diagonal-block entries into the smem triangle D
-// (column-major, stride LDD), pruned rows into the panel buffer.  Four loads in flight per thread.
-template <int LDD>
-__device__ __forceinline__ void scatter_panel(const double* __restrict__ Lv, const int32_t* __restrict__ dest,
-                                              double* __restrict__ PB, double* D, const Panel& pn, int t, int nthr) {
-  constexpr int U = 4;
-  for (int64_t q0 = pn.csc_begin + t; q0 < pn.csc_end; q0 += (int64_t)U * nthr) {
-    double v[U];
-    int32_t d[U];
+// Scatter of the CSC values of a panel's columns: diagonal-block entries into the smem triangle D
+// (column-major, stride LDD), pruned rows into the panel buffer.  U loads in flight per thread; the
+// first batch is issued before the caller's zeroing work so its latency overlaps it.
+#ifndef SC_PREP_U
+#define SC_PREP_U 8
+#endif
+template <int U>
+struct ScatterBatch {
+  double v[U];
+  int32_t d[U];
+  __device__ __forceinline__ void load(const double* __restrict__ Lv, const int32_t* __restrict__ dest, int64_t q0,
+                                       int64_t end, int nthr) {
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int64_t q = q0 + (int64_t)u * nthr;
       d[u] = INT32_MIN;
-      if (q < pn.csc_end) {
+      if (q < end) {
         v[u] = __ldg(Lv + q);
         d[u] = __ldg(dest + q);
       }
     }
+  }
+  template <int LDD>
+  __device__ __forceinline__ void store(double* __restrict__ PB, double* D) const {
 #pragma unroll
     for (int u = 0; u < U; u++) {
       if (d[u] == INT32_MIN) continue;
@@ -117,6 +123,17 @@ __device__ __forceinline__ void scatter_panel(const double* __restrict__ Lv, con
         PB[d[u]] = v[u];
       }
     }
+  }
+};
+template <int LDD, int U>
+__device__ __forceinline__ void scatter_rest(ScatterBatch<U>& sb, const double* __restrict__ Lv,
+                                             const int32_t* __restrict__ dest, double* __restrict__ PB, double* D,
+                                             const Panel& pn, int t, int nthr) {
+  for (int64_t q0 = pn.csc_begin + t;;) {
+    sb.template store<LDD>(PB, D);
+    q0 += (int64_t)U * nthr;
+    if (q0 >= pn.csc_end) break;
+    sb.load(Lv, dest, q0, pn.csc_end, nthr);
   }
 }
 
@@ -237,9 +254,11 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0)
     double2* D2 = reinterpret_cast<double2*>(D);
     for (int q = tid; q < npad * kLdT / 2; q += kThreads) D2[q] = make_double2(0.0, 0.0);
   }
+  ScatterBatch<4> sb;
+  sb.load(Lv, dest, pn.csc_begin + tid, pn.csc_end, kThreads);
   zero_chunk_gaps(PB, pn, tid, kThreads);
   __syncthreads();
-  scatter_panel<kLdT>(Lv, dest, PB, D, pn, tid, kThreads);
+  scatter_rest<kLdT>(sb, Lv, dest, PB, D, pn, tid, kThreads);
   // unit diagonal in the padding (its inverse stays the identity)
   for (int i = kw + tid; i < npad; i += kThreads) D[i * kLdT + i] = 1.0;
   __syncthreads();
@@ -337,10 +356,12 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
   const double* __restrict__ Lv = P.Lptr[sub];
   double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
   const int kw = pn.kw, kw4 = pn.kw4;
+  ScatterBatch<SC_PREP_U> sb;
+  sb.load(Lv, dest, pn.csc_begin + lane, pn.csc_end, 32);
   for (int q = lane; q < NPAD * LD / 2; q += 32) reinterpret_cast<double2*>(D)[q] = make_double2(0.0, 0.0);
   zero_chunk_gaps(PB, pn, lane, 32);
   __syncwarp();
-  scatter_panel<LD>(Lv, dest, PB, D, pn, lane, 32);
+  scatter_rest<LD>(sb, Lv, dest, PB, D, pn, lane, 32);
   for (int i = kw + lane; i < NPAD; i += 32) D[i * LD + i] = 1.0;
   __syncwarp();
   {  // level 0: lane -> (8x8 block lane/8, column lane%8)
