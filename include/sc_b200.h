@@ -145,6 +145,19 @@ sc_status sc_assemble_batch_host(sc_plan_t p, const double* const* L_values_host
    sum; multi-GPU callers all-reduce q over ranks (torch.distributed / NCCL).  Deterministic. */
 sc_status sc_apply(sc_plan_t p, const double* lambda, double* q, void* stream);
 
+/* Factor staging only (the prep phase of sc_assemble_batch): the plan's panel buffers receive the
+   supernodal factor panels of L (inverted diagonal blocks + pruned row chunks), which is what the
+   implicit apply needs; F is not assembled.  Same argument rules as sc_assemble_batch. */
+sc_status sc_prepare_factor(sc_plan_t p, const double* const* L_values, void* stream);
+
+/* Implicit dual-operator application (eq. dualop_apply_impl): q[g] = sum_i
+   sum_{a: lambda_map_i(a) = g} (B~_i K_i^{-1} B~_i^T lambda_i)(a), computed WITHOUT F by one forward
+   and one backward substitution per subdomain with the factor staged by the last
+   sc_prepare_factor / sc_assemble_batch (SC_ERR_STATE if none).  One CTA per subdomain; its work
+   vector lives in shared memory when n_i <= 25,600, else in plan-owned global memory.  lambda, q:
+   DEVICE arrays of n_lambda_global doubles; q overwritten; deterministic. */
+sc_status sc_apply_implicit(sc_plan_t p, const double* lambda, double* q, void* stream);
+
 /* Synchronise the plan's last stream and report a sticky device error (SC_ERR_ZERO_PIVOT). */
 sc_status sc_check(sc_plan_t p);
 
@@ -177,6 +190,7 @@ sc_status sc_set_timing_events(sc_plan_t p, void* const* events, int32_t n);
 /* Number of kernel launches one sc_assemble_batch / sc_apply enqueues. */
 int32_t sc_launches_per_assemble(sc_plan_t p);
 int32_t sc_launches_per_apply(sc_plan_t p);
+int32_t sc_launches_per_apply_implicit(sc_plan_t p);
 
 /* Frees F storage, workspace and device copies (synchronises the device first). */
 void sc_plan_destroy(sc_plan_t p);

@@ -88,6 +88,24 @@ sc_status sc_apply(sc_plan_t p, const double* lambda, double* q, void* stream) {
   return st == SC_OK ? SC_OK : fail(st, err);
 }
 
+sc_status sc_prepare_factor(sc_plan_t p, const double* const* L_values, void* stream) {
+  if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
+  if (!L_values && p->P.nsub > 0) return fail(SC_ERR_INVALID_ARG, "NULL L_values");
+  std::string err;
+  sc_status st = sc::launch_prepare(p->P, L_values, stream, err);
+  return st == SC_OK ? SC_OK : fail(st, err);
+}
+
+sc_status sc_apply_implicit(sc_plan_t p, const double* lambda, double* q, void* stream) {
+  if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
+  if ((!lambda || !q) && p->P.n_lambda > 0) return fail(SC_ERR_INVALID_ARG, "NULL lambda or q");
+  std::string err;
+  sc_status st = sc::launch_apply_implicit(p->P, lambda, q, stream, err);
+  return st == SC_OK ? SC_OK : fail(st, err);
+}
+
 sc_status sc_check(sc_plan_t p) {
   if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
   if (!p->P.on_device) return SC_OK;
@@ -189,6 +207,11 @@ int32_t sc_launches_per_assemble(sc_plan_t p) {
   for (int b = 0; b < 3; b++) small += p->P.small_begin[b + 1] > p->P.small_begin[b] ? 1 : 0;
   return (p->P.prep_tasks.empty() ? 0 : 1) + small +
          (p->P.trsm_tasks.empty() ? 0 : 1) + (p->P.syrk_tasks.empty() ? 0 : 1);
+}
+
+int32_t sc_launches_per_apply_implicit(sc_plan_t p) {
+  if (!p) return 0;
+  return (p->P.nsub > 0 ? 1 : 0) + (p->P.n_lambda > 0 ? 1 : 0);
 }
 
 int32_t sc_launches_per_apply(sc_plan_t p) {

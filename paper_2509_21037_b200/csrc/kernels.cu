@@ -1033,6 +1033,108 @@ __global__ void __launch_bounds__(kThreads) apply_scatter_kernel(DevPlan P, doub
 
 
 // ------------------------------------------------------------------------------------------------
+// Implicit apply (row f2; eq. dualop_apply_impl): q = sum_i B~_i K_i^{-1} B~_i^T lambda_i
+// without F, by one forward and one backward substitution with the prepared factor panels (the
+// panel buffers of the last sc_prepare_factor / sc_assemble_batch).  One CTA per subdomain; its
+// work vector (n doubles, permuted order) in shared memory when it fits, else in global memory.
+//   forward, panels ascending:  y_p = inv(L_pp) x_p;  x[R_p] -= L[R_p,p] y_p   (W mode: W_p x_p)
+//   backward, descending:       z_p = inv(L_pp)^T (y_p - L[R_p,p]^T z[R_p])   (W mode:
+//                               z_p = inv(L_pp)^T y_p - W_p^T z[R_p])
+// ------------------------------------------------------------------------------------------------
+template <bool SMEMV>
+__global__ void __launch_bounds__(kThreads) implicit_apply_kernel(DevPlan P, const double* __restrict__ lambda) {
+  extern __shared__ __align__(16) unsigned char iv_smem[];
+  __shared__ double yv[kMaxPanel], zv[kMaxPanel];
+  const int sub = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cls = P.sub_cls[sub];
+  const int p0 = P.cls_panel0[cls], p1 = P.cls_panel0[cls + 1];
+  const int m = P.sub_m[sub];
+  const Panel last = P.panels[p1 - 1];
+  const int n = last.a + last.kw;
+  double* x = SMEMV ? reinterpret_cast<double*>(iv_smem) : P.xv + (int64_t)sub * P.max_n;
+  const double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
+  const int32_t* __restrict__ ibp = P.ib_ptr + P.cls_ib0[cls];
+  const int64_t* __restrict__ slm = P.slm + P.sub_slm_off[sub];
+  for (int i = tid; i < n; i += kThreads) x[i] = 0.0;
+  __syncthreads();
+  for (int a = tid; a < m; a += kThreads) {  // x = P B~^T lambda_i
+    const double la = lambda[slm[a]];
+    for (int e = ibp[a]; e < ibp[a + 1]; e++) atomicAdd(&x[P.ib_row[e]], P.ib_val[e] * la);
+  }
+  __syncthreads();
+  for (int p = p0; p < p1; p++) {  // forward
+    const Panel pn = P.panels[p];
+    const double* inv = PB + pn.buf_off;
+    const double* ch0 = inv + (int64_t)pn.ldD * pn.kw4;
+    if (tid < pn.kw) {
+      double y = 0.0;
+#pragma unroll 8
+      for (int k = 0; k <= tid; k++) y = fma(__ldg(inv + k * pn.ldD + tid), x[pn.a + k], y);
+      yv[tid] = y;
+    }
+    __syncthreads();
+    // chunk rows: L (Y mode) times y, or W times the old x_p (W mode)
+    for (int k = tid; k < pn.nR; k += kThreads) {
+      const int c = k / kChunk, kr = k - c * kChunk;
+      const int ld = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
+      const double* col = ch0 + (int64_t)c * kLdC * pn.kw4 + kr;
+      double s = 0.0;
+#pragma unroll 8
+      for (int j = 0; j < pn.kw; j++) s = fma(__ldg(col + j * ld), P.wmode ? x[pn.a + j] : yv[j], s);
+      x[__ldg(P.Rrows + pn.R_off + k)] -= s;
+    }
+    __syncthreads();
+    if (tid < pn.kw) x[pn.a + tid] = yv[tid];
+    __syncthreads();
+  }
+  for (int p = p1 - 1; p >= p0; p--) {  // backward
+    const Panel pn = P.panels[p];
+    const double* inv = PB + pn.buf_off;
+    const double* ch0 = inv + (int64_t)pn.ldD * pn.kw4;
+    for (int j = warp; j < pn.kw; j += kThreads / 32) {  // s_j = sum_k L[R_k, j] z[R_k]
+      double s = 0.0;
+#pragma unroll 4
+      for (int k = lane; k < pn.nR; k += 32) {
+        const int c = k / kChunk, kr = k - c * kChunk;
+        const int ld = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
+        s = fma(__ldg(ch0 + (int64_t)c * kLdC * pn.kw4 + (int64_t)j * ld + kr), x[__ldg(P.Rrows + pn.R_off + k)], s);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == 0) yv[j] = P.wmode ? s : x[pn.a + j] - s;
+    }
+    __syncthreads();
+    for (int j = warp; j < pn.kw; j += kThreads / 32) {  // z_j = sum_{r >= j} inv[r][j] v_r
+      double z = 0.0;
+      for (int r = j + lane; r < pn.kw; r += 32) z = fma(__ldg(inv + j * pn.ldD + r), P.wmode ? x[pn.a + r] : yv[r], z);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
+      if (lane == 0) zv[j] = P.wmode ? z - yv[j] : z;
+    }
+    __syncthreads();
+    if (tid < pn.kw) x[pn.a + tid] = zv[tid];
+    __syncthreads();
+  }
+  double* u = P.upart + P.sub_slm_off[sub];
+  for (int a = tid; a < m; a += kThreads) {  // u = B~ P^T z
+    double s = 0.0;
+    for (int e = ibp[a]; e < ibp[a + 1]; e++) s = fma(P.ib_val[e], x[P.ib_row[e]], s);
+    u[a] = s;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) implicit_scatter_kernel(DevPlan P, double* __restrict__ q, int64_t nl) {
+  const int64_t gidx = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+  if (gidx >= nl) return;
+  double s = 0.0;
+  for (int64_t p = P.qg_ptr[gidx]; p < P.qg_ptr[gidx + 1]; p++) {
+    const int64_t sa = P.qg_sub_a[p];
+    s += P.upart[P.sub_slm_off[(int)(sa >> 32)] + (sa & 0xffffffff)];
+  }
+  q[gidx] = s;
+}
+
+// ------------------------------------------------------------------------------------------------
 // host side
 // ------------------------------------------------------------------------------------------------
 namespace {
@@ -1134,6 +1236,25 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, pairs, &D.pairs, err));
   TRY(upload(P, segs, &D.segs, err));
   TRY(upload(P, P.sub_cls, &D.sub_cls, err));
+  {
+    std::vector<int32_t> cp0(P.cls_panel_begin);
+    cp0.push_back((int32_t)panels.size());
+    TRY(upload(P, cp0, &D.cls_panel0, err));
+    std::vector<int64_t> ib0;
+    std::vector<int32_t> ibp, ibr;
+    std::vector<double> ibv;
+    for (auto& C : P.classes) {
+      ib0.push_back((int64_t)ibp.size());
+      for (int32_t v : C.ib_ptr) ibp.push_back(v + (int32_t)ibr.size());
+      ibr.insert(ibr.end(), C.ib_row.begin(), C.ib_row.end());
+      ibv.insert(ibv.end(), C.ib_val.begin(), C.ib_val.end());
+    }
+    TRY(upload(P, ib0, &D.cls_ib0, err));
+    TRY(upload(P, ibp, &D.ib_ptr, err));
+    TRY(upload(P, ibr, &D.ib_row, err));
+    TRY(upload(P, ibv, &D.ib_val, err));
+    TRY(alloc_zero(P, (int64_t)P.slm.size(), &D.upart, err));
+  }
   TRY(upload(P, P.sub_X_base, &D.sub_X_base, err));
   TRY(upload(P, P.sub_F_base, &D.sub_F_base, err));
   TRY(upload(P, P.sub_PB_base, &D.sub_PB_base, err));
@@ -1280,11 +1401,9 @@ static sc_status set_Lptr(Plan& P, const double* const* Lptr_host, cudaStream_t 
   return SC_OK;
 }
 
-// All phases (prep, TRSM, SYRK) for the subdomains [s0, s1) on `stream`; timing events only for the
-// whole batch.
-static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, bool timing, std::string& err) {
+// prep kernels (factor panels) for the subdomains [s0, s1)
+static sc_status launch_prep_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, std::string& err) {
   const bool all = s0 == 0 && s1 == P.nsub;
-  if (timing && P.tev[0]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[0], stream));
   {
     const int npr = (int)P.prep_tasks.size();
     const int a = all ? 0 : task_lb(P.prep_tasks, 0, npr, s0), b = all ? npr : task_lb(P.prep_tasks, 0, npr, s1);
@@ -1305,6 +1424,18 @@ static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stre
       launch_prep_small<false>(bkt, t0, t1, P, stream);
     }
     CUDA_TRY(cudaGetLastError());
+  }
+  return SC_OK;
+}
+
+// All phases (prep, TRSM, SYRK) for the subdomains [s0, s1) on `stream`; timing events only for the
+// whole batch.
+static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, bool timing, std::string& err) {
+  const bool all = s0 == 0 && s1 == P.nsub;
+  if (timing && P.tev[0]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[0], stream));
+  {
+    sc_status st = launch_prep_range(P, s0, s1, stream, err);
+    if (st != SC_OK) return st;
   }
   if (timing && P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
   {
@@ -1355,6 +1486,7 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
   sc_status st = set_Lptr(P, Lptr_host, stream, err);
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
+  P.factor_ready = true;
   return launch_range(P, 0, P.nsub, stream, true, err);
 }
 
@@ -1392,6 +1524,7 @@ sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* str
   sc_status st = set_Lptr(P, dptrs.data(), stream, err);
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
+  P.factor_ready = true;
   cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream);
   // the staging buffer is reused: copies wait for everything enqueued on `stream` before this call
   CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_start), stream));
@@ -1435,6 +1568,49 @@ sc_status launch_apply(Plan& P, const double* lambda, double* q, void* stream_v,
   if (P.n_lambda > 0) {
     const int64_t nb = (P.n_lambda + kThreads - 1) / kThreads;
     apply_scatter_kernel<<<(unsigned)nb, kThreads, 0, stream>>>(P.dev, q, P.n_lambda);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return SC_OK;
+}
+
+sc_status launch_prepare(Plan& P, const double* const* Lptr_host, void* stream_v, std::string& err) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  CUDA_TRY(cudaSetDevice(P.opt.device));
+  sc_status st = set_Lptr(P, Lptr_host, stream, err);
+  if (st != SC_OK) return st;
+  P.last_stream = stream_v;
+  st = launch_prep_range(P, 0, P.nsub, stream, err);
+  if (st == SC_OK) P.factor_ready = true;
+  return st;
+}
+
+sc_status launch_apply_implicit(Plan& P, const double* lambda, double* q, void* stream_v, std::string& err) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  CUDA_TRY(cudaSetDevice(P.opt.device));
+  if (!P.factor_ready) {
+    err = "no prepared factor: call sc_prepare_factor or sc_assemble_batch first";
+    return SC_ERR_STATE;
+  }
+  P.last_stream = stream_v;
+  const size_t vbytes = sizeof(double) * (size_t)P.max_n;
+  const bool in_smem = vbytes <= 200 * 1024;
+  if (!in_smem && !P.dev.xv) {
+    double* xv = nullptr;
+    TRY(alloc_zero(P, (int64_t)P.nsub * P.max_n, &xv, err));
+    P.dev.xv = xv;
+  }
+  if (P.nsub > 0) {
+    if (in_smem) {
+      CUDA_TRY(cudaFuncSetAttribute(implicit_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vbytes));
+      implicit_apply_kernel<true><<<P.nsub, kThreads, vbytes, stream>>>(P.dev, lambda);
+    } else {
+      implicit_apply_kernel<false><<<P.nsub, kThreads, 0, stream>>>(P.dev, lambda);
+    }
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (P.n_lambda > 0) {
+    const int64_t nb = (P.n_lambda + kThreads - 1) / kThreads;
+    implicit_scatter_kernel<<<(unsigned)nb, kThreads, 0, stream>>>(P.dev, q, P.n_lambda);
     CUDA_TRY(cudaGetLastError());
   }
   return SC_OK;

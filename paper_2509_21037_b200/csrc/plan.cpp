@@ -315,6 +315,15 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
   std::stable_sort(C.sigma.begin(), C.sigma.end(), [&](int32_t a, int32_t b) { return piv[(size_t)a] < piv[(size_t)b]; });
   C.pivot.resize((size_t)m);
   for (int32_t a = 0; a < m; a++) C.pivot[(size_t)a] = piv[(size_t)C.sigma[(size_t)a]];
+  // B~^T by stepped column, rows permuted (for the implicit apply)
+  C.ib_ptr.assign((size_t)m + 1, 0);
+  for (int32_t a = 0; a < m; a++) {
+    for (auto& e : bcol[(size_t)C.sigma[(size_t)a]]) {
+      C.ib_row.push_back(e.first);
+      C.ib_val.push_back(e.second);
+    }
+    C.ib_ptr[(size_t)a + 1] = (int32_t)C.ib_row.size();
+  }
 
   // --- work counters: c_k = #columns whose X(k,:) is structurally non-zero
   {

@@ -158,6 +158,8 @@ struct ClassPlan {
   std::vector<Group> groups;
   std::vector<Reach> greach;
   std::vector<BInit> binit;
+  std::vector<int32_t> ib_ptr, ib_row;  // B~^T by stepped column (m+1 pointers, permuted rows)
+  std::vector<double> ib_val;
   std::vector<Pair> pairs;
   std::vector<Seg> segs;
   int64_t x_doubles = 0;           // X region (group strips) per subdomain
@@ -192,6 +194,13 @@ struct DevPlan {
   const Pair* pairs;
   const Seg* segs;
   const int32_t* sub_cls;          // per subdomain
+  const int32_t* cls_panel0;       // per class: first global panel, then (next entry) the end
+  const int64_t* cls_ib0;          // per class: offset into ib_ptr; ib_ptr values are global entry indices
+  const int32_t* ib_ptr;
+  const int32_t* ib_row;
+  const double* ib_val;
+  double* upart;                   // implicit apply: per (subdomain, stepped column) result, sub_slm_off
+  double* xv;                      // implicit apply: per subdomain work vector (n doubles) if not in smem
   const int64_t* sub_X_base;       // per subdomain, doubles
   const int64_t* sub_F_base;       // per subdomain, doubles (F' lower, column-major, ld = m)
   const int64_t* sub_PB_base;      // per subdomain panel buffer, doubles
@@ -214,6 +223,7 @@ struct DevPlan {
   double* part;
   unsigned long long* err;         // sticky device error: ((sub+1) << 32) | col
   int32_t nsub, max_n, T, G;
+  int32_t factor_ready;            // (host-side bookkeeping mirrors Plan::factor_ready)
   int32_t wmode;                         // 1: chunks hold W_p = L[R_p,p] inv(L_pp) (W mode), 0: L (Y mode)
 };
 
@@ -221,6 +231,7 @@ struct Plan {
   sc_options opt{};
   int32_t T = 32, G = 64, PW = 64, ring_bytes = 0;
   bool gstrip = false;             // X strips solved in place in the group strips (global memory)
+  bool factor_ready = false;       // panel buffers hold the factor of the last prepare / assemble
   bool wmode = true;               // TRSM update operand W_p = L[R_p,p] inv(L_pp) (wide panels) or L (Y mode)
   int32_t nsub = 0;
   std::vector<ClassPlan> classes;
@@ -270,6 +281,8 @@ sc_status upload_plan(Plan& P, std::string& err);
 void free_plan_device(Plan& P);
 sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream, std::string& err);
 sc_status launch_apply(Plan& P, const double* lambda, double* q, void* stream, std::string& err);
+sc_status launch_prepare(Plan& P, const double* const* Lptr_host, void* stream, std::string& err);
+sc_status launch_apply_implicit(Plan& P, const double* lambda, double* q, void* stream, std::string& err);
 sc_status device_check(Plan& P, std::string& err);
 sc_status copy_F_lower(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
 sc_status copy_X_strips(Plan& P, int32_t i, std::vector<double>& out, std::string& err);

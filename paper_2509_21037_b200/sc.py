@@ -63,7 +63,8 @@ _lib = None
 EXPORTS = ["sc_options_default", "sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply",
            "sc_check", "sc_get_F", "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_plan_subdomain_costs",
            "sc_set_timing_events", "sc_launches_per_assemble",
-           "sc_launches_per_apply", "sc_plan_destroy", "sc_last_error"]
+           "sc_launches_per_apply", "sc_plan_destroy", "sc_last_error", "sc_prepare_factor", "sc_apply_implicit",
+           "sc_launches_per_apply_implicit"]
 
 
 def lib():
@@ -81,6 +82,10 @@ def lib():
     L.sc_assemble_batch_host.argtypes = [_P, ctypes.POINTER(_P), _P]
     L.sc_apply.argtypes = [_P, _P, _P, _P]
     L.sc_check.argtypes = [_P]
+    L.sc_prepare_factor.argtypes = [_P, ctypes.POINTER(_P), _P]
+    L.sc_apply_implicit.argtypes = [_P, _P, _P, _P]
+    L.sc_launches_per_apply_implicit.argtypes = [_P]
+    L.sc_launches_per_apply_implicit.restype = ctypes.c_int32
     L.sc_get_F.argtypes = [_P, ctypes.c_int32, _P, ctypes.c_int64]
     L.sc_get_X.argtypes = [_P, ctypes.c_int32, _P, _P]
     L.sc_plan_strip_rows.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _P, _P]
@@ -96,6 +101,7 @@ def lib():
     L.sc_last_error.argtypes = []
     L.sc_last_error.restype = ctypes.c_char_p
     for f in ("sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply", "sc_check", "sc_get_F",
+              "sc_prepare_factor", "sc_apply_implicit",
               "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_set_timing_events", "sc_plan_subdomain_costs"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -180,6 +186,17 @@ class SCPlan:
         _check(lib().sc_assemble_batch_host(self._h, ptrs, _stream_handle(stream)))
 
     # -- solution
+    def prepare_factor(self, L_values: Sequence, stream=None):
+        """Stage the factor panels only (no F): what apply_implicit needs."""
+        ptrs = (_P * max(self.nsub, 1))()
+        for i, t in enumerate(L_values):
+            ptrs[i] = t if isinstance(t, int) else t.data_ptr()
+        _check(lib().sc_prepare_factor(self._h, ptrs, _stream_handle(stream)))
+
+    def apply_implicit(self, lam, q, stream=None):
+        """q <- sum_i scatter(B~_i K_i^{-1} B~_i^T gather(lam)) without F (two substitutions per subdomain)."""
+        _check(lib().sc_apply_implicit(self._h, lam.data_ptr(), q.data_ptr(), _stream_handle(stream)))
+
     def apply(self, lam, q, stream=None):
         """q <- sum_i scatter(F_i gather(lam)) over this plan's subdomains (device tensors, float64)."""
         _check(lib().sc_apply(self._h, lam.data_ptr(), q.data_ptr(), _stream_handle(stream)))
