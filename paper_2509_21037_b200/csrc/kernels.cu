@@ -430,6 +430,9 @@ static_assert(kLdC == block_ld(kChunk), "chunk ld");
 #ifndef SC_WN16
 #define SC_WN16 1
 #endif
+#ifndef SC_GEMM1_SPLIT
+#define SC_GEMM1_SPLIT 2
+#endif
 #ifndef SC_WN32
 #define SC_WN32 1
 #endif
@@ -691,9 +694,10 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, MINB) trsm_smem_kernel(De
     // k < 8 (i + 1)); kept in registers until the step's barrier
     double yn[WM][WN][2];
     {
-      double ya[2][WM][WN][2];
+      constexpr int YS = SC_GEMM1_SPLIT;  // independent accumulator sets (k steps round-robin)
+      double ya[YS][WM][WN][2];
 #pragma unroll
-      for (int h = 0; h < 2; h++)
+      for (int h = 0; h < YS; h++)
 #pragma unroll
         for (int i = 0; i < WM; i++)
 #pragma unroll
@@ -713,7 +717,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, MINB) trsm_smem_kernel(De
 #pragma unroll
             for (int i = 0; i < WM; i++)
 #pragma unroll
-              for (int j = 0; j < WN; j++) dmma(ya[ks & 1][i][j][0], ya[ks & 1][i][j][1], a[i], yf[ks][j]);
+              for (int j = 0; j < WN; j++) dmma(ya[ks % YS][i][j][0], ya[ks % YS][i][j][1], a[i], yf[ks][j]);
           }
         }
       }
@@ -723,8 +727,13 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, MINB) trsm_smem_kernel(De
       for (int i = 0; i < WM; i++)
 #pragma unroll
         for (int j = 0; j < WN; j++) {
-          yn[i][j][0] = ya[0][i][j][0] + ya[1][i][j][0];
-          yn[i][j][1] = ya[0][i][j][1] + ya[1][i][j][1];
+          yn[i][j][0] = ya[0][i][j][0];
+          yn[i][j][1] = ya[0][i][j][1];
+#pragma unroll
+          for (int h = 1; h < YS; h++) {
+            yn[i][j][0] += ya[h][i][j][0];
+            yn[i][j][1] += ya[h][i][j][1];
+          }
         }
     }
     if constexpr (YM) {
