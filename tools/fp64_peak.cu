@@ -22,6 +22,41 @@ __global__ void dmma_loop(const double* a, double* c) {
   if (s == 12345.678) c[threadIdx.x] = s;
 }
 
+// sm_90+ FP64 shapes: m16n8k4 (A 2, B 1, C 4 doubles per lane), m16n8k8 (A 4, B 2), m16n8k16 (A 8, B 4)
+template <int ITER, int K>
+__global__ void dmma16_loop(const double* a, double* c) {
+  double x[8], y[4];
+#pragma unroll
+  for (int i = 0; i < 8; i++) x[i] = a[(threadIdx.x + i) & 31];
+#pragma unroll
+  for (int i = 0; i < 4; i++) y[i] = a[(threadIdx.x + 5 + i) & 31];
+  double d[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; i++) d[i][0] = d[i][1] = d[i][2] = d[i][3] = 0.0;
+  for (int it = 0; it < ITER; it++) {
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      if constexpr (K == 4)
+        asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+                     : "+d"(d[i][0]), "+d"(d[i][1]), "+d"(d[i][2]), "+d"(d[i][3]) : "d"(x[0]), "d"(x[1]), "d"(y[0]));
+      else if constexpr (K == 8)
+        asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+                     : "+d"(d[i][0]), "+d"(d[i][1]), "+d"(d[i][2]), "+d"(d[i][3])
+                     : "d"(x[0]), "d"(x[1]), "d"(x[2]), "d"(x[3]), "d"(y[0]), "d"(y[1]));
+      else
+        asm volatile("mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+                     "{%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
+                     : "+d"(d[i][0]), "+d"(d[i][1]), "+d"(d[i][2]), "+d"(d[i][3])
+                     : "d"(x[0]), "d"(x[1]), "d"(x[2]), "d"(x[3]), "d"(x[4]), "d"(x[5]), "d"(x[6]), "d"(x[7]),
+                       "d"(y[0]), "d"(y[1]), "d"(y[2]), "d"(y[3]));
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; i++) s += d[i][0] + d[i][1] + d[i][2] + d[i][3];
+  if (s == 12345.678) c[threadIdx.x] = s;
+}
+
 template <int ITER>
 __global__ void dfma_loop(const double* a, double* c) {
   double x = a[threadIdx.x & 31], y = a[(threadIdx.x + 3) & 31];
@@ -70,6 +105,23 @@ int main() {
       flops = 2.0 * 32 * 16 * (double)ITER * blocks * warps;
       if (rep) printf("{\"kind\":\"dfma\",\"warps_per_cta\":%d,\"ctas\":%d,\"tflops\":%.3f}\n", warps, blocks, flops / ms / 1e9);
     }
+  }
+  for (int warps = 4; warps <= 16; warps *= 2) {
+    const int blocks = nsm * 2, threads = warps * 32;
+    float ms;
+    auto run = [&](auto kern, int k, const char* name) {
+      kern<<<blocks, threads>>>(a, c);
+      cudaEventRecord(e0);
+      kern<<<blocks, threads>>>(a, c);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      cudaEventElapsedTime(&ms, e0, e1);
+      const double flops = 2.0 * 16 * 8 * k * 8 * (double)ITER * blocks * warps;
+      printf("{\"kind\":\"%s\",\"warps_per_cta\":%d,\"ctas\":%d,\"tflops\":%.3f}\n", name, warps, blocks, flops / ms / 1e9);
+    };
+    run(dmma16_loop<ITER, 4>, 4, "dmma_m16n8k4");
+    run(dmma16_loop<ITER, 8>, 8, "dmma_m16n8k8");
+    run(dmma16_loop<ITER, 16>, 16, "dmma_m16n8k16");
   }
   printf("sms=%d err=%s\n", nsm, cudaGetErrorString(cudaGetLastError()));
   return 0;
