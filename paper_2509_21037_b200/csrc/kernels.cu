@@ -430,6 +430,9 @@ static_assert(kLdC == block_ld(kChunk), "chunk ld");
 #ifndef SC_WN16
 #define SC_WN16 1
 #endif
+#ifndef SC_NCW
+#define SC_NCW 8
+#endif
 #ifndef SC_GEMM1_SPLIT
 #define SC_GEMM1_SPLIT 2
 #endif
@@ -443,7 +446,7 @@ struct TileCfg {
   // 8 consumer warps (16 measured slower: 3.0 vs 2.6 ms cfg2, 17.2 vs 15.5 ms cfg3), one column
   // block each (keeps the register-resident Y fragments small); a 64 x T chunk product is
   // (8 / warp rows) row blocks per warp
-  static constexpr int NCW = 8;
+  static constexpr int NCW = T == 8 ? 8 : SC_NCW;
   static constexpr int CT = NCW * 32;           // consumer threads
   static constexpr int WN = T >= 32 ? SC_WN32 : (T == 16 ? SC_WN16 : 1);  // column blocks per warp
   static constexpr int NWC = NB / WN;           // warps along the columns
@@ -1149,6 +1152,14 @@ __global__ void __launch_bounds__(kThreads) implicit_scatter_kernel(DevPlan P, d
 namespace {
 
 using TrsmFn = void (*)(DevPlan, TrsmLaunch);
+int trsm_threads(int T) {
+  switch (T) {
+    case 8: return TileCfg<8>::CT + 32;
+    case 16: return TileCfg<16>::CT + 32;
+    case 32: return TileCfg<32>::CT + 32;
+    default: return TileCfg<64>::CT + 32;
+  }
+}
 template <bool YM>
 TrsmFn trsm_kernel_ptr_m(int T, bool gs) {
   switch (T) {
@@ -1459,16 +1470,16 @@ static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stre
       cudaStream_t side = static_cast<cudaStream_t>(P.side_stream);
       CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_fork), stream));
       CUDA_TRY(cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(P.ev_fork), 0));
-      fn<<<nl, TileCfg<8>::CT + 32, P.smem_trsm, side>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
+      fn<<<nl, trsm_threads(P.T), P.smem_trsm, side>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_join), side));
-      fn2<<<ns, TileCfg<8>::CT + 32, P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
+      fn2<<<ns, trsm_threads(P.T), P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(P.ev_join), 0));
     } else if (ns > 0) {
-      fn2<<<ns, TileCfg<8>::CT + 32, P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
+      fn2<<<ns, trsm_threads(P.T), P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
     } else if (nl > 0) {
-      fn<<<nl, TileCfg<8>::CT + 32, P.smem_trsm, stream>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
+      fn<<<nl, trsm_threads(P.T), P.smem_trsm, stream>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
     }
     CUDA_TRY(cudaGetLastError());
   }
