@@ -433,6 +433,15 @@ static_assert(kLdC == block_ld(kChunk), "chunk ld");
 #ifndef SC_NCW
 #define SC_NCW 8
 #endif
+#ifndef SC_KSPLIT
+#define SC_KSPLIT 1   // chunk-product accumulator sets per output block, <= 2 blocks per warp
+#endif                // (1 / 2 / 4 / 8 measured: fewer is faster, cfg2 TRSM 1.56 / 1.59 / 1.72 / - ms)
+#ifndef SC_KSPLIT4
+#define SC_KSPLIT4 1  // same for 4 output blocks per warp (T = 32): 1 vs 2 -> cfg4 TRSM 54.5 vs 59.4 ms
+#endif
+#ifndef SC_CHUNK_PIPE
+#define SC_CHUNK_PIPE 0
+#endif
 #ifndef SC_GEMM1_SPLIT
 #define SC_GEMM1_SPLIT 2
 #endif
@@ -762,40 +771,46 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, MINB) trsm_smem_kernel(De
       }
     }
     // X[R_p] -= W_p X_p (W mode) or L[R_p, p] Y (Y mode), one 64-row chunk (one ring block) at a
-    // time; chunks update disjoint rows and each warp releases its ring slot itself
-    for (int c = 0; c < pn.nchunk; c++) {
+    // time; chunks update disjoint rows and each warp releases its ring slot itself.  Software
+    // pipelined over chunk pairs: the read-modify-write of chunk c - 1 runs while the tensor cores
+    // work on chunk c (two accumulator sets, no register copies).
+    // (pipelined only where registers allow: 2 output blocks per warp, one CTA per SM)
+    constexpr bool PIPE = SC_CHUNK_PIPE && (WM * WN <= 2) && MINB == 1;
+    constexpr int KSPLIT = PIPE ? 2 : ((WM * WN <= 2) ? SC_KSPLIT : SC_KSPLIT4);
+    struct ChunkAcc {
+      double acc[KSPLIT][WM][WN][2];
+      double2 xold[WM][WN];
+      int sr[WM];
+      bool on;
+    };
+    auto issue = [&](int c, ChunkAcc& R) {
       b++;
       const int rows_c = min(kChunk, pn.nR - c * kChunk);
       const int ld = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
       const int slot = b % kSlots;
       mbar_wait(&full[slot], (uint32_t)(b / kSlots) & 1u);
       const double* A = reinterpret_cast<const double*>(ring + rec[slot].off);
-      int sr[WM];
 #pragma unroll
-      for (int i = 0; i < WM; i++) sr[i] = (int)srow[slot * kChunk + (br0 + i) * 8 + g];
-      // global strip: fetch the rows to update before the products (L2 latency under the DMMAs)
-      double2 xold[WM][WN];
-      if constexpr (GS) {
-        if (br0 * 8 < rows_c) {
+      for (int i = 0; i < WM; i++) R.sr[i] = (int)srow[slot * kChunk + (br0 + i) * 8 + g];
+      R.on = br0 * 8 < rows_c;
+      if constexpr (GS) {  // global strip: fetch the rows to update before the products
+        if (R.on) {
 #pragma unroll
           for (int i = 0; i < WM; i++)
 #pragma unroll
             for (int j = 0; j < WN; j++)
-              xold[i][j] = (sr[i] == 0xFFFF) ? make_double2(0.0, 0.0)
-                                             : *reinterpret_cast<const double2*>(Xs + xi(sr[i], (bc0 + j) * 8 + 2 * t4));
+              R.xold[i][j] = (R.sr[i] == 0xFFFF)
+                                 ? make_double2(0.0, 0.0)
+                                 : *reinterpret_cast<const double2*>(Xs + xi(R.sr[i], (bc0 + j) * 8 + 2 * t4));
         }
       }
-      // KSPLIT independent accumulators per output block (k steps round-robin) keep enough DMMA
-      // chains in flight per warp
-      constexpr int KSPLIT = (WM * WN <= 2) ? 4 : 2;
-      double acc[KSPLIT][WM][WN][2];
-      if (br0 * 8 < rows_c) {
+      if (R.on) {
 #pragma unroll
         for (int h = 0; h < KSPLIT; h++)
 #pragma unroll
           for (int i = 0; i < WM; i++)
 #pragma unroll
-            for (int j = 0; j < WN; j++) acc[h][i][j][0] = acc[h][i][j][1] = 0.0;
+            for (int j = 0; j < WN; j++) R.acc[h][i][j][0] = R.acc[h][i][j][1] = 0.0;
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) {
           if (ks % 4 == 0 && 4 * ks >= kw4) break;  // warp-uniform exit per group of 4 k steps
@@ -807,36 +822,53 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, MINB) trsm_smem_kernel(De
             for (int i = 0; i < WM; i++)
 #pragma unroll
               for (int j = 0; j < WN; j++)
-                dmma(acc[ks % KSPLIT][i][j][0], acc[ks % KSPLIT][i][j][1], a[i], yf[ks][j]);
+                dmma(R.acc[ks % KSPLIT][i][j][0], R.acc[ks % KSPLIT][i][j][1], a[i], yf[ks][j]);
           }
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
-      if (br0 * 8 < rows_c) {
+    };
+    auto finish = [&](ChunkAcc& R) {
+      if (!R.on) return;
 #pragma unroll
-        for (int i = 0; i < WM; i++) {
-          if (sr[i] == 0xFFFF) continue;  // row outside this tile's reach (or padding): update is 0
+      for (int i = 0; i < WM; i++) {
+        if (R.sr[i] == 0xFFFF) continue;  // row outside this tile's reach (or padding): update is 0
 #pragma unroll
-          for (int j = 0; j < WN; j++) {
-            double s0 = acc[0][i][j][0], s1 = acc[0][i][j][1];
+        for (int j = 0; j < WN; j++) {
+          double s0 = R.acc[0][i][j][0], s1 = R.acc[0][i][j][1];
 #pragma unroll
-            for (int h = 1; h < KSPLIT; h++) {
-              s0 += acc[h][i][j][0];
-              s1 += acc[h][i][j][1];
-            }
-            double2* p = reinterpret_cast<double2*>(Xs + xi(sr[i], (bc0 + j) * 8 + 2 * t4));
-            double2 v;
-            if constexpr (GS) {
-              v = xold[i][j];
-            } else {
-              v = *p;
-            }
-            v.x -= s0;
-            v.y -= s1;
-            *p = v;
+          for (int h = 1; h < KSPLIT; h++) {
+            s0 += R.acc[h][i][j][0];
+            s1 += R.acc[h][i][j][1];
           }
+          double2* p = reinterpret_cast<double2*>(Xs + xi(R.sr[i], (bc0 + j) * 8 + 2 * t4));
+          double2 v;
+          if constexpr (GS) {
+            v = R.xold[i][j];
+          } else {
+            v = *p;
+          }
+          v.x -= s0;
+          v.y -= s1;
+          *p = v;
         }
+      }
+    };
+    if constexpr (PIPE) {
+      ChunkAcc S0, S1;
+      for (int c = 0; c < pn.nchunk; c += 2) {
+        issue(c, S0);
+        if (c >= 1) finish(S1);  // chunk c - 1
+        if (c + 1 < pn.nchunk) issue(c + 1, S1);
+        finish(S0);
+      }
+      if (pn.nchunk > 0 && (pn.nchunk & 1) == 0) finish(S1);
+    } else {
+      ChunkAcc S0;
+      for (int c = 0; c < pn.nchunk; c++) {
+        issue(c, S0);
+        finish(S0);
       }
     }
     // the column-block group's R_p updates are visible before the next panel reads its rows, and
