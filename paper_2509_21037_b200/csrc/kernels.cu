@@ -954,11 +954,18 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
       kn = min(kKC, s.len - ck0);
       double* As = Sbuf + (2 * stage) * kKC * kLdG;
       double* Bs = As + kKC * kLdG;
-      for (int q = tid; q < kKC * (kGroup / 2); q += kThreads) {
-        const int r = q / (kGroup / 2), j = 2 * (q - r * (kGroup / 2));
-        const int rr = r < kn ? r : 0;
-        cp_async16(As + r * kLdG + j, XI + (int64_t)(s.offI + ck0 + rr) * kGroup + j, r < kn ? 16 : 0);
-        cp_async16(Bs + r * kLdG + j, XJ + (int64_t)(s.offJ + ck0 + rr) * kGroup + j, r < kn ? 16 : 0);
+      // thread -> (row r0 + u * RSTEP, column pair j): fixed per thread, only the row bases move
+      constexpr int CP = kGroup / 2, RSTEP = kThreads / CP, NU = kKC / RSTEP;
+      const int r0 = tid / CP, j = 2 * (tid % CP);
+      const double* srcI = XI + (int64_t)(s.offI + ck0) * kGroup + j;
+      const double* srcJ = XJ + (int64_t)(s.offJ + ck0) * kGroup + j;
+#pragma unroll
+      for (int u = 0; u < NU; u++) {
+        const int r = r0 + u * RSTEP;
+        const int ok = r < kn;
+        const int rr = ok ? r : 0;
+        cp_async16(As + r * kLdG + j, srcI + rr * kGroup, ok ? 16 : 0);
+        cp_async16(Bs + r * kLdG + j, srcJ + rr * kGroup, ok ? 16 : 0);
       }
       ck0 += kKC;
       if (ck0 >= s.len) {
@@ -979,7 +986,7 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
     const double* Bs = As + kKC * kLdG;
     const int kn4 = (kn + 3) & ~3;
     if (active) {
-      for (int k = 0; k < kn4; k += 4) {
+      auto kstep = [&](int k) {
         double a[WM], b[WN];
 #pragma unroll
         for (int i = 0; i < WM; i++) a[i] = As[(k + t4) * kLdG + (br0 + i) * 8 + g];
@@ -989,6 +996,12 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
         for (int i = 0; i < WM; i++)
 #pragma unroll
           for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      };
+      if (kn4 == kKC) {  // full chunk: fixed trip count, fully unrolled
+#pragma unroll
+        for (int k = 0; k < kKC; k += 4) kstep(k);
+      } else {
+        for (int k = 0; k < kn4; k += 4) kstep(k);
       }
     }
     __syncthreads();
