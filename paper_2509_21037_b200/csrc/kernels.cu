@@ -156,17 +156,15 @@ __device__ __forceinline__ void zero_chunk_gaps(double* PB, const Panel& pn, int
     const int ld = (ch == pn.nchunk - 1) ? pn.ldLast : kLdC;
     const int rows = (ch == pn.nchunk - 1) ? last_rows : kChunk;
     double* blk = c0 + (int64_t)ch * kLdC * kw4;
-    const int gap = ld - rows;
-    // rows [rows, ld) of columns [0, kw) and all ld rows of columns [kw, kw4)
-    for (int q = t; q < gap * pn.kw + ld * (kw4 - pn.kw); q += nthr) {
-      if (q < gap * pn.kw) {
-        const int c = q / gap;
-        blk[(int64_t)c * ld + rows + (q - c * gap)] = 0.0;
-      } else {
-        const int q2 = q - gap * pn.kw;
-        blk[(int64_t)(pn.kw + q2 / ld) * ld + (q2 % ld)] = 0.0;
-      }
+    const int gap = ld - rows;  // < 8
+    // rows [rows, ld) of columns [0, kw) (8 slots per column, no integer division) and all ld rows
+    // of columns [kw, kw4)
+    for (int q = t; q < 8 * pn.kw; q += nthr) {
+      const int c = q >> 3, r = q & 7;
+      if (r < gap) blk[(int64_t)c * ld + rows + r] = 0.0;
     }
+    for (int c = pn.kw; c < kw4; c++)
+      for (int r = t; r < ld; r += nthr) blk[(int64_t)c * ld + r] = 0.0;
   }
 }
 
@@ -269,16 +267,19 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0)
   // squares serve as the temporary C inv(A).
   if (warp * 8 < npad && lane < 8) {
     const int base = warp * 8, j = lane;
+    // one division per lane: lane j holds 1 / d_jj, broadcast by shuffles
+    const double djj = D[(base + j) * kLdT + base + j];
+    if (base + j < kw && (!(djj > 0.0) || !isfinite(djj)))
+      atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + base + j));
+    const double rj = 1.0 / djj;
     double x[8];
 #pragma unroll
     for (int i = 0; i < 8; i++) {
       double s = (i == j) ? 1.0 : 0.0;
 #pragma unroll
       for (int k = 0; k < i; k++) s -= (k >= j) ? D[(base + k) * kLdT + base + i] * x[k] : 0.0;
-      const double dii = D[(base + i) * kLdT + base + i];
-      if (base + i < kw && (!(dii > 0.0) || !isfinite(dii)))
-        atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + base + i));
-      x[i] = (i >= j) ? s / dii : 0.0;
+      const double ri = __shfl_sync(0xffu, rj, i);  // every lane of the mask shuffles
+      x[i] = (i >= j) ? s * ri : 0.0;
     }
 #pragma unroll
     for (int i = 0; i < 8; i++) W[(base + j) * kLdT + base + i] = x[i];
@@ -319,10 +320,8 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0)
   // write inv(L_pp): ldD x kw4 column-major, zero outside [0,kw) x [0,kw)
   double* Dinv = PB + pn.buf_off;
   const int ldD = pn.ldD;
-  for (int q = tid; q < ldD * kw4; q += kThreads) {
-    const int j = q / ldD, i = q - j * ldD;
-    Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * kLdT + i] : 0.0;
-  }
+  for (int j = warp; j < kw4; j += kThreads / 32)  // warp per column, lanes over rows
+    for (int i = lane; i < ldD; i += 32) Dinv[j * ldD + i] = (i < kw && j < kw && i >= j) ? W[j * kLdT + i] : 0.0;
   // chunks: L[R_p, p] -> W_p = L[R_p, p] inv(L_pp) (the TRSM's update operand)
   if constexpr (WMODE) chunks_times_inverse<kLdT, kMaxPanel>(PB, pn, W, warp, kThreads / 32, lane);
 }
@@ -364,20 +363,24 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
   scatter_rest<LD>(sb, Lv, dest, PB, D, pn, lane, 32);
   for (int i = kw + lane; i < NPAD; i += 32) D[i * LD + i] = 1.0;
   __syncwarp();
-  {  // level 0: lane -> (8x8 block lane/8, column lane%8)
+  {  // level 0: lane -> (8x8 block lane/8, column lane%8); all lanes run (blocks past NPAD read a
+     // clamped block and store nothing) so the reciprocals can be shuffled with a full mask
     const int base = (lane >> 3) * 8, j = lane & 7;
+    const int rb = base < NPAD ? base : 0;
+    const double djj = D[(rb + j) * LD + rb + j];
+    if (base < NPAD && base + j < kw && (!(djj > 0.0) || !isfinite(djj)))
+      atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + base + j));
+    const double rj = 1.0 / djj;  // one division per lane, broadcast within the 8-lane group
+    double x[8];
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      double s = (i == j) ? 1.0 : 0.0;
+#pragma unroll
+      for (int k = 0; k < i; k++) s -= (k >= j) ? D[(rb + k) * LD + rb + i] * x[k] : 0.0;
+      const double ri = __shfl_sync(0xffffffffu, rj, (lane & ~7) + i);  // every lane shuffles
+      x[i] = (i >= j) ? s * ri : 0.0;
+    }
     if (base < NPAD) {
-      double x[8];
-#pragma unroll
-      for (int i = 0; i < 8; i++) {
-        double s = (i == j) ? 1.0 : 0.0;
-#pragma unroll
-        for (int k = 0; k < i; k++) s -= (k >= j) ? D[(base + k) * LD + base + i] * x[k] : 0.0;
-        const double dii = D[(base + i) * LD + base + i];
-        if (j == 0 && base + i < kw && (!(dii > 0.0) || !isfinite(dii)))
-          atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + base + i));
-        x[i] = (i >= j) ? s / dii : 0.0;
-      }
 #pragma unroll
       for (int i = 0; i < 8; i++) W[(base + j) * LD + base + i] = x[i];
     }
@@ -414,10 +417,8 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
   }
   double* Dinv = PB + pn.buf_off;
   const int ldD = pn.ldD;
-  for (int q = lane; q < ldD * kw4; q += 32) {
-    const int j = q / ldD, i = q - j * ldD;
-    Dinv[q] = (i < kw && j < kw && i >= j) ? W[j * LD + i] : 0.0;
-  }
+  for (int j = 0; j < kw4; j++)
+    for (int i = lane; i < ldD; i += 32) Dinv[j * ldD + i] = (i < kw && j < kw && i >= j) ? W[j * LD + i] : 0.0;
   if constexpr (WMODE) chunks_times_inverse<LD, NPAD>(PB, pn, W, 0, 1, lane);
 }
 
