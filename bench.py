@@ -15,7 +15,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import time
 
@@ -56,48 +55,68 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region: NVML polled from
+    a background thread every ~2 ms (the timed region can be tens of ms), plus one sample at entry
+    and one at exit.  Falls back to nvidia-smi if NVML is unavailable."""
 
     def __init__(self, index: int):
         self.index = index
-        self.proc = None
-        self.path = os.path.join("/tmp", f"clocks_{os.getpid()}.csv")
+        self.rows = []
+        self._stop = None
+        self._thr = None
+
+    def _sample(self):
+        import pynvml
+        sm = pynvml.nvmlDeviceGetClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        try:
+            rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        except Exception:
+            rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+        self.rows.append((sm, rs))
 
     def __enter__(self):
+        import threading
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
-                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
-                 "--format=csv,noheader,nounits", "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self._sample()
+            self._stop = threading.Event()
+
+            def loop():
+                while not self._stop.wait(0.002):
+                    try:
+                        self._sample()
+                    except Exception:
+                        break
+            self._thr = threading.Thread(target=loop, daemon=True)
+            self._thr.start()
         except Exception:
-            self.proc = None
+            self.h = None
         return self
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        if self._thr:
+            self._stop.set()
+            self._thr.join(timeout=2)
+        if getattr(self, "h", None) is not None:
             try:
-                self.proc.wait(timeout=5)
+                self._sample()
             except Exception:
-                self.proc.kill()
+                pass
 
     def summary(self):
-        try:
-            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
-        except Exception:
-            rows = []
-        if not rows:
+        if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in rows]
-        reasons = set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for r in rows:
-            for k, nm in enumerate(names):
-                if len(r) > 3 + k and "Active" in r[3 + k] and "Not" not in r[3 + k]:
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][1]), "reasons": sorted(reasons),
-                "samples": len(rows)}
+        import pynvml
+        names = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                 "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                 "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                 "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+        reasons = sorted({nm for _, rs in self.rows for nm, bit in names.items() if rs & bit})
+        return {"sm_mhz": float(np.median([r[0] for r in self.rows])), "sm_max_mhz": float(self.max_mhz),
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML, ~2 ms polling during the timed region"}
 
 
 def dist_setup(args):
