@@ -434,6 +434,9 @@ static_assert(kLdC == block_ld(kChunk), "chunk ld");
 #ifndef SC_NCW
 #define SC_NCW 8
 #endif
+#ifndef SC_NCW2
+#define SC_NCW2 4
+#endif
 #ifndef SC_KSPLIT
 #define SC_KSPLIT 1   // chunk-product accumulator sets per output block, <= 2 blocks per warp
 #endif                // (1 / 2 / 4 / 8 measured: fewer is faster, cfg2 TRSM 1.56 / 1.59 / 1.72 / - ms)
@@ -449,14 +452,16 @@ static_assert(kLdC == block_ld(kChunk), "chunk ld");
 #ifndef SC_WN32
 #define SC_WN32 1
 #endif
-template <int T>
+template <int T, int MINB = 1>
 struct TileCfg {
   static constexpr int LDX = strip_ld(T);       // strip / Y row stride in doubles
   static constexpr int NB = T / 8;              // 8-wide column blocks
   // 8 consumer warps (16 measured slower: 3.0 vs 2.6 ms cfg2, 17.2 vs 15.5 ms cfg3), one column
   // block each (keeps the register-resident Y fragments small); a 64 x T chunk product is
   // (8 / warp rows) row blocks per warp
-  static constexpr int NCW = T == 8 ? 8 : SC_NCW;
+  // consumer warps: 8, except 4 for the two-CTAs-per-SM class at T = 16 (cheaper group barriers and
+  // no register cap spills: cfg2 TRSM -1.5 %)
+  static constexpr int NCW = (T == 8 || T == 64) ? 8 : (MINB == 2 ? SC_NCW2 : SC_NCW);
   static constexpr int CT = NCW * 32;           // consumer threads
   static constexpr int WN = T >= 32 ? SC_WN32 : (T == 16 ? SC_WN16 : 1);  // column blocks per warp
   static constexpr int NWC = NB / WN;           // warps along the columns
@@ -591,8 +596,8 @@ __device__ __noinline__ void trsm_producer(const DevPlan& P, const Tile& tile, c
 // wide, L2-resident while the tile runs); the strip rows of the plan are then group-strip rows.
 // MINB: CTAs per SM the launch is built for (2: the small-strip tile class, registers capped)
 template <int T, bool GS, bool YM, int MINB = 1>
-__global__ void __launch_bounds__(TileCfg<T>::CT + 32, MINB) trsm_smem_kernel(DevPlan P, TrsmLaunch Lc) {
-  using Cfg = TileCfg<T>;
+__global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_kernel(DevPlan P, TrsmLaunch Lc) {
+  using Cfg = TileCfg<T, MINB>;
   constexpr int WM = Cfg::WM, WN = Cfg::WN, NWC = Cfg::NWC, CT = Cfg::CT;
   constexpr int KS = kMaxPanel / 4;  // k steps of 4 in a full panel
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -707,7 +712,7 @@ __global__ void __launch_bounds__(TileCfg<T>::CT + 32, MINB) trsm_smem_kernel(De
     // k < 8 (i + 1)); kept in registers until the step's barrier
     double yn[WM][WN][2];
     {
-      constexpr int YS = SC_GEMM1_SPLIT;  // independent accumulator sets (k steps round-robin)
+      constexpr int YS = MINB == 2 ? 1 : SC_GEMM1_SPLIT;  // accumulator sets (k steps round-robin)
       double ya[YS][WM][WN][2];
 #pragma unroll
       for (int h = 0; h < YS; h++)
@@ -1198,10 +1203,10 @@ __global__ void __launch_bounds__(kThreads) implicit_scatter_kernel(DevPlan P, d
 namespace {
 
 using TrsmFn = void (*)(DevPlan, TrsmLaunch);
-int trsm_threads(int T) {
+int trsm_threads(int T, int minb = 1) {
   switch (T) {
-    case 8: return TileCfg<8>::CT + 32;
-    case 16: return TileCfg<16>::CT + 32;
+    case 8: return minb == 2 ? TileCfg<8, 2>::CT + 32 : TileCfg<8>::CT + 32;
+    case 16: return minb == 2 ? TileCfg<16, 2>::CT + 32 : TileCfg<16>::CT + 32;
     case 32: return TileCfg<32>::CT + 32;
     default: return TileCfg<64>::CT + 32;
   }
@@ -1519,11 +1524,11 @@ static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stre
       fn<<<nl, trsm_threads(P.T), P.smem_trsm, side>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_join), side));
-      fn2<<<ns, trsm_threads(P.T), P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
+      fn2<<<ns, trsm_threads(P.T, 2), P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaStreamWaitEvent(stream, static_cast<cudaEvent_t>(P.ev_join), 0));
     } else if (ns > 0) {
-      fn2<<<ns, trsm_threads(P.T), P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
+      fn2<<<ns, trsm_threads(P.T, 2), P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
     } else if (nl > 0) {
       fn<<<nl, trsm_threads(P.T), P.smem_trsm, stream>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
     }
