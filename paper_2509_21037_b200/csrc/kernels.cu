@@ -461,7 +461,7 @@ struct TileCfg {
   // (8 / warp rows) row blocks per warp
   // consumer warps: 8, except 4 for the two-CTAs-per-SM class at T = 16 (cheaper group barriers and
   // no register cap spills: cfg2 TRSM -1.5 %)
-  static constexpr int NCW = (T == 8 || T == 64) ? 8 : (MINB == 2 ? SC_NCW2 : SC_NCW);
+  static constexpr int NCW = T == 64 ? 8 : (MINB == 2 ? SC_NCW2 : (T == 8 ? 8 : SC_NCW));
   static constexpr int CT = NCW * 32;           // consumer threads
   static constexpr int WN = T >= 32 ? SC_WN32 : (T == 16 ? SC_WN16 : 1);  // column blocks per warp
   static constexpr int NWC = NB / WN;           // warps along the columns
