@@ -254,7 +254,10 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0)
   }
   ScatterBatch<4> sb;
   sb.load(Lv, dest, pn.csc_begin + tid, pn.csc_end, kThreads);
-  zero_chunk_gaps(PB, pn, tid, kThreads);
+  // Y mode: every chunk position the scatter does not write (padding, explicit zeros of merged
+  // supernodes) is zero since the plan zero-filled the panel buffer and nothing else writes there;
+  // W mode overwrites whole chunks with W_p, so their zeros are restored here
+  if constexpr (WMODE) zero_chunk_gaps(PB, pn, tid, kThreads);
   __syncthreads();
   scatter_rest<kLdT>(sb, Lv, dest, PB, D, pn, tid, kThreads);
   // unit diagonal in the padding (its inverse stays the identity)
@@ -320,8 +323,10 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0)
   // write inv(L_pp): ldD x kw4 column-major, zero outside [0,kw) x [0,kw)
   double* Dinv = PB + pn.buf_off;
   const int ldD = pn.ldD;
-  for (int j = warp; j < kw4; j += kThreads / 32)  // warp per column, lanes over rows
-    for (int i = lane; i < ldD; i += 32) Dinv[j * ldD + i] = (i < kw && j < kw && i >= j) ? W[j * kLdT + i] : 0.0;
+  // only the lower triangle: the upper triangle and the padding columns stay zero from plan creation
+  // (the padding rows are never used)
+  for (int j = warp; j < kw; j += kThreads / 32)  // warp per column, lanes over rows
+    for (int i = j + lane; i < kw; i += 32) Dinv[j * ldD + i] = W[j * kLdT + i];
   // chunks: L[R_p, p] -> W_p = L[R_p, p] inv(L_pp) (the TRSM's update operand)
   if constexpr (WMODE) chunks_times_inverse<kLdT, kMaxPanel>(PB, pn, W, warp, kThreads / 32, lane);
 }
@@ -358,7 +363,7 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
   ScatterBatch<SC_PREP_U> sb;
   sb.load(Lv, dest, pn.csc_begin + lane, pn.csc_end, 32);
   for (int q = lane; q < NPAD * LD / 2; q += 32) reinterpret_cast<double2*>(D)[q] = make_double2(0.0, 0.0);
-  zero_chunk_gaps(PB, pn, lane, 32);
+  if constexpr (WMODE) zero_chunk_gaps(PB, pn, lane, 32);  // (Y mode: zero since plan creation)
   __syncwarp();
   scatter_rest<LD>(sb, Lv, dest, PB, D, pn, lane, 32);
   for (int i = kw + lane; i < NPAD; i += 32) D[i * LD + i] = 1.0;
@@ -417,8 +422,21 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
   }
   double* Dinv = PB + pn.buf_off;
   const int ldD = pn.ldD;
-  for (int j = 0; j < kw4; j++)
-    for (int i = lane; i < ldD; i += 32) Dinv[j * ldD + i] = (i < kw && j < kw && i >= j) ? W[j * LD + i] : 0.0;
+  // only the lower triangle (upper triangle and padding columns stay zero from plan creation): one
+  // flat pass over the kw (kw + 1) / 2 packed entries, column j from the packed index
+  for (int q = lane; q < kw * (kw + 1) / 2; q += 32) {
+    int j = (int)((2.0f * kw + 1.0f - sqrtf((2.0f * kw + 1.0f) * (2.0f * kw + 1.0f) - 8.0f * q)) * 0.5f);
+    int c0 = j * kw - j * (j - 1) / 2;  // packed start of column j
+    if (q < c0) {
+      j--;
+      c0 = j * kw - j * (j - 1) / 2;
+    } else if (q >= c0 + (kw - j)) {
+      c0 += kw - j;
+      j++;
+    }
+    const int i = j + (q - c0);
+    Dinv[j * ldD + i] = W[j * LD + i];
+  }
   if constexpr (WMODE) chunks_times_inverse<LD, NPAD>(PB, pn, W, 0, 1, lane);
 }
 
