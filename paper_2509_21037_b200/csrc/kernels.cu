@@ -1,23 +1,27 @@
 // kernels.cu — the device hot path (sm_100a, FP64).
 //
-//   prep_panel_kernel     one CTA per (subdomain, factor panel): scatters the panel's CSC values of
-//                         L into the panel buffer (dense diagonal block, pruned below-diagonal rows in
-//                         64-row chunks) and replaces the diagonal block by its inverse
-//                         (recursive doubling: 8x8 substitutions + DMMA products), so every tile's
-//                         diagonal solve becomes a tensor-core product.
-//   trsm_smem_kernel<T>   "X init + stepped supernodal TRSM" (SURVEY §8 rows a2+a3): one CTA per
-//                         (subdomain, RHS column tile of T columns).  The tile's X strip (the rows of
-//                         the panels of its reach only) lives in shared memory for the whole solve:
+//   prep_panel_kernel /   one CTA per (subdomain, panel wider than 32) / one warp per narrower panel
+//   prep_small_kernel     (NPAD = 8/16/32): scatters the panel's CSC values of L into the panel
+//                         buffer (dense diagonal block, pruned below-diagonal rows in 64-row chunks,
+//                         P:482-494) and replaces the diagonal block by its inverse (recursive
+//                         doubling: 8x8 substitutions + DMMA products), so every tile's diagonal solve
+//                         becomes a tensor-core product (W mode also forms W_p = L[R_p,p] inv(L_pp)).
+//   trsm_smem_kernel      "X init + stepped supernodal TRSM" (SURVEY §8 rows a2+a3): one CTA per
+//     <T, GS, YM, MINB>   (subdomain, RHS column tile of T columns).  X strip (rows of the panels of
+//                         the tile's reach) in shared memory, or in place in the group strip (GS);
 //                         zero + scatter of the permuted B~^T, then per panel
 //                         Y = inv(L_pp) X_p and X[R_p] -= L[R_p,p] Y as FP64 DMMA (mma.sync m8n8k4)
-//                         tiles.  A dedicated producer warp streams the L blocks with cp.async.bulk
-//                         (TMA bulk copies) into a byte ring guarded by full/empty mbarriers; the
-//                         eight consumer warps synchronise only per panel.  The strip is written out
-//                         once into the G-column group layout the SYRK reads.
+//                         tiles.  A producer warp streams the L blocks with cp.async.bulk (TMA bulk
+//                         copies) into a byte ring guarded by full/empty mbarriers and passes the step
+//                         geometry in per-slot records; consumer warps synchronise per column-block
+//                         group; solved rows go straight to the SYRK's group strip.  MINB = 2: the
+//                         small-strip tile class at two CTAs per SM.
 //   syrk_pair_kernel<G>   "block-sparse SYRK" (row a4): one CTA per G x G output tile (I >= J) of
 //                         F' = X^T X, k restricted to rows both group strips hold.
 //   apply_*               "explicit apply" (row a6): batched symmetric mat-vec on the lower F' with
 //                         the stepped-order gather of lambda and a deterministic scatter-sum.
+//   implicit_*            "implicit apply": forward + backward substitution per subdomain
+//                         with the staged factor panels, no F.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -1290,7 +1294,6 @@ sc_status upload_plan(Plan& P, std::string& err) {
   std::vector<Tile> tiles;
   std::vector<Step> steps;
   std::vector<uint16_t> srows;
-  std::vector<WSeg> wsegs;
   std::vector<Group> groups;
   std::vector<Reach> greach;
   std::vector<BInit> binit;
@@ -1304,7 +1307,6 @@ sc_status upload_plan(Plan& P, std::string& err) {
     tiles.insert(tiles.end(), C.tiles.begin(), C.tiles.end());
     steps.insert(steps.end(), C.steps.begin(), C.steps.end());
     srows.insert(srows.end(), C.srows.begin(), C.srows.end());
-    wsegs.insert(wsegs.end(), C.wsegs.begin(), C.wsegs.end());
     groups.insert(groups.end(), C.groups.begin(), C.groups.end());
     greach.insert(greach.end(), C.greach.begin(), C.greach.end());
     binit.insert(binit.end(), C.binit.begin(), C.binit.end());
@@ -1318,7 +1320,6 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, tiles, &D.tiles, err));
   TRY(upload(P, steps, &D.steps, err));
   TRY(upload(P, srows, &D.srows, err));
-  TRY(upload(P, wsegs, &D.wsegs, err));
   TRY(upload(P, groups, &D.groups, err));
   TRY(upload(P, greach, &D.greach, err));
   TRY(upload(P, binit, &D.binit, err));
@@ -1420,7 +1421,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   if (P.ntrsm_small > 0) CUDA_TRY(smem_attr((const void*)trsm_kernel_ptr2(P.T, P.wmode), P.smem_trsm_small));
   double total = 8.0 * (P.X_doubles + P.F_doubles + P.PB_doubles + P.part_doubles);
   total += dest.size() * 4.0 + Rrows.size() * 4.0 + panels.size() * sizeof(Panel) + tiles.size() * sizeof(Tile) +
-           steps.size() * sizeof(Step) + wsegs.size() * sizeof(WSeg) + groups.size() * sizeof(Group) +
+           steps.size() * sizeof(Step) + groups.size() * sizeof(Group) +
            greach.size() * sizeof(Reach) + binit.size() * sizeof(BInit) + pairs.size() * sizeof(Pair) +
            segs.size() * sizeof(Seg) + P.slm.size() * 8.0 + P.qg_sub_a.size() * 8.0 + P.qg_ptr.size() * 8.0;
   P.stats.device_bytes = total;

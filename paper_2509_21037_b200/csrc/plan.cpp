@@ -490,31 +490,6 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
           C.binit.push_back({strip_base[(size_t)p] + (e.first - C.panels[(size_t)p].a), a - t.col0, e.second});
         }
       t.binit_end = (int32_t)C.binit.size();
-      // write-out segments of a shared-memory strip into the group strip
-      t.wseg_begin = t.wseg_end = (int32_t)C.wsegs.size();
-      if (gstrip) continue;
-      size_t k = 0;
-      int32_t src = 0;
-      for (int32_t qg = G.reach_begin; qg < G.reach_end; qg++) {
-        const Reach& R = C.greach[(size_t)qg];
-        const int32_t kw = C.panels[(size_t)R.panel].kw;
-        int32_t sidx = -1;
-        if (k < tp.size() && tp[k] == R.panel) {
-          sidx = src;
-          src += kw;
-          k++;
-        }
-        if ((int32_t)C.wsegs.size() > t.wseg_begin) {
-          WSeg& last = C.wsegs.back();
-          const bool contig_dst = last.dst + last.len == R.off;
-          if (contig_dst && ((sidx < 0 && last.src < 0) || (sidx >= 0 && last.src >= 0 && last.src + last.len == sidx))) {
-            last.len += kw;
-            continue;
-          }
-        }
-        C.wsegs.push_back({sidx, R.off, kw, 0});
-      }
-      t.wseg_end = (int32_t)C.wsegs.size();
     }
     C.groups.push_back(G);
     J0 = J1;
@@ -843,7 +818,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   // --- global concatenation: class-local indices -> global
   int64_t srow_base = 0;
   int32_t tile_base = 0, step_base = 0, binit_base = 0, seg_base = 0, R_base = 0, pair_base = 0, panel_base = 0,
-          group_base = 0, greach_base = 0, wseg_base = 0;
+          group_base = 0, greach_base = 0;
   for (auto& C : P.classes) {
     P.cls_tile_begin.push_back(tile_base);
     P.cls_pair_begin.push_back(pair_base);
@@ -860,8 +835,6 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
       t.step_end += step_base;
       t.binit_begin += binit_base;
       t.binit_end += binit_base;
-      t.wseg_begin += wseg_base;
-      t.wseg_end += wseg_base;
       t.group += group_base;
     }
     for (auto& g : C.groups) {
@@ -883,7 +856,6 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     panel_base += (int32_t)C.panels.size();
     group_base += (int32_t)C.groups.size();
     greach_base += (int32_t)C.greach.size();
-    wseg_base += (int32_t)C.wsegs.size();
     srow_base += (int64_t)C.srows.size();
   }
 

@@ -80,7 +80,6 @@ struct Tile {
   int32_t col0, width, strip_rows, group;
   int32_t step_begin, step_end;    // panels visited (global indices into steps[])
   int32_t binit_begin, binit_end;  // B~^T scatter entries (global indices into binit[])
-  int32_t wseg_begin, wseg_end;    // write-out segments into the group strip (global, wsegs[])
   int32_t col_in_group, pad;
 };
 
@@ -94,11 +93,6 @@ struct Step {
   int64_t srow_off;
 };
 
-// Write-out of a tile strip into its group strip: rows [src, src+len) of the tile strip go to
-// rows [dst, dst+len) of the group strip; src < 0: the tile does not hold that panel (zeros).
-struct WSeg {
-  int32_t src, dst, len, pad;
-};
 
 // SYRK column group (width kGroup, a union of TRSM tiles): its X strip in global memory holds
 // the union of the member tiles' panels; reach entries (panel, off) in panel order.
@@ -154,7 +148,6 @@ struct ClassPlan {
   std::vector<Tile> tiles;         // *_begin/_end: class-local until build_plan globalises them
   std::vector<Step> steps;
   std::vector<uint16_t> srows;     // per step, per chunk: 64 strip rows of R_p (see Step)
-  std::vector<WSeg> wsegs;
   std::vector<Group> groups;
   std::vector<Reach> greach;
   std::vector<BInit> binit;
@@ -187,7 +180,6 @@ struct DevPlan {
   const Tile* tiles;
   const Step* steps;
   const uint16_t* srows;           // concatenated per class (Step.srow_off globalised)
-  const WSeg* wsegs;
   const Group* groups;
   const Reach* greach;
   const BInit* binit;
