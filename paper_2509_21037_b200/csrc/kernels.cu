@@ -924,7 +924,10 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
 // ------------------------------------------------------------------------------------------------
 // SYRK over G-column groups: F'[I,J] = sum_seg X_I[seg]^T X_J[seg] (lower part of F' only)
 // ------------------------------------------------------------------------------------------------
-constexpr int kKC = 32;       // k rows staged per chunk
+#ifndef SC_SYRK_KC
+#define SC_SYRK_KC 32
+#endif
+constexpr int kKC = SC_SYRK_KC;  // k rows staged per chunk
 
 template <int G>
 struct SyrkCfg {              // (G/8)^2 output blocks of 8x8 over 8 warps
