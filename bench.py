@@ -182,6 +182,9 @@ def main():
     ap.add_argument("--skip", default="exact", choices=["none", "envelope", "exact"])
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--panel", type=int, default=0)
+    ap.add_argument("--shard", action="store_true",
+                    help="strong scaling: the config's batch is LPT-partitioned over the ranks by the "
+                         "planner's per-subdomain cost (default: every rank assembles its own batch)")
     ap.add_argument("--strip", default="auto", choices=["auto", "shared", "global"],
                     help="where TRSM tiles keep their X strip (sc_options.x_strip)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
@@ -208,9 +211,22 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = load_peaks()
 
-    # each rank: its own cluster (replica of the config batch with its own coefficients)
+    # each rank: its own cluster (replica of the config batch with its own coefficients), or with
+    # --shard its LPT share of one batch (partition by plan cost, no collective)
     t_plan0 = time.perf_counter()
-    P = config_problem(args.config, seed=rank)
+    shard_info = None
+    if args.shard:
+        from paper_2509_21037_b200.shard import imbalance, lpt_partition
+        from synth.mesh import CONFIGS, make_problem
+        Pall = config_problem(args.config)
+        costs = SCPlan(Pall.subdomains, n_lambda=Pall.n_lambda, device=-1).subdomain_costs()
+        parts = lpt_partition(costs, world)
+        P = make_problem(name=args.config, subdomains=parts[rank], **CONFIGS[args.config])
+        shard_info = {"nsub_total": len(Pall.subdomains), "imbalance": imbalance(costs, parts),
+                      "partition": "LPT on executed-flop cost"}
+        del Pall
+    else:
+        P = config_problem(args.config, seed=rank)
     skip = {"none": 0, "envelope": 1, "exact": 2}[args.skip]
     plan = SCPlan(P.subdomains, n_lambda=P.n_lambda, skip=skip, tile_cols=args.tile, panel_cols=args.panel,
                   device=local, x_strip={"auto": 0, "shared": 1, "global": 2}[args.strip])
@@ -255,7 +271,14 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = t.item() / args.steps
-    value = world * nsub / (ms_step / 1e3)
+    nsub_job = shard_info["nsub_total"] if shard_info else world * nsub
+    # job-wide flops: summed over ranks (each rank's batch differs under --shard)
+    fl = torch.tensor([useful, st["flops_trsm_executed"] + st["flops_syrk_executed"]], dtype=torch.float64,
+                      device="cuda")
+    if world > 1:
+        dist.all_reduce(fl)
+    useful_job, executed_job = float(fl[0]), float(fl[1])
+    value = nsub_job / (ms_step / 1e3)
 
     # e2e through the public API with HOST inputs: pinned L values -> H2D inside the call ->
     # assemble -> one explicit apply q = F lambda (solution stage) -> D2H of q
@@ -287,7 +310,7 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         h2d = int(sum(8 * sd.L_values.size for sd in P.subdomains) + 8 * P.n_lambda)
-        e2e = {"value": world * nsub / (te.item() / 1e3), "unit": "subdomains/s", "ms_per_step": te.item(),
+        e2e = {"value": nsub_job / (te.item() / 1e3), "unit": "subdomains/s", "ms_per_step": te.item(),
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * P.n_lambda,
                "includes": "pinned H2D of all L values + assemble + 1 sc_apply (+all-reduce) + D2H of q"}
 
@@ -393,18 +416,20 @@ def main():
     clocks = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": "subdomains/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong" if shard_info else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CFG_DESC[args.config], "name": args.config, "subdomains_per_gpu": nsub,
                    "skip": args.skip, "tile_cols": st["tile_cols"], "panel_cols": st["panel_cols"],
                    "x_strip": {1: "shared", 2: "global"}.get(st["x_strip"], "?"),
                    "trsm_tasks_2cta": st["trsm_tasks_2cta"],
                    "parallelism": f"subdomain-sharded x{world} (no collective in assembly)",
+                   "shard": shard_info,
                    "l2": f"inputs larger than L2: L values {st['bytes_L_values'] / 1e9:.2f} GB, "
                          f"X {st['bytes_X'] / 1e9:.2f} GB, F {8 * sum(m * m for m in plan.m) / 1e9:.2f} GB per GPU"},
-        "gflops_useful": world * useful / (ms_step / 1e3) / 1e9,
-        "gflops_executed": world * (st["flops_trsm_executed"] + st["flops_syrk_executed"]) / (ms_step / 1e3) / 1e9,
-        "fp64_frac_useful": useful / (ms_step / 1e3) / 1e12 / peaks["fp64_tflops"],
+        "gflops_useful": useful_job / (ms_step / 1e3) / 1e9,
+        "gflops_executed": executed_job / (ms_step / 1e3) / 1e9,
+        "fp64_frac_useful": useful_job / world / (ms_step / 1e3) / 1e12 / peaks["fp64_tflops"],
         "phase_ms": {"prep": ms_prep, "trsm": ms_trsm, "syrk": ms_syrk},
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "amortization": amort,
         "gpu_launches": args.steps * plan.launches_per_assemble,
