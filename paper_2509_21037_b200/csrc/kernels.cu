@@ -1446,6 +1446,11 @@ void free_plan_device(Plan& P) {
   if (P.ev_fork) cudaEventDestroy(static_cast<cudaEvent_t>(P.ev_fork));
   if (P.ev_join) cudaEventDestroy(static_cast<cudaEvent_t>(P.ev_join));
   P.side_stream = P.ev_fork = P.ev_join = nullptr;
+  for (int i = 0; i < 2; i++)
+    if (P.ov_stream[i]) cudaStreamDestroy(static_cast<cudaStream_t>(P.ov_stream[i]));
+  P.ov_stream[0] = P.ov_stream[1] = nullptr;
+  for (void* e : P.ev_ov) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  P.ev_ov.clear();
   if (P.copy_stream) cudaStreamDestroy(static_cast<cudaStream_t>(P.copy_stream));
   if (P.ev_start) cudaEventDestroy(static_cast<cudaEvent_t>(P.ev_start));
   for (void* e : P.ev_chunk) cudaEventDestroy(static_cast<cudaEvent_t>(e));
@@ -1523,14 +1528,8 @@ static sc_status launch_prep_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
 
 // All phases (prep, TRSM, SYRK) for the subdomains [s0, s1) on `stream`; timing events only for the
 // whole batch.
-static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, bool timing, std::string& err) {
+static sc_status launch_trsm_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, std::string& err) {
   const bool all = s0 == 0 && s1 == P.nsub;
-  if (timing && P.tev[0]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[0], stream));
-  {
-    sc_status st = launch_prep_range(P, s0, s1, stream, err);
-    if (st != SC_OK) return st;
-  }
-  if (timing && P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
   {
     // tiles with small strips (2 CTAs per SM) and the rest (1 CTA per SM): two launches, the large
     // ones on a side stream so both classes share the SMs and neither launch's tail idles them
@@ -1556,7 +1555,11 @@ static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stre
     }
     CUDA_TRY(cudaGetLastError());
   }
-  if (timing && P.tev[2]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[2], stream));
+  return SC_OK;
+}
+
+static sc_status launch_syrk_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, std::string& err) {
+  const bool all = s0 == 0 && s1 == P.nsub;
   {
     const int nsy = (int)P.syrk_tasks.size();
     const int a = all ? 0 : task_lb(P.syrk_tasks, 0, nsy, s0), b = all ? nsy : task_lb(P.syrk_tasks, 0, nsy, s1);
@@ -1569,7 +1572,62 @@ static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stre
       CUDA_TRY(cudaGetLastError());
     }
   }
+  return SC_OK;
+}
+
+// All phases (prep, TRSM, SYRK) for the subdomains [s0, s1) on `stream`; timing events only for the
+// whole batch.
+static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, bool timing, std::string& err) {
+  if (timing && P.tev[0]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[0], stream));
+  sc_status st = launch_prep_range(P, s0, s1, stream, err);
+  if (st != SC_OK) return st;
+  if (timing && P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
+  st = launch_trsm_range(P, s0, s1, stream, err);
+  if (st != SC_OK) return st;
+  if (timing && P.tev[2]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[2], stream));
+  st = launch_syrk_range(P, s0, s1, stream, err);
+  if (st != SC_OK) return st;
   if (timing && P.tev[3]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[3], stream));
+  return SC_OK;
+}
+
+// Phase-overlapped batch (P.overlap chunks of subdomains): prep of chunk k+1 (on `stream`), TRSM of
+// chunk k and SYRK of chunk k-1 (two plan-owned streams) run concurrently, ordered per chunk by events.
+static sc_status launch_overlapped(Plan& P, cudaStream_t stream, std::string& err) {
+  const int K = P.overlap;
+  if (!P.ov_stream[0]) {
+    for (int i = 0; i < 2; i++)
+      CUDA_TRY(cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&P.ov_stream[i]), cudaStreamNonBlocking));
+  }
+  while ((int)P.ev_ov.size() < 2 * K + 2) {
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    P.ev_ov.push_back(e);
+  }
+  cudaStream_t ts = static_cast<cudaStream_t>(P.ov_stream[0]), ss = static_cast<cudaStream_t>(P.ov_stream[1]);
+  auto ev = [&](int i) { return static_cast<cudaEvent_t>(P.ev_ov[(size_t)i]); };
+  if (P.tev[0]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[0], stream));
+  CUDA_TRY(cudaEventRecord(ev(0), stream));
+  CUDA_TRY(cudaStreamWaitEvent(ts, ev(0), 0));
+  CUDA_TRY(cudaStreamWaitEvent(ss, ev(0), 0));
+  for (int k = 0; k < K; k++) {
+    const int32_t s0 = (int32_t)((int64_t)P.nsub * k / K), s1 = (int32_t)((int64_t)P.nsub * (k + 1) / K);
+    sc_status st = launch_prep_range(P, s0, s1, stream, err);
+    if (st != SC_OK) return st;
+    CUDA_TRY(cudaEventRecord(ev(2 + 2 * k), stream));
+    CUDA_TRY(cudaStreamWaitEvent(ts, ev(2 + 2 * k), 0));
+    st = launch_trsm_range(P, s0, s1, ts, err);
+    if (st != SC_OK) return st;
+    CUDA_TRY(cudaEventRecord(ev(3 + 2 * k), ts));
+    CUDA_TRY(cudaStreamWaitEvent(ss, ev(3 + 2 * k), 0));
+    st = launch_syrk_range(P, s0, s1, ss, err);
+    if (st != SC_OK) return st;
+  }
+  if (P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));  // all prep issued/done on stream
+  if (P.tev[2]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[2], ts));
+  CUDA_TRY(cudaEventRecord(ev(1), ss));
+  CUDA_TRY(cudaStreamWaitEvent(stream, ev(1), 0));
+  if (P.tev[3]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[3], stream));
   return SC_OK;
 }
 
@@ -1580,6 +1638,7 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
   P.factor_ready = true;
+  if (P.overlap > 1 && P.nsub >= 2 * P.overlap) return launch_overlapped(P, stream, err);
   return launch_range(P, 0, P.nsub, stream, true, err);
 }
 

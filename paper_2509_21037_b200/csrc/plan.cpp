@@ -654,6 +654,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   // per subdomain in prep: no intra-step barrier, but the prep transform costs more than the
   // barrier saves: cfg2-5 measured equal or slower in total, e.g. cfg4 3649 vs 3730 subdomains/s)
   P.wmode = false;
+  if (const char* e = std::getenv("SC_OVERLAP")) P.overlap = std::atoi(e);
   if (const char* e = std::getenv("SC_TRSM_MODE")) P.wmode = e[0] == 'W';
   if (const char* e = std::getenv("SC_GROUP")) G0 = std::atoi(e);
   if (!(G0 == 16 || G0 == 32 || G0 == 64)) FAIL(SC_ERR_INVALID_ARG, "SC_GROUP must be 16, 32 or 64");

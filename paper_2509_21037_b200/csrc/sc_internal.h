@@ -260,6 +260,9 @@ struct Plan {
   void* side_stream = nullptr;   // cudaStream_t for the large-strip launch
   void* ev_fork = nullptr;       // cudaEvent_t
   void* ev_join = nullptr;
+  int32_t overlap = 0;           // >1: phase-overlapped assembly over this many subdomain chunks
+  void* ov_stream[2] = {nullptr, nullptr};
+  std::vector<void*> ev_ov;
   void* copy_stream = nullptr;   // host-fed pipeline (sc_assemble_batch_host): H2D copies
   void* ev_start = nullptr;
   std::vector<void*> ev_chunk;
