@@ -1067,10 +1067,13 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
 // a row's tiles, in a fixed order (deterministic, no atomics).
 __device__ __forceinline__ int64_t apply_tile_index(int rb, int cb) { return (int64_t)rb * (rb + 1) / 2 + cb; }
 
+// Warp w holds columns 8w..8w+7 of the tile, lane l rows l and l + 32, straight from HBM into
+// registers (each load instruction reads 32 consecutive doubles of one column): column sums by warp
+// shuffles, row sums over the 8 warps through a 4 KB shared reduction.
 __global__ void __launch_bounds__(kThreads) apply_tile_kernel(DevPlan P, const double* __restrict__ lambda) {
   constexpr int AT = kApplyTile;
-  __shared__ double Ft[AT][AT + 1];
-  __shared__ double xr[AT], xc[AT];
+  static_assert(AT == 64 && kThreads == 256, "apply tile mapping");
+  __shared__ double red[kThreads / 32][AT];
   const ApplyTask task = P.apply_tasks[blockIdx.x];
   const int sub = task.sub, rb = task.rb, cb = task.cb;
   const int m = P.sub_m[sub];
@@ -1078,27 +1081,42 @@ __global__ void __launch_bounds__(kThreads) apply_tile_kernel(DevPlan P, const d
   const int nr = min(AT, m - r0), nc = min(AT, m - c0);
   const double* __restrict__ F = P.F + P.sub_F_base[sub];
   const int64_t* __restrict__ slm = P.slm + P.sub_slm_off[sub];
-  const int tid = threadIdx.x;
-  if (tid < AT) xr[tid] = (tid < nr) ? lambda[slm[r0 + tid]] : 0.0;
-  else if (tid < 2 * AT) xc[tid - AT] = (tid - AT < nc) ? lambda[slm[c0 + tid - AT]] : 0.0;
-  for (int q = tid; q < AT * AT; q += kThreads) {
-    const int c = q / AT, r = q - c * AT;
-    Ft[r][c] = (r < nr && c < nc) ? F[(int64_t)(c0 + c) * m + (r0 + r)] : 0.0;
-  }
-  __syncthreads();
-  double* part = P.part + P.sub_part_off[sub] + apply_tile_index(rb, cb) * 2 * AT;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool diag = (rb == cb);
+  const int rA = lane, rB = lane + 32;
+  const double xA = (rA < nr) ? __ldg(lambda + slm[r0 + rA]) : 0.0;
+  const double xB = (rB < nr) ? __ldg(lambda + slm[r0 + rB]) : 0.0;
+  double fa[8], fb[8], xc[8];
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const int c = warp * 8 + k;
+    const double* col = F + (int64_t)(c0 + c) * m + r0;
+    const bool cv = c < nc;
+    fa[k] = (cv && rA < nr) ? __ldg(col + rA) : 0.0;
+    fb[k] = (cv && rB < nr) ? __ldg(col + rB) : 0.0;
+    xc[k] = cv ? __ldg(lambda + slm[c0 + c]) : 0.0;
+  }
+  double* part = P.part + P.sub_part_off[sub] + apply_tile_index(rb, cb) * 2 * AT;
+  double uA = 0.0, uB = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; k++) {
+    const int c = warp * 8 + k;
+    uA = fma(fa[k], xc[k], uA);
+    uB = fma(fb[k], xc[k], uB);
+    // column sum v_c = sum_r F[r][c] x_r (strictly lower part on a diagonal tile)
+    double v = ((diag && rA <= c) ? 0.0 : fa[k] * xA) + ((diag && rB <= c) ? 0.0 : fb[k] * xB);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) part[AT + c] = v;
+  }
+  red[warp][rA] = uA;
+  red[warp][rB] = uB;
+  __syncthreads();
   if (tid < AT) {
     double u = 0.0;
-#pragma unroll 8
-    for (int c = 0; c < AT; c++) u = fma(Ft[tid][c], xc[c], u);
+#pragma unroll
+    for (int w = 0; w < kThreads / 32; w++) u += red[w][tid];
     part[tid] = u;
-  } else if (tid < 2 * AT) {
-    const int c = tid - AT;
-    double v = 0.0;
-#pragma unroll 8
-    for (int r = 0; r < AT; r++) v = (diag && r <= c) ? v : fma(Ft[r][c], xr[r], v);
-    part[AT + c] = v;
   }
 }
 
