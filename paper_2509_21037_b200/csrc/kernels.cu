@@ -1070,11 +1070,20 @@ __device__ __forceinline__ int64_t apply_tile_index(int rb, int cb) { return (in
 // Warp w holds columns 8w..8w+7 of the tile, lane l rows l and l + 32, straight from HBM into
 // registers (each load instruction reads 32 consecutive doubles of one column): column sums by warp
 // shuffles, row sums over the 8 warps through a 4 KB shared reduction.
-__global__ void __launch_bounds__(kThreads) apply_tile_kernel(DevPlan P, const double* __restrict__ lambda) {
+#ifndef SC_APPLY_TPC
+#define SC_APPLY_TPC 4
+#endif
+constexpr int kApplyTPC = SC_APPLY_TPC;  // tiles per CTA
+
+__global__ void __launch_bounds__(kThreads) apply_tile_kernel(DevPlan P, const double* __restrict__ lambda, int ntask) {
   constexpr int AT = kApplyTile;
   static_assert(AT == 64 && kThreads == 256, "apply tile mapping");
   __shared__ double red[kThreads / 32][AT];
-  const ApplyTask task = P.apply_tasks[blockIdx.x];
+  for (int it = 0; it < kApplyTPC; it++) {
+  const int ti = blockIdx.x * kApplyTPC + it;
+  if (ti >= ntask) return;
+  if (it > 0) __syncthreads();  // red reused
+  const ApplyTask task = P.apply_tasks[ti];
   const int sub = task.sub, rb = task.rb, cb = task.cb;
   const int m = P.sub_m[sub];
   const int r0 = rb * AT, c0 = cb * AT;
@@ -1117,6 +1126,7 @@ __global__ void __launch_bounds__(kThreads) apply_tile_kernel(DevPlan P, const d
 #pragma unroll
     for (int w = 0; w < kThreads / 32; w++) u += red[w][tid];
     part[tid] = u;
+  }
   }
 }
 
@@ -1732,7 +1742,7 @@ sc_status launch_apply(Plan& P, const double* lambda, double* q, void* stream_v,
   P.last_stream = stream_v;
   const int na = (int)P.apply_tasks.size();
   if (na > 0) {
-    apply_tile_kernel<<<na, kThreads, 0, stream>>>(P.dev, lambda);
+    apply_tile_kernel<<<(na + kApplyTPC - 1) / kApplyTPC, kThreads, 0, stream>>>(P.dev, lambda, na);
     CUDA_TRY(cudaGetLastError());
   }
   if (P.n_lambda > 0) {
