@@ -357,6 +357,13 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
   std::vector<int32_t> inreach((size_t)np, -1), stamp((size_t)n, -1), strip_base((size_t)np, -1),
       in_tile((size_t)np, -1);
   std::vector<std::vector<int32_t>> tile_panels((size_t)ntiles);
+  // exact mode: row-level reach of each SYRK group (the rows its columns' etree paths pass through);
+  // the SYRK's k ranges skip the rows of a common panel that are structurally zero for one side
+  // (e.g. the rows of a supernode above the column's entry point)
+  const int32_t ngroups_r = (m + kGroup - 1) / kGroup;
+  const bool row_reach = skip == SC_SKIP_EXACT && !std::getenv("SC_SYRK_PANEL_REACH");
+  std::vector<std::vector<char>> grow_reach(row_reach ? (size_t)ngroups_r : 0);
+  for (auto& v : grow_reach) v.assign((size_t)n, 0);
   for (int32_t J = 0; J < ntiles; J++) {
     Tile t{};
     t.col0 = J * T;
@@ -372,6 +379,7 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
           for (int32_t c = e.first; c >= 0 && stamp[(size_t)c] != J; c = parent[(size_t)c]) {
             stamp[(size_t)c] = J;
             inreach[(size_t)panel_of_col[(size_t)c]] = J;
+            if (row_reach) grow_reach[(size_t)t.group][(size_t)c] = 1;
           }
       for (int32_t p = 0; p < np; p++)
         if (inreach[(size_t)p] == J) tp.push_back(p);
@@ -571,18 +579,26 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
           qj++;
           continue;
         }
-        const int32_t len = C.panels[(size_t)a.panel].kw;
-        K += len;
-        if ((int32_t)C.segs.size() > pr.seg_begin) {
-          Seg& last = C.segs.back();
-          if (last.offI + last.len == a.off && last.offJ + last.len == b.off) {
-            last.len += len;
-            qi++;
-            qj++;
+        const Panel& Pp = C.panels[(size_t)a.panel];
+        // runs of rows reached by both groups (whole panel without row-level reach)
+        for (int32_t r = 0; r < Pp.kw;) {
+          if (row_reach && !(grow_reach[(size_t)I][(size_t)(Pp.a + r)] && grow_reach[(size_t)J][(size_t)(Pp.a + r)])) {
+            r++;
             continue;
           }
+          int32_t e = r + 1;
+          while (e < Pp.kw && (!row_reach || (grow_reach[(size_t)I][(size_t)(Pp.a + e)] &&
+                                              grow_reach[(size_t)J][(size_t)(Pp.a + e)])))
+            e++;
+          const int32_t len = e - r, oi = a.off + r, oj = b.off + r;
+          K += len;
+          Seg* last = (int32_t)C.segs.size() > pr.seg_begin ? &C.segs.back() : nullptr;
+          if (last && last->offI + last->len == oi && last->offJ + last->len == oj)
+            last->len += len;
+          else
+            C.segs.push_back({oi, oj, len, 0});
+          r = e;
         }
-        C.segs.push_back({a.off, b.off, len, 0});
         qi++;
         qj++;
       }
