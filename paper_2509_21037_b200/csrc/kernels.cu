@@ -1276,6 +1276,11 @@ TrsmFn trsm_kernel_ptr_m(int T, bool gs) {
 TrsmFn trsm_kernel_ptr(int T, bool gs, bool wmode) {
   return wmode ? trsm_kernel_ptr_m<false>(T, gs) : trsm_kernel_ptr_m<true>(T, gs);
 }
+// global strips at two CTAs per SM (T = 16, plan option gs2)
+TrsmFn trsm_kernel_ptr_gs2(bool wmode) {
+  return wmode ? trsm_smem_kernel<16, true, false, 2> : trsm_smem_kernel<16, true, true, 2>;
+}
+
 // small-strip class (shared strips, T <= 16 only), two CTAs per SM
 TrsmFn trsm_kernel_ptr2(int T, bool wmode) {
   switch (T) {
@@ -1448,7 +1453,8 @@ sc_status upload_plan(Plan& P, std::string& err) {
   CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<16>, syrk_smem_bytes<16>()));
   CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<32>, syrk_smem_bytes<32>()));
   CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<64>, syrk_smem_bytes<64>()));
-  CUDA_TRY(smem_attr((const void*)trsm_kernel_ptr(P.T, P.gstrip, P.wmode), P.smem_trsm));
+  CUDA_TRY(smem_attr((const void*)(P.gs2 ? trsm_kernel_ptr_gs2(P.wmode) : trsm_kernel_ptr(P.T, P.gstrip, P.wmode)),
+                     P.smem_trsm));
   if (P.ntrsm_small > 0) CUDA_TRY(smem_attr((const void*)trsm_kernel_ptr2(P.T, P.wmode), P.smem_trsm_small));
   double total = 8.0 * (P.X_doubles + P.F_doubles + P.PB_doubles + P.part_doubles);
   total += dest.size() * 4.0 + Rrows.size() * 4.0 + panels.size() * sizeof(Panel) + tiles.size() * sizeof(Tile) +
@@ -1562,7 +1568,9 @@ static sc_status launch_trsm_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
     // tiles with small strips (2 CTAs per SM) and the rest (1 CTA per SM): two launches, the large
     // ones on a side stream so both classes share the SMs and neither launch's tail idles them
     const int ntr = (int)P.trsm_tasks.size(), nsm = P.ntrsm_small;
-    const TrsmFn fn = trsm_kernel_ptr(P.T, P.gstrip, P.wmode), fn2 = trsm_kernel_ptr2(P.T, P.wmode);
+    const TrsmFn fn = P.gs2 ? trsm_kernel_ptr_gs2(P.wmode) : trsm_kernel_ptr(P.T, P.gstrip, P.wmode),
+                 fn2 = trsm_kernel_ptr2(P.T, P.wmode);
+    const int thr = P.gs2 ? trsm_threads(16, 2) : trsm_threads(P.T);
     const int sa = all ? 0 : task_lb(P.trsm_tasks, 0, nsm, s0), sb = all ? nsm : task_lb(P.trsm_tasks, 0, nsm, s1);
     const int la = all ? nsm : task_lb(P.trsm_tasks, nsm, ntr, s0), lb = all ? ntr : task_lb(P.trsm_tasks, nsm, ntr, s1);
     const int ns = sb - sa, nl = lb - la;
@@ -1570,7 +1578,7 @@ static sc_status launch_trsm_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
       cudaStream_t side = static_cast<cudaStream_t>(P.side_stream);
       CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_fork), stream));
       CUDA_TRY(cudaStreamWaitEvent(side, static_cast<cudaEvent_t>(P.ev_fork), 0));
-      fn<<<nl, trsm_threads(P.T), P.smem_trsm, side>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
+      fn<<<nl, thr, P.smem_trsm, side>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
       CUDA_TRY(cudaGetLastError());
       CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_join), side));
       fn2<<<ns, trsm_threads(P.T, 2), P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
@@ -1579,7 +1587,7 @@ static sc_status launch_trsm_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
     } else if (ns > 0) {
       fn2<<<ns, trsm_threads(P.T, 2), P.smem_trsm_small, stream>>>(P.dev, TrsmLaunch{sa, P.ring_small, P.strip_small, 0});
     } else if (nl > 0) {
-      fn<<<nl, trsm_threads(P.T), P.smem_trsm, stream>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
+      fn<<<nl, thr, P.smem_trsm, stream>>>(P.dev, TrsmLaunch{la, P.ring_bytes, P.max_strip_rows, 0});
     }
     CUDA_TRY(cudaGetLastError());
   }

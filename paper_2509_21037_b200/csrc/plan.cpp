@@ -803,6 +803,12 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   }
   for (auto& C : P.classes) P.max_strip_rows = std::max(P.max_strip_rows, C.max_strip_rows);
   P.ring_bytes = (int32_t)std::max<int64_t>(ring_for(P.T), 0);
+  if (P.gstrip && P.T == 16 && std::getenv("SC_GS2")) {  // two CTAs per SM: ring within half an SM
+    P.gs2 = true;
+    const int64_t half = kSmemPerSM / 2 - 1024;
+    const int64_t fixed = (int64_t)trsm_smem_layout(16, 0, 0, true, !P.wmode).total;
+    P.ring_bytes = (int32_t)(std::min<int64_t>(P.ring_bytes, half - fixed) & ~(int64_t)127);
+  }
   // small-strip tile class (shared strips): tiles whose strip fits next to a ring of >= 2 of the
   // largest L blocks (and >= 32 KB) within half of the SM's shared memory run two CTAs per SM
   // (T <= 16 only: the register cap of two 288-thread CTAs per SM makes wider tiles spill)
