@@ -776,9 +776,16 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     const int* cand = opt.tile_cols ? &opt.tile_cols : cand_auto;
     const int ncand = opt.tile_cols ? 1 : (opt.x_strip == SC_STRIP_SHARED ? 3 : 2);
     bool fits = false;
+    // large operators (3D): global strips at T = 16, two CTAs per SM (see gs2 below)
+    if (!opt.tile_cols && max_m > 512 && opt.x_strip == SC_STRIP_AUTO) {
+      sc_status st = analyse_all(16, true, -1);
+      if (st != SC_OK) return st;
+      fits = true;
+      P.gstrip = true;
+    }
     // small operators (2D): T = 16 at two CTAs per SM beats T = 32 at one when most tiles' strips
     // fit in half an SM (cfg2 TRSM 1.72 vs 2.01 ms)
-    if (!opt.tile_cols && max_m <= 512) {
+    if (!fits && !opt.tile_cols && max_m <= 512) {
       sc_status st = analyse_all(16, false, strip_limit_for(16));
       if (st != SC_OK) return st;
       if (!too_big() && ring_for(16) > 0) {
@@ -803,7 +810,10 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   }
   for (auto& C : P.classes) P.max_strip_rows = std::max(P.max_strip_rows, C.max_strip_rows);
   P.ring_bytes = (int32_t)std::max<int64_t>(ring_for(P.T), 0);
-  if (P.gstrip && P.T == 16 && std::getenv("SC_GS2")) {  // two CTAs per SM: ring within half an SM
+  // global strips at T = 16 run two CTAs per SM (4 consumer warps each; measured: cfg3 TRSM 12.6 vs
+  // 13.7 ms with shared strips, cfg4 51.8 vs 54.5 ms at T = 32, cfg5 324 vs 339 ms); SC_GS2=0 disables
+  const char* gs2_env = std::getenv("SC_GS2");
+  if (P.gstrip && P.T == 16 && !(gs2_env && gs2_env[0] == '0')) {  // ring within half an SM
     P.gs2 = true;
     const int64_t half = kSmemPerSM / 2 - 1024;
     const int64_t fixed = (int64_t)trsm_smem_layout(16, 0, 0, true, !P.wmode).total;

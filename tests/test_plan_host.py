@@ -232,12 +232,12 @@ def test_empty_subdomain_and_empty_columns():
 
 def test_auto_tile_and_strip_selection_defaults():
     """The planner's measured defaults: 2D cfg2 -> T=16 shared strips, all tiles in the
-    two-CTAs-per-SM class, 32-wide panels; 3D heat cfg3 -> T=16 shared strips, one CTA per SM;
-    3D elasticity cfg4 -> T=32 global strips (only an 8-column shared strip would fit)."""
+    two-CTAs-per-SM class, 32-wide panels; 3D (cfg3, cfg4) -> T=16 global strips at two CTAs per SM,
+    64-wide panels."""
     from synth import make_problem
     cases = [(dict(dim=2, physics="heat", S=32, E=64), 16, scmod.STRIP_SHARED, "all", 32),
-             (dict(dim=3, physics="heat", S=8, E=16), 16, scmod.STRIP_SHARED, "none", 64),
-             (dict(dim=3, physics="elasticity", S=8, E=12), 32, scmod.STRIP_GLOBAL, "none", 64)]
+             (dict(dim=3, physics="heat", S=8, E=16), 16, scmod.STRIP_GLOBAL, "none", 64),
+             (dict(dim=3, physics="elasticity", S=8, E=12), 16, scmod.STRIP_GLOBAL, "none", 64)]
     for spec, T, strip, two_cta, pw in cases:
         P = make_problem(subdomains=[0, 5, spec["S"] ** spec["dim"] // 2], **spec)
         st = SCPlan(P.subdomains, n_lambda=P.n_lambda, device=-1).stats()
