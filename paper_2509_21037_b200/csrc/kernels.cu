@@ -483,7 +483,7 @@ struct TileCfg {
   // (8 / warp rows) row blocks per warp
   // consumer warps: 8, except 4 for the two-CTAs-per-SM class at T = 16 (cheaper group barriers and
   // no register cap spills: cfg2 TRSM -1.5 %)
-  static constexpr int NCW = T == 64 ? 8 : (MINB == 2 ? SC_NCW2 : (T == 8 ? 8 : SC_NCW));
+  static constexpr int NCW = T == 64 ? 8 : (MINB >= 2 ? SC_NCW2 : (T == 8 ? 8 : SC_NCW));
   static constexpr int CT = NCW * 32;           // consumer threads
   static constexpr int WN = T >= 32 ? SC_WN32 : (T == 16 ? SC_WN16 : 1);  // column blocks per warp
   static constexpr int NWC = NB / WN;           // warps along the columns
@@ -1277,7 +1277,8 @@ TrsmFn trsm_kernel_ptr(int T, bool gs, bool wmode) {
   return wmode ? trsm_kernel_ptr_m<false>(T, gs) : trsm_kernel_ptr_m<true>(T, gs);
 }
 // global strips at two CTAs per SM (T = 16, plan option gs2)
-TrsmFn trsm_kernel_ptr_gs2(bool wmode) {
+TrsmFn trsm_kernel_ptr_gs2(bool wmode, int ctas = 2) {
+  if (ctas == 3) return wmode ? trsm_smem_kernel<16, true, false, 3> : trsm_smem_kernel<16, true, true, 3>;
   return wmode ? trsm_smem_kernel<16, true, false, 2> : trsm_smem_kernel<16, true, true, 2>;
 }
 
@@ -1453,7 +1454,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<16>, syrk_smem_bytes<16>()));
   CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<32>, syrk_smem_bytes<32>()));
   CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<64>, syrk_smem_bytes<64>()));
-  CUDA_TRY(smem_attr((const void*)(P.gs2 ? trsm_kernel_ptr_gs2(P.wmode) : trsm_kernel_ptr(P.T, P.gstrip, P.wmode)),
+  CUDA_TRY(smem_attr((const void*)(P.gs2 ? trsm_kernel_ptr_gs2(P.wmode, P.gs2) : trsm_kernel_ptr(P.T, P.gstrip, P.wmode)),
                      P.smem_trsm));
   if (P.ntrsm_small > 0) CUDA_TRY(smem_attr((const void*)trsm_kernel_ptr2(P.T, P.wmode), P.smem_trsm_small));
   double total = 8.0 * (P.X_doubles + P.F_doubles + P.PB_doubles + P.part_doubles);
@@ -1568,7 +1569,7 @@ static sc_status launch_trsm_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
     // tiles with small strips (2 CTAs per SM) and the rest (1 CTA per SM): two launches, the large
     // ones on a side stream so both classes share the SMs and neither launch's tail idles them
     const int ntr = (int)P.trsm_tasks.size(), nsm = P.ntrsm_small;
-    const TrsmFn fn = P.gs2 ? trsm_kernel_ptr_gs2(P.wmode) : trsm_kernel_ptr(P.T, P.gstrip, P.wmode),
+    const TrsmFn fn = P.gs2 ? trsm_kernel_ptr_gs2(P.wmode, P.gs2) : trsm_kernel_ptr(P.T, P.gstrip, P.wmode),
                  fn2 = trsm_kernel_ptr2(P.T, P.wmode);
     const int thr = P.gs2 ? trsm_threads(16, 2) : trsm_threads(P.T);
     const int sa = all ? 0 : task_lb(P.trsm_tasks, 0, nsm, s0), sb = all ? nsm : task_lb(P.trsm_tasks, 0, nsm, s1);

@@ -813,11 +813,11 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   // global strips at T = 16 run two CTAs per SM (4 consumer warps each; measured: cfg3 TRSM 12.6 vs
   // 13.7 ms with shared strips, cfg4 51.8 vs 54.5 ms at T = 32, cfg5 324 vs 339 ms); SC_GS2=0 disables
   const char* gs2_env = std::getenv("SC_GS2");
-  if (P.gstrip && P.T == 16 && !(gs2_env && gs2_env[0] == '0')) {  // ring within half an SM
-    P.gs2 = true;
-    const int64_t half = kSmemPerSM / 2 - 1024;
+  if (P.gstrip && P.T == 16 && !(gs2_env && gs2_env[0] == '0')) {  // ring within 1/ctas of an SM
+    P.gs2 = (gs2_env && gs2_env[0] == '3') ? 3 : 2;
+    const int64_t share = kSmemPerSM / P.gs2 - 1024;
     const int64_t fixed = (int64_t)trsm_smem_layout(16, 0, 0, true, !P.wmode).total;
-    P.ring_bytes = (int32_t)(std::min<int64_t>(P.ring_bytes, half - fixed) & ~(int64_t)127);
+    P.ring_bytes = (int32_t)(std::min<int64_t>(P.ring_bytes, share - fixed) & ~(int64_t)127);
   }
   // small-strip tile class (shared strips): tiles whose strip fits next to a ring of >= 2 of the
   // largest L blocks (and >= 32 KB) within half of the SM's shared memory run two CTAs per SM

@@ -223,7 +223,7 @@ struct Plan {
   sc_options opt{};
   int32_t T = 32, G = 64, PW = 64, ring_bytes = 0;
   bool gstrip = false;             // X strips solved in place in the group strips (global memory)
-  bool gs2 = false;                // global strips at T = 16, two CTAs per SM (experimental, SC_GS2)
+  int32_t gs2 = 0;                 // global strips at T = 16 with this many CTAs per SM (2; 3 via SC_GS2=3)
   bool factor_ready = false;       // panel buffers hold the factor of the last prepare / assemble
   bool wmode = true;               // TRSM update operand W_p = L[R_p,p] inv(L_pp) (wide panels) or L (Y mode)
   int32_t nsub = 0;
