@@ -86,6 +86,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       : "memory");
 }
 
+// Sticky zero-pivot flags (reset at the start of every assemble / prepare): err[0] = the first
+// failing (subdomain + 1, column) of the batch, err[1 + sub] = 1 + the first failing column of `sub`.
+__device__ __forceinline__ void flag_zero_pivot(const DevPlan& P, int sub, int col) {
+  atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)col);
+  atomicCAS(P.err + 1 + sub, 0ull, (unsigned long long)col + 1ull);
+}
+
 // ------------------------------------------------------------------------------------------------
 // prep: panel buffer = [inv(L_pp) | L[R_p, p] chunks]
 // ------------------------------------------------------------------------------------------------
@@ -276,8 +283,7 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0)
     const int base = warp * 8, j = lane;
     // one division per lane: lane j holds 1 / d_jj, broadcast by shuffles
     const double djj = D[(base + j) * kLdT + base + j];
-    if (base + j < kw && (!(djj > 0.0) || !isfinite(djj)))
-      atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + base + j));
+    if (base + j < kw && (!(djj > 0.0) || !isfinite(djj))) flag_zero_pivot(P, sub, pn.a + base + j);
     const double rj = 1.0 / djj;
     double x[8];
 #pragma unroll
@@ -377,8 +383,7 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
     const int base = (lane >> 3) * 8, j = lane & 7;
     const int rb = base < NPAD ? base : 0;
     const double djj = D[(rb + j) * LD + rb + j];
-    if (base < NPAD && base + j < kw && (!(djj > 0.0) || !isfinite(djj)))
-      atomicCAS(P.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + base + j));
+    if (base < NPAD && base + j < kw && (!(djj > 0.0) || !isfinite(djj))) flag_zero_pivot(P, sub, pn.a + base + j);
     const double rj = 1.0 / djj;  // one division per lane, broadcast within the 8-lane group
     double x[8];
 #pragma unroll
@@ -734,7 +739,7 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
     // k < 8 (i + 1)); kept in registers until the step's barrier
     double yn[WM][WN][2];
     {
-      constexpr int YS = MINB == 2 ? 1 : SC_GEMM1_SPLIT;  // accumulator sets (k steps round-robin)
+      constexpr int YS = MINB >= 2 ? 1 : SC_GEMM1_SPLIT;  // accumulator sets (k steps round-robin)
       double ya[YS][WM][WN][2];
 #pragma unroll
       for (int h = 0; h < YS; h++)
@@ -1165,8 +1170,11 @@ __global__ void __launch_bounds__(kThreads) implicit_apply_kernel(DevPlan P, con
   const int cls = P.sub_cls[sub];
   const int p0 = P.cls_panel0[cls], p1 = P.cls_panel0[cls + 1];
   const int m = P.sub_m[sub];
-  const Panel last = P.panels[p1 - 1];
-  const int n = last.a + last.kw;
+  int n = 0;
+  if (p1 > p0) {
+    const Panel last = P.panels[p1 - 1];
+    n = last.a + last.kw;
+  }
   double* x = SMEMV ? reinterpret_cast<double*>(iv_smem) : P.xv + (int64_t)sub * P.max_n;
   const double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
   const int32_t* __restrict__ ibp = P.ib_ptr + P.cls_ib0[cls];
@@ -1322,6 +1330,24 @@ sc_status alloc_zero(Plan& P, int64_t count, V** dst, std::string& err) {
 
 sc_status upload_plan(Plan& P, std::string& err) {
   CUDA_TRY(cudaSetDevice(P.opt.device));
+  // shared-memory fit checks before any allocation
+  if (P.ring_bytes <= 0) {
+    err = "X strip of " + std::to_string(P.max_strip_rows) + " rows x " + std::to_string(P.T) +
+          " columns leaves no room for the L-block ring in shared memory; use smaller tile_cols";
+    return SC_ERR_INVALID_ARG;
+  }
+  P.smem_trsm = trsm_smem_layout(P.T, P.ring_bytes, P.max_strip_rows, P.gstrip, !P.wmode).total;
+  if (P.ntrsm_small > 0) P.smem_trsm_small = trsm_smem_layout(P.T, P.ring_small, P.strip_small, false, !P.wmode).total;
+  {
+    int dev_smem = 0;
+    CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.opt.device));
+    if (P.smem_trsm > (size_t)dev_smem) {
+      err = "X strip of " + std::to_string(P.max_strip_rows) + " rows x " + std::to_string(P.T) +
+            " columns does not fit in shared memory (" + std::to_string(P.smem_trsm) + " > " + std::to_string(dev_smem) +
+            " bytes); use smaller tile_cols";
+      return SC_ERR_INVALID_ARG;
+    }
+  }
   DevPlan& D = P.dev;
   std::memset(&D, 0, sizeof(D));
   // concatenate class data
@@ -1400,7 +1426,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(alloc_zero(P, P.F_doubles, &D.F, err));
   TRY(alloc_zero(P, P.PB_doubles, &D.PB, err));
   TRY(alloc_zero(P, P.part_doubles, &D.part, err));
-  TRY(alloc_zero(P, 1, &D.err, err));
+  TRY(alloc_zero(P, 1 + (int64_t)P.nsub, &D.err, err));
   double** dl = nullptr;
   TRY(alloc_zero(P, std::max(P.nsub, 1), &dl, err));
   P.d_Lptr = dl;
@@ -1416,25 +1442,10 @@ sc_status upload_plan(Plan& P, std::string& err) {
   D.T = P.T;
   D.G = P.G;
   D.wmode = P.wmode ? 1 : 0;
-  if (P.ring_bytes <= 0) {
-    err = "X strip of " + std::to_string(P.max_strip_rows) + " rows x " + std::to_string(P.T) +
-          " columns leaves no room for the L-block ring in shared memory; use smaller tile_cols";
-    return SC_ERR_INVALID_ARG;
-  }
-  P.smem_trsm = trsm_smem_layout(P.T, P.ring_bytes, P.max_strip_rows, P.gstrip, !P.wmode).total;
-  if (P.ntrsm_small > 0) {  // small-strip tile class: its own (smaller) launch footprint
-    P.smem_trsm_small = trsm_smem_layout(P.T, P.ring_small, P.strip_small, false, !P.wmode).total;
+  if (P.ntrsm_small > 0) {  // small-strip tile class: its own launch on a side stream
     CUDA_TRY(cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&P.side_stream), cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(&P.ev_fork), cudaEventDisableTiming));
     CUDA_TRY(cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(&P.ev_join), cudaEventDisableTiming));
-  }
-  int dev_smem = 0;
-  CUDA_TRY(cudaDeviceGetAttribute(&dev_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.opt.device));
-  if (P.smem_trsm > (size_t)dev_smem) {
-    err = "X strip of " + std::to_string(P.max_strip_rows) + " rows x " + std::to_string(P.T) +
-          " columns does not fit in shared memory (" + std::to_string(P.smem_trsm) + " > " + std::to_string(dev_smem) +
-          " bytes); use smaller tile_cols";
-    return SC_ERR_INVALID_ARG;
   }
   // every kernel: the largest shared-memory carveout (the default left prep_small<16> at 3 CTAs/SM)
   auto smem_attr = [&](const void* fn, size_t bytes) -> cudaError_t {
@@ -1467,8 +1478,10 @@ sc_status upload_plan(Plan& P, std::string& err) {
   return SC_OK;
 }
 
+// Releases everything the plan allocated on the device / pinned host, whether or not upload_plan
+// completed (a failed upload must not orphan its allocations).
 void free_plan_device(Plan& P) {
-  if (!P.on_device) return;
+  if (P.opt.device < 0) return;
   cudaSetDevice(P.opt.device);
   cudaDeviceSynchronize();
   for (void* p : P.allocations) cudaFree(p);
@@ -1675,6 +1688,7 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
   P.factor_ready = true;
+  CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   if (P.overlap > 1 && P.nsub >= 2 * P.overlap) return launch_overlapped(P, stream, err);
   return launch_range(P, 0, P.nsub, stream, true, err);
 }
@@ -1714,6 +1728,7 @@ sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* str
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
   P.factor_ready = true;
+  CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream);
   // the staging buffer is reused: copies wait for everything enqueued on `stream` before this call
   CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_start), stream));
@@ -1768,6 +1783,7 @@ sc_status launch_prepare(Plan& P, const double* const* Lptr_host, void* stream_v
   sc_status st = set_Lptr(P, Lptr_host, stream, err);
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
+  CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   st = launch_prep_range(P, 0, P.nsub, stream, err);
   if (st == SC_OK) P.factor_ready = true;
   return st;
@@ -1818,8 +1834,22 @@ sc_status device_check(Plan& P, std::string& err) {
   return SC_OK;
 }
 
+// zero-pivot flag of subdomain i only (other subdomains' F stay readable)
+static sc_status device_check_sub(Plan& P, int32_t i, std::string& err) {
+  CUDA_TRY(cudaSetDevice(P.opt.device));
+  CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(P.last_stream)));
+  unsigned long long flag = 0;
+  CUDA_TRY(cudaMemcpy(&flag, P.dev.err + 1 + i, sizeof(flag), cudaMemcpyDeviceToHost));
+  if (flag) {
+    err = "non-positive or non-finite diagonal of L in subdomain " + std::to_string(i) + " column " +
+          std::to_string(flag - 1);
+    return SC_ERR_ZERO_PIVOT;
+  }
+  return SC_OK;
+}
+
 sc_status copy_F_lower(Plan& P, int32_t i, std::vector<double>& out, std::string& err) {
-  TRY(device_check(P, err));
+  TRY(device_check_sub(P, i, err));
   int64_t m = P.sub_m[(size_t)i];
   out.resize((size_t)(m * m));
   if (m > 0)
@@ -1828,7 +1858,7 @@ sc_status copy_F_lower(Plan& P, int32_t i, std::vector<double>& out, std::string
 }
 
 sc_status copy_X_strips(Plan& P, int32_t i, std::vector<double>& out, std::string& err) {
-  TRY(device_check(P, err));
+  TRY(device_check_sub(P, i, err));
   const ClassPlan& C = P.classes[(size_t)P.sub_cls[(size_t)i]];
   out.resize((size_t)C.x_doubles);
   if (C.x_doubles > 0)

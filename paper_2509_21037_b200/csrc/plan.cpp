@@ -557,6 +557,32 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     fprintf(stderr, "live rows: strip mean %.0f max %d | live(B upfront) mean %.0f max %d | live(B at own step) mean %.0f max %d\n",
             sum_all / C.tiles.size(), C.max_strip_rows, sum_up / C.tiles.size(), mx_up, sum_own / C.tiles.size(), mx_own);
   }
+  if (std::getenv("SC_DEBUG_TILES")) {
+    double st = 0, rows = 0, bytes = 0, flops = 0, nch = 0;
+    int mxs = 0, mxr = 0;
+    std::vector<int> kwh(9, 0);
+    for (auto& t : C.tiles) {
+      st += t.step_end - t.step_begin;
+      mxs = std::max(mxs, t.step_end - t.step_begin);
+      rows += t.strip_rows;
+      mxr = std::max(mxr, t.strip_rows);
+      for (int32_t s2 = t.step_begin; s2 < t.step_end; s2++) {
+        const Panel& P = C.panels[(size_t)C.steps[(size_t)s2].panel];
+        bytes += 8.0 * (P.ldD * P.kw4 + (P.nchunk ? ((P.nchunk - 1) * kLdC + P.ldLast) * P.kw4 : 0));
+        flops += 2.0 * T * P.kw * (P.kw + P.nR);
+        nch += P.nchunk;
+        kwh[std::min(8, (P.kw + 7) / 8)]++;
+      }
+    }
+    double pbytes = 0;
+    for (auto& P : C.panels) pbytes += 8.0 * (P.ldD * P.kw4 + (P.nchunk ? ((P.nchunk - 1) * kLdC + P.ldLast) * P.kw4 : 0));
+    const double nt = (double)C.tiles.size();
+    fprintf(stderr, "tiles n=%d m=%d T=%d: %zu tiles, steps/tile %.1f (max %d), chunks/tile %.1f, strip rows %.0f (max %d), "
+            "L block bytes/tile %.0f (panel buffer %.0f, reuse %.1f), flops/tile %.3g, kw/8 hist of steps",
+            n, m, T, C.tiles.size(), st / nt, mxs, nch / nt, rows / nt, mxr, bytes / nt, pbytes, bytes / pbytes, flops / nt);
+    for (int h : kwh) fprintf(stderr, " %d", h);
+    fprintf(stderr, "\n");
+  }
   if (std::getenv("SC_DEBUG_PLAN"))
     fprintf(stderr, "class n=%d m=%d T=%d gstrip=%d: panels %d tiles %zu steps %zu srows %zu Rrows %zu greach %zu binit %zu\n",
             n, m, T, (int)gstrip, np, C.tiles.size(), C.steps.size(), C.srows.size(), C.Rrows.size(), C.greach.size(),
@@ -814,9 +840,18 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   // 13.7 ms with shared strips, cfg4 51.8 vs 54.5 ms at T = 32, cfg5 324 vs 339 ms); SC_GS2=0 disables
   const char* gs2_env = std::getenv("SC_GS2");
   if (P.gstrip && P.T == 16 && !(gs2_env && gs2_env[0] == '0')) {  // ring within 1/ctas of an SM
-    P.gs2 = (gs2_env && gs2_env[0] == '3') ? 3 : 2;
-    const int64_t share = kSmemPerSM / P.gs2 - 1024;
+    int64_t maxblk = 16;
+    for (auto& C : P.classes)
+      for (auto& p : C.panels) {
+        maxblk = std::max<int64_t>(maxblk, (int64_t)p.ldD * p.kw4 * 8);
+        if (p.nchunk > 0) maxblk = std::max<int64_t>(maxblk, (int64_t)(p.nchunk > 1 ? kLdC : p.ldLast) * p.kw4 * 8);
+      }
     const int64_t fixed = (int64_t)trsm_smem_layout(16, 0, 0, true, !P.wmode).total;
+    // 3 CTAs per SM only when the ring still holds two of the largest L blocks (double buffering)
+    const int want = (gs2_env && gs2_env[0] == '3') ? 3 : 2;
+    P.gs2 = 2;
+    if (want == 3 && ((kSmemPerSM / 3 - 1024 - fixed) & ~(int64_t)127) >= 2 * maxblk) P.gs2 = 3;
+    const int64_t share = kSmemPerSM / P.gs2 - 1024;
     P.ring_bytes = (int32_t)(std::min<int64_t>(P.ring_bytes, share - fixed) & ~(int64_t)127);
   }
   // small-strip tile class (shared strips): tiles whose strip fits next to a ring of >= 2 of the

@@ -443,6 +443,10 @@ CONFIGS: Dict[str, dict] = {
     "t2d": dict(dim=2, physics="heat", S=3, E=6),
     "t3d": dict(dim=3, physics="heat", S=2, E=4),
     "t3e": dict(dim=3, physics="elasticity", S=2, E=3),
+    # S=3 per axis: all 27 boundary classes (x=0 Dirichlet face / edges / corner, the other faces,
+    # edges and corners, and the interior subdomain 13)
+    "t3h3": dict(dim=3, physics="heat", S=3, E=4),
+    "t3e3": dict(dim=3, physics="elasticity", S=3, E=3),
 }
 
 
