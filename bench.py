@@ -375,6 +375,7 @@ def main():
         torch.cuda.synchronize()
         t_expl = a0.elapsed_time(a1) / reps
         # GPU implicit apply (two substitutions per subdomain with the staged factor, no F)
+        plan.prepare_factor(Ls)
         for _ in range(3):
             plan.apply_implicit(lam_d, q_d)
         torch.cuda.synchronize()

@@ -88,8 +88,15 @@ typedef struct {
                                 (shared memory when the largest strip fits next to the L-block
                                 ring, else global), SC_STRIP_SHARED, SC_STRIP_GLOBAL (in place in the
                                 SYRK group strip in HBM/L2; large subdomains, e.g. cfg5)             */
-  int32_t reserved[6];       /* must be zero                                                        */
+  int32_t trsm_kernel;       /* SC_TRSM_AUTO, SC_TRSM_CTA (warp-specialised CTA per tile, factor
+                                staged by the prep kernels) or SC_TRSM_WARP (one warp per tile, DMMA
+                                fragments gathered straight from the CSC values of L: L read once,
+                                no prep; panels <= 32 columns, global strips, tile_cols 8 or 16).
+                                AUTO = WARP for small operators (max m <= 512, e.g. 2D), else CTA   */
+  int32_t reserved[5];       /* must be zero                                                        */
 } sc_options;
+
+enum { SC_TRSM_AUTO = 0, SC_TRSM_CTA = 1, SC_TRSM_WARP = 2 };
 
 /* Work and size counters (SURVEY.md Appendix A definitions).  flops: 2 per multiply-add, 1 per
    division.  "useful" = etree-exact structural non-zero work (independent of skip mode and tile
@@ -114,6 +121,8 @@ typedef struct {
   int32_t group_cols;        /* SYRK output tile width G                                            */
   int32_t x_strip;           /* SC_STRIP_SHARED or SC_STRIP_GLOBAL: the mode the plan chose         */
   int64_t trsm_tasks_2cta;   /* TRSM tiles in the small-strip class (own launch, two CTAs per SM)   */
+  int32_t trsm_kernel;       /* SC_TRSM_CTA or SC_TRSM_WARP: the TRSM kernel the plan chose         */
+  int32_t pad0;
 } sc_stats;
 
 /* Fill `opt` with defaults: precision 64, skip EXACT, tile/panel auto, device 0. */

@@ -205,7 +205,8 @@ int32_t sc_launches_per_assemble(sc_plan_t p) {
   if (!p) return 0;
   int small = 0;
   for (int b = 0; b < 3; b++) small += p->P.small_begin[b + 1] > p->P.small_begin[b] ? 1 : 0;
-  return (p->P.prep_tasks.empty() ? 0 : 1) + small +
+  if (p->P.warp_trsm) small = 0;
+  return (p->P.prep_tasks.empty() || p->P.warp_trsm ? 0 : 1) + small +
          (p->P.trsm_tasks.empty() ? 0 : 1) + (p->P.syrk_tasks.empty() ? 0 : 1);
 }
 

@@ -926,6 +926,249 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
   }
 }
 
+
+// ------------------------------------------------------------------------------------------------
+// Warp TRSM (rows a1+a2+a3 fused for narrow panels, e.g. 2D): one warp per (subdomain, tile of
+// T = 8 NB columns), no CTA barriers, no prep.  The tile's X strip lives in its T columns of the
+// SYRK group strip (global memory, L2-resident while the tile runs).  Per step (factor panel p in
+// the tile's reach, kw <= 32):
+//   X_p <- L_pp^{-1} X_p   blocked by 8: each 8x8 diagonal block by substitution in registers
+//                          (lanes = (row g, column pair 2t)), the blocks below by DMMA;
+//   X[R_p] -= L[R_p,p] X_p DMMA over 8-row blocks of the pruned rows R_p, read-modify-write of the
+//                          strip rows (row map = the group strip's srows).
+// Every A fragment is gathered straight from the caller's CSC values through the plan's fragment
+// gather map (Panel::gx_off), so L crosses HBM once and nothing is staged.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+__device__ __forceinline__ double gather_l(const double* __restrict__ Lv, int32_t q) {
+  return q >= 0 ? __ldg(Lv + q) : 0.0;
+}
+
+#ifndef SC_WARP_MINB
+#define SC_WARP_MINB 4
+#endif
+constexpr int kWarpTri = 10 * 64;  // staged triangle values per warp: <= 10 8x8 blocks (kw <= 32)
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+
+// R-row update (X[R_p] -= L[R_p, p] Y) in batches of NRBB 8-row blocks (KS <= KSMAX k steps).
+// q / row hold the gather map / row map of one batch (q[r * KSMAX/2 + k2]); warp_r_idx loads them
+// (L2), warp_r_run gathers the L values (HBM) and the old X rows (L2) of the batch, issues the next
+// batch's maps, then D = X - L Y by DMMA with Y's B fragments from shared memory, and stores.
+template <int KSMAX, int NRBB>
+__device__ __forceinline__ void warp_r_idx(const int32_t* __restrict__ gr, const uint16_t* __restrict__ srw, int R0,
+                                           int nRB, int KS, int lane, int2 (&q)[8], int (&row)[4]) {
+  const int g = lane >> 2;
+#pragma unroll
+  for (int r = 0; r < NRBB; r++) {
+    const bool on = R0 + r < nRB;
+    row[r] = on ? (int)__ldg(srw + 8 * (R0 + r) + g) : 0xFFFF;
+    const int2* gi = reinterpret_cast<const int2*>(gr + ((int64_t)(R0 + r) * 32 + lane) * KS);
+#pragma unroll
+    for (int k2 = 0; k2 < KSMAX / 2; k2++) q[r * (KSMAX / 2) + k2] = (on && 2 * k2 < KS) ? __ldg(gi + k2) : make_int2(-1, -1);
+  }
+}
+template <int NB, int KSMAX, int NRBB, int LDY>
+__device__ __forceinline__ void warp_r_run(const double* __restrict__ Lv, const int32_t* __restrict__ gr,
+                                          const uint16_t* __restrict__ srw, double* __restrict__ Xs, const int G,
+                                          const double* __restrict__ Ys, const int nRB, const int KS, const int lane,
+                                          int2 (&q)[8], int (&row)[4]) {
+  const int g = lane >> 2, t = lane & 3;
+  for (int R0 = 0; R0 < nRB; R0 += NRBB) {
+    double a[NRBB][KSMAX];
+    double2 xo[NRBB][NB];
+    int rc[NRBB];
+#pragma unroll
+    for (int r = 0; r < NRBB; r++) {
+      rc[r] = row[r];
+#pragma unroll
+      for (int k2 = 0; k2 < KSMAX / 2; k2++) {
+        a[r][2 * k2] = -gather_l(Lv, q[r * (KSMAX / 2) + k2].x);
+        a[r][2 * k2 + 1] = -gather_l(Lv, q[r * (KSMAX / 2) + k2].y);
+      }
+#pragma unroll
+      for (int j = 0; j < NB; j++)
+        xo[r][j] = rc[r] != 0xFFFF ? *reinterpret_cast<const double2*>(Xs + (int64_t)rc[r] * G + 8 * j + 2 * t)
+                                   : make_double2(0.0, 0.0);
+    }
+    if (R0 + NRBB < nRB) warp_r_idx<KSMAX, NRBB>(gr, srw, R0 + NRBB, nRB, KS, lane, q, row);
+#pragma unroll
+    for (int ks = 0; ks < KSMAX; ks++) {
+      if (ks >= KS) break;
+#pragma unroll
+      for (int j = 0; j < NB; j++) {
+        const double b = Ys[(4 * ks + t) * LDY + 8 * j + g];
+#pragma unroll
+        for (int r = 0; r < NRBB; r++) dmma(xo[r][j].x, xo[r][j].y, a[r][ks], b);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NRBB; r++)
+      if (rc[r] != 0xFFFF) {
+#pragma unroll
+        for (int j = 0; j < NB; j++) *reinterpret_cast<double2*>(Xs + (int64_t)rc[r] * G + 8 * j + 2 * t) = xo[r][j];
+      }
+  }
+}
+
+// Gathers of a panel's triangle values (fragment order) into Ts with cp.async (no registers held
+// while they travel; structural zeros zero-filled).
+__device__ __forceinline__ void warp_tri_gather(const double* __restrict__ Lv, const int2 (&q)[10], int ntb,
+                                                double* Ts, int lane) {
+#pragma unroll
+  for (int b = 0; b < 10; b++)
+    if (b < ntb) {
+      cp_async8(Ts + 64 * b + lane, Lv + (q[b].x >= 0 ? q[b].x : 0), q[b].x >= 0 ? 8 : 0);
+      cp_async8(Ts + 64 * b + 32 + lane, Lv + (q[b].y >= 0 ? q[b].y : 0), q[b].y >= 0 ? 8 : 0);
+    }
+}
+__device__ __forceinline__ void warp_tri_idx(const int32_t* __restrict__ gx, int ntb, int lane, int2 (&q)[10]) {
+#pragma unroll
+  for (int b = 0; b < 10; b++) q[b] = b < ntb ? __ldg(reinterpret_cast<const int2*>(gx + 64 * b) + lane) : make_int2(-1, -1);
+}
+
+// One warp per (subdomain, tile), software-pipelined over the tile's steps: the next panel's
+// descriptors and triangle gather map are loaded during the current step and its triangle values are
+// gathered (cp.async) as soon as the current triangle is solved; the first R batch's maps are
+// loaded before the triangle solve.  Per warp shared memory: X_p / Y (32 x LDY), the triangle
+// values (block b, k step s: Ts[64 b + 32 s + lane]) and the reciprocal pivots.
+template <int NB>
+__global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P, int t0, int ntask) {
+  constexpr int T = 8 * NB, LDY = T + 4;
+  __shared__ __align__(16) double wsm[4][32 * LDY + kWarpTri + 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wt = blockIdx.x * 4 + wid;
+  if (wt >= ntask) return;
+  double* __restrict__ Ys = wsm[wid];
+  double* __restrict__ Ts = Ys + 32 * LDY;
+  double* __restrict__ Rv = Ts + kWarpTri;
+  const I2 task = P.trsm_tasks[t0 + wt];
+  const int sub = task.x;
+  const Tile tile = P.tiles[task.y];
+  const double* __restrict__ Lv = P.Lptr[sub];
+  const int G = P.G;
+  double* __restrict__ Xs = P.X + P.sub_X_base[sub] + P.groups[tile.group].x_off + tile.col_in_group;
+  const int g = lane >> 2, t = lane & 3;
+  constexpr int VPR = T / 2, RPI = 32 / VPR;  // double2 per strip row, rows per warp instruction
+  const int vr0 = lane / VPR, vc2 = 2 * (lane % VPR);
+  Step st_n{};
+  Panel pn_n{};
+  int2 qt[10];
+  if (tile.step_begin < tile.step_end) {
+    st_n = P.steps[tile.step_begin];
+    pn_n = P.panels[st_n.panel];
+    const int k8 = (pn_n.kw + 7) >> 3;
+    warp_tri_idx(P.gidx + pn_n.gx_off, k8 * (k8 + 1) / 2, lane, qt);
+    warp_tri_gather(Lv, qt, k8 * (k8 + 1) / 2, Ts, lane);
+  }
+  // X init (row a2): zero the tile's columns of every group-strip row, scatter B~^T
+  for (int r = vr0; r < tile.strip_rows; r += RPI)
+    *reinterpret_cast<double2*>(Xs + (int64_t)r * G + vc2) = make_double2(0.0, 0.0);
+  __syncwarp();
+  for (int q = tile.binit_begin + lane; q < tile.binit_end; q += 32) {
+    const BInit bi = P.binit[q];
+    Xs[(int64_t)bi.strip_row * G + bi.col] = bi.val;
+  }
+  __syncwarp();
+  for (int s = tile.step_begin; s < tile.step_end; s++) {
+    const Step st = st_n;
+    const Panel pn = pn_n;
+    const int kw = pn.kw, kw8 = (kw + 7) >> 3, KS = 2 * kw8;
+    const int32_t* __restrict__ gx = P.gidx + pn.gx_off;
+    double* __restrict__ xp = Xs + (int64_t)st.strip_row * G;
+    // X_p -> Ys (cp.async; rows kw..8 kw8 zero-filled)
+    for (int r = vr0; r < 8 * kw8; r += RPI)
+      cp_async16(Ys + r * LDY + vc2, xp + (int64_t)(r < kw ? r : 0) * G + vc2, r < kw ? 16 : 0);
+    cp_async_commit();
+    const bool more = s + 1 < tile.step_end;
+    if (more) {  // next step's descriptors and triangle gather map
+      st_n = P.steps[s + 1];
+      pn_n = P.panels[st_n.panel];
+      const int k8 = (pn_n.kw + 7) >> 3;
+      warp_tri_idx(P.gidx + pn_n.gx_off, k8 * (k8 + 1) / 2, lane, qt);
+    }
+    // first R batch's maps
+    const int nRB = (pn.nR + 7) >> 3;
+    const int32_t* __restrict__ gr = gx + 64 * (kw8 * (kw8 + 1) / 2);
+    const uint16_t* __restrict__ srw = P.srows + st.srow_off;
+    int2 qr[8];
+    int rr[4];
+    if (KS <= 4) warp_r_idx<4, 4>(gr, srw, 0, nRB, KS, lane, qr, rr);
+    else warp_r_idx<8, 2>(gr, srw, 0, nRB, KS, lane, qr, rr);
+    cp_async_wait<0>();  // this step's triangle values (issued during the previous step) and X_p
+    __syncwarp();
+    {  // reciprocal pivots, one row per lane
+      const int K = lane >> 3, gg = lane & 7;
+      const bool live = lane < kw;
+      const double d = live ? Ts[64 * warp_tri_block(K, K, kw8) + 32 * (gg >> 2) + 4 * gg + (gg & 3)] : 1.0;
+      if (live && (!(d > 0.0) || !isfinite(d))) flag_zero_pivot(P, sub, pn.a + lane);
+      Rv[lane] = live ? 1.0 / d : 0.0;
+    }
+    __syncwarp();
+    // X_p <- L_pp^{-1} X_p over 8-row blocks K: X_K -= L_KJ Y_J (J < K, DMMA on C fragments), then
+    // the 8x8 diagonal block by substitution, one column per lane (L entries broadcast from Ts)
+    for (int K = 0; K < kw8; K++) {
+      if (K > 0) {
+        double2 x[NB];
+#pragma unroll
+        for (int j = 0; j < NB; j++) x[j] = *reinterpret_cast<const double2*>(Ys + (8 * K + g) * LDY + 8 * j + 2 * t);
+        for (int J = 0; J < K; J++) {
+          const double* tb = Ts + 64 * warp_tri_block(J, K, kw8);
+          const double a0 = -tb[lane], a1 = -tb[32 + lane];
+#pragma unroll
+          for (int j = 0; j < NB; j++) {
+            dmma(x[j].x, x[j].y, a0, Ys[(8 * J + t) * LDY + 8 * j + g]);
+            dmma(x[j].x, x[j].y, a1, Ys[(8 * J + 4 + t) * LDY + 8 * j + g]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < NB; j++) *reinterpret_cast<double2*>(Ys + (8 * K + g) * LDY + 8 * j + 2 * t) = x[j];
+        __syncwarp();
+      }
+      if (lane < T) {
+        const double* tb = Ts + 64 * warp_tri_block(K, K, kw8);
+        double xv[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++) xv[i] = Ys[(8 * K + i) * LDY + lane];
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          xv[k] *= Rv[8 * K + k];
+#pragma unroll
+          for (int i = k + 1; i < 8; i++) xv[i] = fma(-tb[32 * (k >> 2) + 4 * i + (k & 3)], xv[k], xv[i]);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; i++) Ys[(8 * K + i) * LDY + lane] = xv[i];
+      }
+      __syncwarp();
+    }
+    // Ts is free: gather the next step's triangle while this step's R rows are updated
+    if (more) {
+      const int k8 = (pn_n.kw + 7) >> 3;
+      warp_tri_gather(Lv, qt, k8 * (k8 + 1) / 2, Ts, lane);
+    }
+    cp_async_commit();
+    // the solved rows are final: into the group strip
+    for (int r = vr0; r < kw; r += RPI)
+      *reinterpret_cast<double2*>(xp + (int64_t)r * G + vc2) = *reinterpret_cast<const double2*>(Ys + r * LDY + vc2);
+    if (KS <= 4) warp_r_run<NB, 4, 4, LDY>(Lv, gr, srw, Xs, G, Ys, nRB, KS, lane, qr, rr);
+    else warp_r_run<NB, 8, 2, LDY>(Lv, gr, srw, Xs, G, Ys, nRB, KS, lane, qr, rr);
+    __syncwarp();  // this step's strip writes are visible to every lane of the next step
+  }
+  cp_async_wait<0>();
+}
+
 // ------------------------------------------------------------------------------------------------
 // SYRK over G-column groups: F'[I,J] = sum_seg X_I[seg]^T X_J[seg] (lower part of F' only)
 // ------------------------------------------------------------------------------------------------
@@ -942,16 +1185,6 @@ struct SyrkCfg {              // (G/8)^2 output blocks of 8x8 over 8 warps
   static constexpr int NWC = NB / WN;
   static constexpr int ACTIVE = (NB / WM) * NWC;   // warps with work (4 for G = 16)
 };
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 
 template <int G>
 constexpr size_t syrk_smem_bytes() {
@@ -1331,12 +1564,12 @@ sc_status alloc_zero(Plan& P, int64_t count, V** dst, std::string& err) {
 sc_status upload_plan(Plan& P, std::string& err) {
   CUDA_TRY(cudaSetDevice(P.opt.device));
   // shared-memory fit checks before any allocation
-  if (P.ring_bytes <= 0) {
+  if (P.ring_bytes <= 0 && !P.warp_trsm) {
     err = "X strip of " + std::to_string(P.max_strip_rows) + " rows x " + std::to_string(P.T) +
           " columns leaves no room for the L-block ring in shared memory; use smaller tile_cols";
     return SC_ERR_INVALID_ARG;
   }
-  P.smem_trsm = trsm_smem_layout(P.T, P.ring_bytes, P.max_strip_rows, P.gstrip, !P.wmode).total;
+  P.smem_trsm = P.warp_trsm ? 0 : trsm_smem_layout(P.T, P.ring_bytes, P.max_strip_rows, P.gstrip, !P.wmode).total;
   if (P.ntrsm_small > 0) P.smem_trsm_small = trsm_smem_layout(P.T, P.ring_small, P.strip_small, false, !P.wmode).total;
   {
     int dev_smem = 0;
@@ -1362,10 +1595,14 @@ sc_status upload_plan(Plan& P, std::string& err) {
   std::vector<BInit> binit;
   std::vector<Pair> pairs;
   std::vector<Seg> segs;
+  std::vector<int32_t> gidx;
   for (auto& C : P.classes) {
     csc_off.push_back((int64_t)dest.size());
     dest.insert(dest.end(), C.dest.begin(), C.dest.end());
+    const size_t p0 = panels.size();
     panels.insert(panels.end(), C.panels.begin(), C.panels.end());
+    for (size_t q = p0; q < panels.size(); q++) panels[q].gx_off += (int64_t)gidx.size();
+    gidx.insert(gidx.end(), C.gidx.begin(), C.gidx.end());
     Rrows.insert(Rrows.end(), C.Rrows.begin(), C.Rrows.end());
     tiles.insert(tiles.end(), C.tiles.begin(), C.tiles.end());
     steps.insert(steps.end(), C.steps.begin(), C.steps.end());
@@ -1377,6 +1614,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
     segs.insert(segs.end(), C.segs.begin(), C.segs.end());
   }
   TRY(upload(P, panels, &D.panels, err));
+  TRY(upload(P, gidx, &D.gidx, err));
   TRY(upload(P, Rrows, &D.Rrows, err));
   TRY(upload(P, dest, &D.dest, err));
   TRY(upload(P, csc_off, &D.cls_csc_off, err));
@@ -1424,7 +1662,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, P.qg_sub_a, &D.qg_sub_a, err));
   TRY(alloc_zero(P, P.X_doubles, &D.X, err));
   TRY(alloc_zero(P, P.F_doubles, &D.F, err));
-  TRY(alloc_zero(P, P.PB_doubles, &D.PB, err));
+  if (!P.warp_trsm) TRY(alloc_zero(P, P.PB_doubles, &D.PB, err));  // warp TRSM: only for the implicit apply, lazily
   TRY(alloc_zero(P, P.part_doubles, &D.part, err));
   TRY(alloc_zero(P, 1 + (int64_t)P.nsub, &D.err, err));
   double** dl = nullptr;
@@ -1465,10 +1703,15 @@ sc_status upload_plan(Plan& P, std::string& err) {
   CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<16>, syrk_smem_bytes<16>()));
   CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<32>, syrk_smem_bytes<32>()));
   CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<64>, syrk_smem_bytes<64>()));
-  CUDA_TRY(smem_attr((const void*)(P.gs2 ? trsm_kernel_ptr_gs2(P.wmode, P.gs2) : trsm_kernel_ptr(P.T, P.gstrip, P.wmode)),
-                     P.smem_trsm));
+  CUDA_TRY(cudaFuncSetAttribute((const void*)trsm_warp_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared));
+  CUDA_TRY(cudaFuncSetAttribute((const void*)trsm_warp_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)cudaSharedmemCarveoutMaxShared));
+  if (!P.warp_trsm)
+    CUDA_TRY(smem_attr((const void*)(P.gs2 ? trsm_kernel_ptr_gs2(P.wmode, P.gs2) : trsm_kernel_ptr(P.T, P.gstrip, P.wmode)),
+                       P.smem_trsm));
   if (P.ntrsm_small > 0) CUDA_TRY(smem_attr((const void*)trsm_kernel_ptr2(P.T, P.wmode), P.smem_trsm_small));
-  double total = 8.0 * (P.X_doubles + P.F_doubles + P.PB_doubles + P.part_doubles);
+  double total = 8.0 * (P.X_doubles + P.F_doubles + (P.warp_trsm ? 0 : P.PB_doubles) + P.part_doubles) + 4.0 * gidx.size();
   total += dest.size() * 4.0 + Rrows.size() * 4.0 + panels.size() * sizeof(Panel) + tiles.size() * sizeof(Tile) +
            steps.size() * sizeof(Step) + groups.size() * sizeof(Group) +
            greach.size() * sizeof(Reach) + binit.size() * sizeof(BInit) + pairs.size() * sizeof(Pair) +
@@ -1578,6 +1821,17 @@ static sc_status launch_prep_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
 // whole batch.
 static sc_status launch_trsm_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, std::string& err) {
   const bool all = s0 == 0 && s1 == P.nsub;
+  if (P.warp_trsm) {
+    const int ntr = (int)P.trsm_tasks.size();
+    const int a = all ? 0 : task_lb(P.trsm_tasks, 0, ntr, s0), b = all ? ntr : task_lb(P.trsm_tasks, 0, ntr, s1);
+    if (b > a) {
+      const int nb = (b - a + 3) / 4;  // 4 warps (tiles) per CTA
+      if (P.T == 8) trsm_warp_kernel<1><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
+      else trsm_warp_kernel<2><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
+      CUDA_TRY(cudaGetLastError());
+    }
+    return SC_OK;
+  }
   {
     // tiles with small strips (2 CTAs per SM) and the rest (1 CTA per SM): two launches, the large
     // ones on a side stream so both classes share the SMs and neither launch's tail idles them
@@ -1629,7 +1883,7 @@ static sc_status launch_syrk_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
 // whole batch.
 static sc_status launch_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, bool timing, std::string& err) {
   if (timing && P.tev[0]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[0], stream));
-  sc_status st = launch_prep_range(P, s0, s1, stream, err);
+  sc_status st = P.warp_trsm ? SC_OK : launch_prep_range(P, s0, s1, stream, err);  // warp TRSM: no prep
   if (st != SC_OK) return st;
   if (timing && P.tev[1]) CUDA_TRY(cudaEventRecord((cudaEvent_t)P.tev[1], stream));
   st = launch_trsm_range(P, s0, s1, stream, err);
@@ -1662,7 +1916,7 @@ static sc_status launch_overlapped(Plan& P, cudaStream_t stream, std::string& er
   CUDA_TRY(cudaStreamWaitEvent(ss, ev(0), 0));
   for (int k = 0; k < K; k++) {
     const int32_t s0 = (int32_t)((int64_t)P.nsub * k / K), s1 = (int32_t)((int64_t)P.nsub * (k + 1) / K);
-    sc_status st = launch_prep_range(P, s0, s1, stream, err);
+    sc_status st = P.warp_trsm ? SC_OK : launch_prep_range(P, s0, s1, stream, err);
     if (st != SC_OK) return st;
     CUDA_TRY(cudaEventRecord(ev(2 + 2 * k), stream));
     CUDA_TRY(cudaStreamWaitEvent(ts, ev(2 + 2 * k), 0));
@@ -1687,7 +1941,7 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
   sc_status st = set_Lptr(P, Lptr_host, stream, err);
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
-  P.factor_ready = true;
+  P.factor_ready = !P.warp_trsm;  // the warp TRSM does not stage the factor panels
   CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   if (P.overlap > 1 && P.nsub >= 2 * P.overlap) return launch_overlapped(P, stream, err);
   return launch_range(P, 0, P.nsub, stream, true, err);
@@ -1727,7 +1981,7 @@ sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* str
   sc_status st = set_Lptr(P, dptrs.data(), stream, err);
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
-  P.factor_ready = true;
+  P.factor_ready = !P.warp_trsm;  // the warp TRSM does not stage the factor panels
   CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream);
   // the staging buffer is reused: copies wait for everything enqueued on `stream` before this call
@@ -1783,6 +2037,12 @@ sc_status launch_prepare(Plan& P, const double* const* Lptr_host, void* stream_v
   sc_status st = set_Lptr(P, Lptr_host, stream, err);
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
+  if (!P.dev.PB) {  // warp-TRSM plans stage the factor panels only for the implicit apply
+    double* pb = nullptr;
+    TRY(alloc_zero(P, P.PB_doubles, &pb, err));
+    P.dev.PB = pb;
+    P.stats.device_bytes += 8.0 * (double)P.PB_doubles;
+  }
   CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   st = launch_prep_range(P, 0, P.nsub, stream, err);
   if (st == SC_OK) P.factor_ready = true;

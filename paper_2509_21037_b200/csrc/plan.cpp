@@ -128,7 +128,7 @@ int relax_wsmall() {
 
 // Steps 2-7 for one class.
 sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, int skip, bool gstrip,
-                        int32_t strip_limit, ClassPlan& C, std::string& err) {
+                        int32_t strip_limit, bool warp, ClassPlan& C, std::string& err) {
   const int32_t n = d.n, m = d.m;
   C.n = n;
   C.m = m;
@@ -276,6 +276,36 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     C.fl_prep_exec += (double)p.kw * p.kw * p.kw / 3.0;
   }
   C.pb_doubles = pb;
+  // warp TRSM: fragment gather maps (sc_internal.h) from the same CSC walk
+  if (warp) {
+    int64_t gx = 0;
+    for (auto& p : C.panels) {
+      if (p.kw > 32) FAIL(SC_ERR_INVALID_ARG, "warp TRSM needs factor panels of <= 32 columns");
+      p.gx_off = gx;
+      gx += warp_gx_size(p.kw, p.nR);
+    }
+    if (cp[n] > INT32_MAX) FAIL(SC_ERR_INVALID_ARG, "warp TRSM: nnz(L) exceeds 2^31");
+    C.gidx.assign((size_t)gx, -1);
+    for (auto& p : C.panels) {
+      const int kw8 = (p.kw + 7) / 8, KS = 2 * kw8;
+      const int64_t roff = p.gx_off + 64 * (int64_t)(kw8 * (kw8 + 1) / 2);
+      const int32_t* R = C.Rrows.data() + p.R_off;
+      const int32_t b = p.a + p.kw;
+      for (int32_t c = p.a; c < b; c++)
+        for (int64_t q = cp[c]; q < cp[c + 1]; q++) {
+          const int32_t r = ri[q], cc = c - p.a;
+          const int s = (cc & 7) >> 2, t = cc & 3;
+          if (r < b) {
+            const int rr = r - p.a, lane = 4 * (rr & 7) + t;
+            C.gidx[(size_t)(p.gx_off + 64 * warp_tri_block(cc >> 3, rr >> 3, kw8) + 2 * lane + s)] = (int32_t)q;
+          } else {
+            const int32_t k = (int32_t)(std::lower_bound(R, R + p.nR, r) - R);
+            const int lane = 4 * (k & 7) + t;
+            C.gidx[(size_t)(roff + ((int64_t)(k >> 3) * 32 + lane) * KS + (cc >> 2))] = (int32_t)q;
+          }
+        }
+    }
+  }
   if (std::getenv("SC_DEBUG_PB")) {
     double inv = 0, chunk = 0, useful = 0, nsmall = 0, nbig = 0;
     std::vector<int> hist(9, 0);
@@ -464,8 +494,12 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
         in_tile[(size_t)p] = J;
         C.steps.push_back({p, strip_base[(size_t)p], C.greach[q].off, 0, 0});
         const Panel& P = C.panels[(size_t)p];
-        // GEMM1 skips the zero blocks above the diagonal of inv(L_pp)
-        C.fl_trsm_exec += 2.0 * T * P.kw4 * (0.5 * (double)P.kw4 + 4.0 + (double)P.nR);
+        if (warp) {  // 8x8 triangle blocks (I >= K) + 8-row blocks of R_p, k padded to 8
+          const double kw8 = (P.kw + 7) / 8, nRB = (P.nR + 7) / 8;
+          C.fl_trsm_exec += 2.0 * T * (32.0 * kw8 * (kw8 + 1) + 64.0 * nRB * kw8);
+        } else {  // GEMM1 skips the zero blocks above the diagonal of inv(L_pp)
+          C.fl_trsm_exec += 2.0 * T * P.kw4 * (0.5 * (double)P.kw4 + 4.0 + (double)P.nR);
+        }
         rows += P.kw;
       }
       t.step_end = (int32_t)C.steps.size();
@@ -582,6 +616,19 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
             n, m, T, C.tiles.size(), st / nt, mxs, nch / nt, rows / nt, mxr, bytes / nt, pbytes, bytes / pbytes, flops / nt);
     for (int h : kwh) fprintf(stderr, " %d", h);
     fprintf(stderr, "\n");
+    std::vector<int> vh(12, 0), rh(20, 0);
+    for (auto& t : C.tiles)
+      for (int32_t s2 = t.step_begin; s2 < t.step_end; s2++) {
+        const Panel& P = C.panels[(size_t)C.steps[(size_t)s2].panel];
+        const int kw8 = (P.kw + 7) / 8, nRB = (P.nR + 7) / 8;
+        vh[std::min(11, (kw8 * (kw8 + 1) + nRB * 2 * kw8) / 8)]++;
+        rh[std::min(19, nRB)]++;
+      }
+    fprintf(stderr, "  values/lane per step (x8) hist:");
+    for (int h : vh) fprintf(stderr, " %d", h);
+    fprintf(stderr, "\n  nRB hist:");
+    for (int h : rh) fprintf(stderr, " %d", h);
+    fprintf(stderr, "\n");
   }
   if (std::getenv("SC_DEBUG_PLAN"))
     fprintf(stderr, "class n=%d m=%d T=%d gstrip=%d: panels %d tiles %zu steps %zu srows %zu Rrows %zu greach %zu binit %zu\n",
@@ -647,7 +694,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     FAIL(SC_ERR_INVALID_ARG, "tile_cols must be 0, 8, 16, 32 or 64");
   if (opt.panel_cols < 0 || opt.panel_cols > kMaxPanel) FAIL(SC_ERR_INVALID_ARG, "panel_cols must be in [0, 64]");
   if (opt.x_strip < 0 || opt.x_strip > 2) FAIL(SC_ERR_INVALID_ARG, "x_strip must be 0, 1 or 2");
-  for (int k = 0; k < 6; k++)
+  for (int k = 0; k < 5; k++)
     if (opt.reserved[k] != 0) FAIL(SC_ERR_INVALID_ARG, "reserved options must be zero");
   P.opt = opt;
   P.nsub = nsub;
@@ -701,6 +748,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   if (const char* e = std::getenv("SC_GROUP")) G0 = std::atoi(e);
   if (!(G0 == 16 || G0 == 32 || G0 == 64)) FAIL(SC_ERR_INVALID_ARG, "SC_GROUP must be 16, 32 or 64");
   // classes are independent: analysed on all host cores
+  bool warp = false;  // analyse for the warp TRSM (fragment gather maps)
   auto analyse_all = [&](int T, bool gstrip, int32_t strip_limit) -> sc_status {
     P.T = T;
     P.G = std::max(G0, T);
@@ -714,7 +762,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
         uint64_t h = P.classes[c].hash;
         P.classes[c] = ClassPlan();
         P.classes[c].hash = h;
-        st[c] = analyse_class(sd[rep[c]], T, P.G, P.PW, opt.skip, gstrip, strip_limit, P.classes[c], errs[c]);
+        st[c] = analyse_class(sd[rep[c]], T, P.G, P.PW, opt.skip, gstrip, strip_limit, warp, P.classes[c], errs[c]);
       }
     };
     const size_t nthr = std::min<size_t>(nc, std::max(1u, std::thread::hardware_concurrency()));
@@ -791,7 +839,26 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   };
   // global-strip tile width: 32 (measured on cfg4 / cfg5: 16 and 64 are slower)
   const int Tg = opt.tile_cols ? opt.tile_cols : 32;
-  if (opt.x_strip == SC_STRIP_GLOBAL) {
+  // warp TRSM (one warp per tile, fragments straight from the CSC values, no prep): small operators
+  // (2D) with narrow panels; tiles of 8 or 16 columns solved in place in the group strips
+  if (opt.trsm_kernel < 0 || opt.trsm_kernel > 2) FAIL(SC_ERR_INVALID_ARG, "trsm_kernel must be 0, 1 or 2");
+  warp = opt.trsm_kernel == SC_TRSM_WARP ||
+         (opt.trsm_kernel == SC_TRSM_AUTO && max_m <= 512 && P.PW <= 32 && !P.wmode &&
+          (opt.tile_cols == 0 || opt.tile_cols <= 16) && opt.x_strip != SC_STRIP_SHARED && !std::getenv("SC_NO_WARP"));
+  if (warp) {
+    if (P.PW > 32) FAIL(SC_ERR_INVALID_ARG, "warp TRSM needs panel_cols <= 32");
+    if (opt.x_strip == SC_STRIP_SHARED) FAIL(SC_ERR_INVALID_ARG, "warp TRSM solves in the global strips");
+    int Tw = opt.tile_cols;
+    if (!Tw) {
+      const char* e = std::getenv("SC_WARP_T");
+      Tw = e ? std::atoi(e) : 16;
+    }
+    if (!(Tw == 8 || Tw == 16)) FAIL(SC_ERR_INVALID_ARG, "warp TRSM needs tile_cols 8 or 16");
+    P.wmode = false;
+    sc_status st = analyse_all(Tw, true, -1);
+    if (st != SC_OK) return st;
+    P.warp_trsm = true;
+  } else if (opt.x_strip == SC_STRIP_GLOBAL) {
     sc_status st = analyse_all(Tg, true, -1);
     if (st != SC_OK) return st;
   } else {
@@ -839,7 +906,8 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   // global strips at T = 16 run two CTAs per SM (4 consumer warps each; measured: cfg3 TRSM 12.6 vs
   // 13.7 ms with shared strips, cfg4 51.8 vs 54.5 ms at T = 32, cfg5 324 vs 339 ms); SC_GS2=0 disables
   const char* gs2_env = std::getenv("SC_GS2");
-  if (P.gstrip && P.T == 16 && !(gs2_env && gs2_env[0] == '0')) {  // ring within 1/ctas of an SM
+  if (P.warp_trsm) P.ring_bytes = 0;
+  if (P.gstrip && !P.warp_trsm && P.T == 16 && !(gs2_env && gs2_env[0] == '0')) {  // ring within 1/ctas of an SM
     int64_t maxblk = 16;
     for (auto& C : P.classes)
       for (auto& p : C.panels) {
@@ -860,7 +928,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   int32_t split_rows = 0;
   bool want_split = true;
   if (const char* e = std::getenv("SC_TRSM_SPLIT")) want_split = std::atoi(e) != 0;
-  if (!P.gstrip && want_split && P.T <= 16) {
+  if (!P.gstrip && !P.warp_trsm && want_split && P.T <= 16) {
     TwoCta tc = two_cta(P.T);
     if (const char* e = std::getenv("SC_TRSM_SPLIT_ROWS")) {  // test hook: force the class boundary
       const int32_t r = std::min(tc.rmax, (int32_t)std::atoi(e));
@@ -1011,6 +1079,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   S.x_strip = P.gstrip ? SC_STRIP_GLOBAL : SC_STRIP_SHARED;
   S.trsm_tasks = (int64_t)P.trsm_tasks.size();
   S.trsm_tasks_2cta = P.ntrsm_small;
+  S.trsm_kernel = P.warp_trsm ? SC_TRSM_WARP : SC_TRSM_CTA;
   S.syrk_tasks = (int64_t)P.syrk_tasks.size();
   S.bytes_X = 8.0 * (double)P.X_doubles;
   // CSR over global multipliers of the (sub, stepped position) contributions, in (sub, a) order

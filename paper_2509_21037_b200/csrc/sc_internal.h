@@ -71,7 +71,20 @@ struct Panel {
   int64_t buf_off;                      // doubles from the subdomain's panel-buffer base
   int64_t csc_begin, csc_end;           // L entries of columns [a, a+kw) in CSC order
   int32_t relaxed, pad;                 // relaxed: merged supernodes (structural zeros inside)
+  int64_t gx_off;                       // warp TRSM: first entry of the panel's fragment gather map
 };
+
+// Warp TRSM (narrow panels, kw <= 32): per panel a gather map from DMMA fragment positions to CSC
+// positions of L (int32 relative to the subdomain's L values, -1 = structural zero), so a warp
+// loads its m8n8k4 A fragments straight from the caller's CSC values (L crosses HBM once):
+//   triangle: 8x8 blocks (I >= K) in the order K = 0.., I = K..kw8-1; per block [lane][s] (s = 0,1)
+//             -> L[a + 8I + g][a + 8K + 4s + t]   (lane = 4g + t)
+//   R rows:   per row block RB of R_p, [lane][s] (s < KS = 2 kw8) -> L[R_p[8RB + g]][a + 4s + t]
+SC_HD inline int64_t warp_tri_block(int K, int I, int kw8) { return (int64_t)(K * kw8 - K * (K - 1) / 2 + (I - K)); }
+SC_HD inline int64_t warp_gx_size(int kw, int nR) {
+  const int kw8 = (kw + 7) / 8, nRB = (nR + 7) / 8;
+  return 64 * (int64_t)(kw8 * (kw8 + 1) / 2) + (int64_t)nRB * 32 * (2 * kw8);
+}
 
 // One RHS column tile of TRSM width T of one pattern class: stepped columns [col0, col0+width)
 // (P:473-480 RHS splitting at tile granularity).  Its X strip holds the rows of the panels of
@@ -155,6 +168,7 @@ struct ClassPlan {
   std::vector<double> ib_val;
   std::vector<Pair> pairs;
   std::vector<Seg> segs;
+  std::vector<int32_t> gidx;       // warp TRSM fragment gather maps (Panel::gx_off, class-local)
   int64_t x_doubles = 0;           // X region (group strips) per subdomain
   int64_t pb_doubles = 0;          // panel buffer per subdomain
   int32_t max_strip_rows = 0;      // over TRSM tiles
@@ -213,7 +227,8 @@ struct DevPlan {
   double* F;
   double* PB;                      // panel buffers
   double* part;
-  unsigned long long* err;         // sticky device error: ((sub+1) << 32) | col
+  unsigned long long* err;         // sticky device error: [0] = ((sub+1) << 32) | col, [1+sub] = col+1
+  const int32_t* gidx;             // warp TRSM gather maps (all classes; Panel::gx_off is global)
   int32_t nsub, max_n, T, G;
   int32_t factor_ready;            // (host-side bookkeeping mirrors Plan::factor_ready)
   int32_t wmode;                         // 1: chunks hold W_p = L[R_p,p] inv(L_pp) (W mode), 0: L (Y mode)
@@ -226,6 +241,8 @@ struct Plan {
   int32_t gs2 = 0;                 // global strips at T = 16 with this many CTAs per SM (2; 3 via SC_GS2=3)
   bool factor_ready = false;       // panel buffers hold the factor of the last prepare / assemble
   bool wmode = true;               // TRSM update operand W_p = L[R_p,p] inv(L_pp) (wide panels) or L (Y mode)
+  bool warp_trsm = false;          // fused warp-per-tile TRSM straight from the CSC values (no prep)
+  int32_t warp_ctas = 4;           // warps (tiles) per CTA of the warp TRSM
   int32_t nsub = 0;
   std::vector<ClassPlan> classes;
   std::vector<int32_t> sub_cls;

@@ -19,6 +19,7 @@ LIB_PATH = os.environ.get("SC_B200_LIB") or os.path.join(HERE, "libsc_b200.so")
 SC_OK, SC_ERR_INVALID_ARG, SC_ERR_PATTERN, SC_ERR_ZERO_PIVOT, SC_ERR_OOM, SC_ERR_CUDA, SC_ERR_STATE = range(7)
 SKIP_NONE, SKIP_ENVELOPE, SKIP_EXACT = 0, 1, 2
 STRIP_AUTO, STRIP_SHARED, STRIP_GLOBAL = 0, 1, 2
+TRSM_AUTO, TRSM_CTA, TRSM_WARP = 0, 1, 2
 _STATUS = {0: "SC_OK", 1: "SC_ERR_INVALID_ARG", 2: "SC_ERR_PATTERN", 3: "SC_ERR_ZERO_PIVOT", 4: "SC_ERR_OOM",
            5: "SC_ERR_CUDA", 6: "SC_ERR_STATE"}
 
@@ -39,7 +40,7 @@ class SubdomainDesc(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("precision", ctypes.c_int32), ("skip", ctypes.c_int32), ("tile_cols", ctypes.c_int32),
                 ("panel_cols", ctypes.c_int32), ("n_lambda_global", ctypes.c_int64), ("device", ctypes.c_int32),
-                ("x_strip", ctypes.c_int32), ("reserved", ctypes.c_int32 * 6)]
+                ("x_strip", ctypes.c_int32), ("trsm_kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 5)]
 
 
 class Stats(ctypes.Structure):
@@ -52,7 +53,7 @@ class Stats(ctypes.Structure):
                                                "flops_syrk_executed", "bytes_L_values", "bytes_F_lower", "bytes_X",
                                                "device_bytes", "bytes_apply", "bytes_panels")] + \
                [("panels", ctypes.c_int64), ("group_cols", ctypes.c_int32), ("x_strip", ctypes.c_int32),
-                ("trsm_tasks_2cta", ctypes.c_int64)]
+                ("trsm_tasks_2cta", ctypes.c_int64), ("trsm_kernel", ctypes.c_int32), ("pad0", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -131,7 +132,8 @@ class SCPlan:
     Bt_colptr, Bt_rowidx, Bt_values, lambda_map (numpy arrays, e.g. synth.Subdomain)."""
 
     def __init__(self, subdomains: Sequence, *, n_lambda: int = 0, skip: int = SKIP_EXACT, tile_cols: int = 0,
-                 panel_cols: int = 0, device: int = 0, x_strip: int = STRIP_AUTO):
+                 panel_cols: int = 0, device: int = 0, x_strip: int = STRIP_AUTO,
+                 trsm_kernel: int = TRSM_AUTO):
         L = lib()
         keep: List[np.ndarray] = []
 
@@ -162,6 +164,7 @@ class SCPlan:
         opt = Options()
         L.sc_options_default(ctypes.byref(opt))
         opt.skip, opt.tile_cols, opt.panel_cols, opt.x_strip = skip, tile_cols, panel_cols, x_strip
+        opt.trsm_kernel = trsm_kernel
         opt.n_lambda_global, opt.device = int(n_lambda), int(device)
         self.device = device
         self.n_lambda = int(n_lambda)

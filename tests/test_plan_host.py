@@ -185,7 +185,8 @@ def test_global_strip_plan_same_reach_and_work():
     P = config_problem("t3e")
     subs = P.subdomains[:6]
     a = SCPlan(subs, n_lambda=P.n_lambda, tile_cols=16, x_strip=scmod.STRIP_SHARED, device=-1)
-    b = SCPlan(subs, n_lambda=P.n_lambda, tile_cols=16, x_strip=scmod.STRIP_GLOBAL, device=-1)
+    b = SCPlan(subs, n_lambda=P.n_lambda, tile_cols=16, x_strip=scmod.STRIP_GLOBAL, device=-1,
+               trsm_kernel=scmod.TRSM_CTA)
     sa, sb = a.stats(), b.stats()
     assert sa["x_strip"] == scmod.STRIP_SHARED and sb["x_strip"] == scmod.STRIP_GLOBAL
     for k in ("flops_trsm_useful", "flops_syrk_useful", "flops_trsm_executed", "flops_syrk_executed", "bytes_X",
@@ -231,17 +232,18 @@ def test_empty_subdomain_and_empty_columns():
 
 
 def test_auto_tile_and_strip_selection_defaults():
-    """The planner's measured defaults: 2D cfg2 -> T=16 shared strips, all tiles in the
-    two-CTAs-per-SM class, 32-wide panels; 3D (cfg3, cfg4) -> T=16 global strips at two CTAs per SM,
+    """The planner's measured defaults: 2D cfg2 -> warp TRSM at T=16 in the global
+    strips, 32-wide panels; 3D (cfg3, cfg4) -> CTA TRSM at T=16 global strips at two CTAs per SM,
     64-wide panels."""
     from synth import make_problem
-    cases = [(dict(dim=2, physics="heat", S=32, E=64), 16, scmod.STRIP_SHARED, "all", 32),
-             (dict(dim=3, physics="heat", S=8, E=16), 16, scmod.STRIP_GLOBAL, "none", 64),
-             (dict(dim=3, physics="elasticity", S=8, E=12), 16, scmod.STRIP_GLOBAL, "none", 64)]
-    for spec, T, strip, two_cta, pw in cases:
+    cases = [(dict(dim=2, physics="heat", S=32, E=64), 16, scmod.STRIP_GLOBAL, "none", 32, scmod.TRSM_WARP),
+             (dict(dim=3, physics="heat", S=8, E=16), 16, scmod.STRIP_GLOBAL, "none", 64, scmod.TRSM_CTA),
+             (dict(dim=3, physics="elasticity", S=8, E=12), 16, scmod.STRIP_GLOBAL, "none", 64, scmod.TRSM_CTA)]
+    for spec, T, strip, two_cta, pw, kern in cases:
         P = make_problem(subdomains=[0, 5, spec["S"] ** spec["dim"] // 2], **spec)
         st = SCPlan(P.subdomains, n_lambda=P.n_lambda, device=-1).stats()
         assert st["tile_cols"] == T and st["x_strip"] == strip and st["panel_cols"] == pw, (spec, st["tile_cols"])
+        assert st["trsm_kernel"] == kern
         if two_cta == "all":
             assert st["trsm_tasks_2cta"] == st["trsm_tasks"] > 0
         else:
