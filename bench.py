@@ -5,9 +5,10 @@
 
 One step = one sc_assemble_batch over the config's whole batch of subdomains (X init + stepped
 supernodal TRSM + block-sparse SYRK), with the L values resident in HBM.  Multi-GPU (torchrun):
-one process per GPU, each rank assembles its own cluster of subdomains (weak scaling, P:276-283:
-"each process handles a single cluster"); no collective on the assembly path; time = max over
-ranks of the CUDA-event time.  `--impl reference` times the CPU oracle (oracle/) on the host cores
+one process per GPU; by default the config's ONE batch is partitioned over the ranks by LPT on the
+planner's per-subdomain cost (strong scaling, BASELINE cfg3 "512 subdomains sharded
+over 1/2/4/8"); `--weak` gives every rank its own replica batch instead.  No collective
+on the assembly path; time = max over ranks of the CUDA-event time.  `--impl reference` times the CPU oracle (oracle/) on the host cores
 on a bounded sample of the same workload (rank 0 only).  Prints ONE JSON line on rank 0.
 """
 from __future__ import annotations
@@ -126,6 +127,16 @@ def dist_setup(args):
     return world, rank, local
 
 
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_oracle_sample(problem, budget_s: float, threads: int):
     """Oracle (as it stands) over subdomains of the workload, one subdomain per host thread, until
     `budget_s` elapses; returns (subdomains/s, subdomains done, wall seconds)."""
@@ -167,9 +178,130 @@ def run_reference(args, world, rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": CFG_DESC[args.config], "subdomains": len(P.subdomains)},
             "cpu_baseline": {"value": value, "unit": "subdomains/s", "cores": threads, "kind": "oracle",
-                             "sample": sample},
+                             "cpu_model": cpu_model(), "sample": sample},
             "e2e": {"value": value, "unit": "subdomains/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def setup_problem(args, cfg, world, rank):
+    """This rank's subdomains: its LPT share of the config's batch (default) or a replica (--weak)."""
+    from paper_2509_21037_b200 import SCPlan
+    from synth import config_problem
+    from synth.mesh import CONFIGS, make_problem
+    if args.weak or world == 1:
+        return config_problem(cfg, seed=rank if args.weak else 0), None
+    from paper_2509_21037_b200.shard import imbalance, lpt_partition
+    Pall = config_problem(cfg)
+    costs = SCPlan(Pall.subdomains, n_lambda=Pall.n_lambda, device=-1).subdomain_costs()
+    parts = lpt_partition(costs, world)
+    P = make_problem(name=cfg, subdomains=parts[rank], **CONFIGS[cfg])
+    info = {"nsub_total": len(Pall.subdomains), "imbalance": imbalance(costs, parts),
+            "partition": "LPT on the planner's executed-flop cost", "nsub_per_rank": [len(p) for p in parts]}
+    return P, info
+
+
+def time_assembly(plan, Ls, steps, warmup, world, clock_index=None):
+    """W untimed + K timed sc_assemble_batch calls; CUDA events on the launching stream (per phase
+    inside the call); barrier + synchronize on both sides; returns (ms_total, phase ms, clocks)."""
+    import torch
+    import torch.distributed as dist
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        plan.assemble(Ls)
+    torch.cuda.synchronize()
+    plan.check()
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
+    for row in evs:  # torch creates the CUDA event lazily on first record
+        for e in row:
+            e.record(stream)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(clock_index if clock_index is not None else torch.cuda.current_device()) as clk:
+        start.record(stream)
+        for k in range(steps):
+            plan.set_timing_events(evs[k])
+            plan.assemble(Ls)
+        stop.record(stream)
+        torch.cuda.synchronize()
+    plan.set_timing_events(None)
+    if world > 1:
+        dist.barrier()
+    plan.check()
+    phases = {"prep": sum(e[0].elapsed_time(e[1]) for e in evs) / steps,
+              "trsm": sum(e[1].elapsed_time(e[2]) for e in evs) / steps,
+              "syrk": sum(e[2].elapsed_time(e[3]) for e in evs) / steps}
+    return start.elapsed_time(stop), phases, clk.summary()
+
+
+def roofline_for(st, phases, ms_step, peaks, cfg):
+    """Dominant kernel of the step vs the roof its algorithmic intensity selects:
+       prep: bytes = L values read once;
+       trsm: flops = useful (etree-exact) TRSM flops, bytes = L values read once + X tile-exact
+             written once (SURVEY §8.1 a2; sc_stats.bytes_X_reach);
+       syrk: flops = useful SYRK flops, bytes = X strips read once + F lower written once."""
+    dom = max(phases, key=phases.get)
+    dom_ms = phases[dom]
+    prof_traffic = None
+    tp = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
+    if os.path.exists(tp):
+        prof_traffic = json.load(open(tp)).get(dom)
+    warp = st.get("trsm_kernel") == 2
+    kernel_names = {"prep": "prep_panel_kernel + prep_small_kernel",
+                    "trsm": (f"trsm_warp_kernel<{st['tile_cols'] // 8}>" if warp else f"trsm_smem_kernel<{st['tile_cols']}>"),
+                    "syrk": f"syrk_pair_kernel<{st['group_cols']}>"}
+    alg = {"prep": (0.0, st["bytes_L_values"]),
+           "trsm": (st["flops_trsm_useful"], st["bytes_L_values"] + st["bytes_X_reach"]),
+           "syrk": (st["flops_syrk_useful"], st["bytes_X"] + st["bytes_F_lower"])}
+    flops, nbytes = alg[dom]
+    ridge = peaks["fp64_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    intensity = flops / nbytes if nbytes else float("inf")
+    if intensity < ridge:
+        achieved = nbytes / (dom_ms / 1e3) / 1e9
+        r = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+             "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks.get("hbm_source", "MEASURED_PEAKS.json hbm_gbs")}
+    else:
+        achieved = flops / (dom_ms / 1e3) / 1e12
+        r = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
+             "frac": achieved / peaks["fp64_tflops"], "dtype": "f64 (DMMA m8n8k4)",
+             "peak_source": peaks["fp64_tflops_source"]}
+    r.update({"algorithmic": {"prep": "L values read once (8 B/nnz(L))",
+                              "trsm": "useful TRSM flops; L values read once + X tile-exact written once",
+                              "syrk": "useful SYRK flops; X strips read once + F lower written once"}[dom],
+              "algorithmic_flops": flops, "algorithmic_bytes": nbytes, "intensity_flop_per_byte": intensity,
+              "ridge_flop_per_byte": ridge, "traffic": prof_traffic, "kernel": kernel_names[dom],
+              "share_of_step": dom_ms / ms_step, "launch_ms": dom_ms})
+    return r
+
+
+def per_config_lines(args, peaks):
+    """Extra configs timed in the same run (N=1): phase times, throughput and roofline of each, so
+    the FP64-bound 3D evidence is measured on the driver's box too."""
+    import torch
+    from paper_2509_21037_b200 import SCPlan
+    from synth import config_problem
+    out = {}
+    for cfg in [c for c in args.per_config.split(",") if c and c != args.config]:
+        P = config_problem(cfg)
+        t0 = time.perf_counter()
+        plan = SCPlan(P.subdomains, n_lambda=P.n_lambda, device=torch.cuda.current_device())
+        t_plan = time.perf_counter() - t0
+        st = plan.stats()
+        Ls = [torch.from_numpy(np.ascontiguousarray(sd.L_values)).cuda() for sd in P.subdomains]
+        steps = max(2, min(args.steps, 5))
+        ms_total, phases, clocks = time_assembly(plan, Ls, steps, 3, 1)
+        ms_step = ms_total / steps
+        useful = st["flops_trsm_useful"] + st["flops_syrk_useful"]
+        out[cfg] = {"workload": CFG_DESC[cfg], "subdomains": len(P.subdomains), "steps": steps, "warmup": 3,
+                    "value": len(P.subdomains) / (ms_step / 1e3), "unit": "subdomains/s", "ms_per_step": ms_step,
+                    "phase_ms": phases, "gflops_useful": useful / (ms_step / 1e3) / 1e9,
+                    "fp64_frac_useful": useful / (ms_step / 1e3) / 1e12 / peaks["fp64_tflops"],
+                    "roofline": roofline_for(st, phases, ms_step, peaks, cfg), "clocks": clocks, "plan_s": t_plan,
+                    "tile_cols": st["tile_cols"], "trsm_kernel": {1: "cta", 2: "warp"}.get(st["trsm_kernel"])}
+        del Ls, plan
+        torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -182,11 +314,15 @@ def main():
     ap.add_argument("--skip", default="exact", choices=["none", "envelope", "exact"])
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--panel", type=int, default=0)
-    ap.add_argument("--shard", action="store_true",
-                    help="strong scaling: the config's batch is LPT-partitioned over the ranks by the "
-                         "planner's per-subdomain cost (default: every rank assembles its own batch)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak scaling: every rank assembles its own replica batch of the config (default: the "
+                         "config's one batch is LPT-partitioned over the ranks by the planner's cost)")
+    ap.add_argument("--shard", action="store_true", help="(default; kept for compatibility)")
     ap.add_argument("--strip", default="auto", choices=["auto", "shared", "global"],
                     help="where TRSM tiles keep their X strip (sc_options.x_strip)")
+    ap.add_argument("--trsm", default="auto", choices=["auto", "cta", "warp"], help="sc_options.trsm_kernel")
+    ap.add_argument("--per-config", default="cfg3,cfg4",
+                    help="extra configs timed in the same run (N=1 only), reported under per_config")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
     ap.add_argument("--ref-budget", type=float, default=8.0, help="seconds of oracle work per reference step")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -202,7 +338,6 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_2509_21037_b200 import SCPlan
-    from synth import config_problem
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the product path has no CPU fallback)")
@@ -211,25 +346,12 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = load_peaks()
 
-    # each rank: its own cluster (replica of the config batch with its own coefficients), or with
-    # --shard its LPT share of one batch (partition by plan cost, no collective)
     t_plan0 = time.perf_counter()
-    shard_info = None
-    if args.shard:
-        from paper_2509_21037_b200.shard import imbalance, lpt_partition
-        from synth.mesh import CONFIGS, make_problem
-        Pall = config_problem(args.config)
-        costs = SCPlan(Pall.subdomains, n_lambda=Pall.n_lambda, device=-1).subdomain_costs()
-        parts = lpt_partition(costs, world)
-        P = make_problem(name=args.config, subdomains=parts[rank], **CONFIGS[args.config])
-        shard_info = {"nsub_total": len(Pall.subdomains), "imbalance": imbalance(costs, parts),
-                      "partition": "LPT on executed-flop cost"}
-        del Pall
-    else:
-        P = config_problem(args.config, seed=rank)
+    P, shard_info = setup_problem(args, args.config, world, rank)
     skip = {"none": 0, "envelope": 1, "exact": 2}[args.skip]
     plan = SCPlan(P.subdomains, n_lambda=P.n_lambda, skip=skip, tile_cols=args.tile, panel_cols=args.panel,
-                  device=local, x_strip={"auto": 0, "shared": 1, "global": 2}[args.strip])
+                  device=local, x_strip={"auto": 0, "shared": 1, "global": 2}[args.strip],
+                  trsm_kernel={"auto": 0, "cta": 1, "warp": 2}[args.trsm])
     t_plan = time.perf_counter() - t_plan0
     st = plan.stats()
     Ls = [torch.from_numpy(np.ascontiguousarray(sd.L_values)).cuda() for sd in P.subdomains]
@@ -237,42 +359,17 @@ def main():
     stream = torch.cuda.current_stream()
     useful = st["flops_trsm_useful"] + st["flops_syrk_useful"]
 
-    # warm-up
-    for _ in range(args.warmup):
-        plan.assemble(Ls)
-    torch.cuda.synchronize()
-    plan.check()
-
-    # timed region: K steps, per-kernel events recorded inside sc_assemble_batch on `stream`
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-    for row in evs:  # torch creates the CUDA event lazily on first record
-        for e in row:
-            e.record(stream)
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        start.record(stream)
-        for k in range(args.steps):
-            plan.set_timing_events(evs[k])
-            plan.assemble(Ls)
-        stop.record(stream)
-        torch.cuda.synchronize()
-    plan.set_timing_events(None)
-    if world > 1:
-        dist.barrier()
-    ms_total = start.elapsed_time(stop)
-    ms_prep = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    ms_trsm = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    ms_syrk = sum(e[2].elapsed_time(e[3]) for e in evs) / args.steps
-    plan.check()
+    ms_total, phases, clocks = time_assembly(plan, Ls, args.steps, args.warmup, world, local)
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
+    per_rank_ms = [ms_total / args.steps]
     if world > 1:
+        allt = [torch.zeros(1, dtype=torch.float64, device="cuda") for _ in range(world)]
+        dist.all_gather(allt, t)
+        per_rank_ms = [float(x.item()) / args.steps for x in allt]
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_step = t.item() / args.steps
     nsub_job = shard_info["nsub_total"] if shard_info else world * nsub
-    # job-wide flops: summed over ranks (each rank's batch differs under --shard)
+    # job-wide flops: summed over ranks (each rank's batch differs when sharded)
     fl = torch.tensor([useful, st["flops_trsm_executed"] + st["flops_syrk_executed"]], dtype=torch.float64,
                       device="cuda")
     if world > 1:
@@ -281,11 +378,11 @@ def main():
     value = nsub_job / (ms_step / 1e3)
 
     # e2e through the public API with HOST inputs: pinned L values -> H2D inside the call ->
-    # assemble -> one explicit apply q = F lambda (solution stage) -> D2H of q
+    # assemble -> one explicit apply q = F lambda (solution stage, NCCL all-reduce for N > 1) -> D2H of q
     e2e = None
     if not args.no_e2e:
         hostL = [torch.from_numpy(np.ascontiguousarray(sd.L_values)).pin_memory() for sd in P.subdomains]
-        lam_h = torch.from_numpy(np.random.default_rng(rank).standard_normal(P.n_lambda)).pin_memory()
+        lam_h = torch.from_numpy(np.random.default_rng(0).standard_normal(P.n_lambda)).pin_memory()
         lam_d = torch.empty(P.n_lambda, dtype=torch.float64, device="cuda")
         q_d = torch.empty_like(lam_d)
         q_h = torch.empty(P.n_lambda, dtype=torch.float64).pin_memory()
@@ -312,55 +409,19 @@ def main():
         h2d = int(sum(8 * sd.L_values.size for sd in P.subdomains) + 8 * P.n_lambda)
         e2e = {"value": nsub_job / (te.item() / 1e3), "unit": "subdomains/s", "ms_per_step": te.item(),
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * P.n_lambda,
-               "includes": "pinned H2D of all L values + assemble + 1 sc_apply (+all-reduce) + D2H of q"}
+               "includes": "pinned H2D of this rank's L values + assemble + 1 sc_apply (+NCCL all-reduce) + D2H of q"}
 
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
         return
 
-    # roofline of the dominant kernel.  Algorithmic work per phase, per launch:
-    #   prep: bytes = L values read once;
-    #   trsm: flops = useful (etree-exact) TRSM flops, bytes = L values read once + X strips written once;
-    #   syrk: flops = useful SYRK flops, bytes = X strips read once + F lower written once.
-    # The binding roof is the one the algorithmic intensity (flops/byte) selects against the ridge
-    # point peak_fp64 / peak_hbm: below it the kernel is reported against HBM (GB/s), above it
-    # against the FP64 tensor (DMMA) peak.
-    phases = {"prep": ms_prep, "trsm": ms_trsm, "syrk": ms_syrk}
-    dom = max(phases, key=phases.get)
-    dom_ms = phases[dom]
-    prof_traffic = None
-    tp = os.path.join(ROOT, "profiles", f"traffic_{args.config}.json")
-    if os.path.exists(tp):
-        prof_traffic = json.load(open(tp)).get(dom)
-    kernel_names = {"prep": "prep_panel_kernel + prep_small_kernel", "trsm": f"trsm_smem_kernel<{st['tile_cols']}>",
-                    "syrk": f"syrk_pair_kernel<{st['group_cols']}>"}
-    alg = {"prep": (0.0, st["bytes_L_values"]),
-           "trsm": (st["flops_trsm_useful"], st["bytes_L_values"] + st["bytes_X"]),
-           "syrk": (st["flops_syrk_useful"], st["bytes_X"] + st["bytes_F_lower"])}
-    flops, nbytes = alg[dom]
-    ridge = peaks["fp64_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
-    intensity = flops / nbytes if nbytes else float("inf")
-    if intensity < ridge:
-        achieved = nbytes / (dom_ms / 1e3) / 1e9
-        roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": achieved / peaks["hbm_gbs"], "peak_source": peaks.get("hbm_source", "MEASURED_PEAKS.json hbm_gbs")}
-    else:
-        achieved = flops / (dom_ms / 1e3) / 1e12
-        roofline = {"bound": "tensor", "achieved": achieved, "peak": peaks["fp64_tflops"], "unit": "TFLOP/s",
-                    "frac": achieved / peaks["fp64_tflops"], "dtype": "f64 (DMMA m8n8k4)",
-                    "peak_source": peaks["fp64_tflops_source"]}
-    roofline.update({"algorithmic": {"prep": "L values read once (8 B/nnz(L))",
-                                     "trsm": "useful TRSM flops; L values read once + X strips written once",
-                                     "syrk": "useful SYRK flops; X strips read once + F lower written once"}[dom],
-                     "algorithmic_flops": flops, "algorithmic_bytes": nbytes, "intensity_flop_per_byte": intensity,
-                     "ridge_flop_per_byte": ridge})
-    roofline.update({"traffic": prof_traffic, "kernel": kernel_names[dom], "share_of_step": dom_ms / ms_step})
+    roofline = roofline_for(st, phases, ms_step * world / world, peaks, args.config)
     # amortization point: explicit GPU (assembly + apply per
     # iteration) vs implicit CPU apply per iteration on the host cores; the factorization is common
     # to both and cancels.  k* = smallest k with t_asm + k t_expl < k t_impl.
     amort = None
-    if not args.no_amortization:
+    if not args.no_amortization and world == 1:
         lam_d = torch.from_numpy(np.random.default_rng(7).standard_normal(P.n_lambda)).cuda()
         q_d = torch.empty_like(lam_d)
         for _ in range(3):
@@ -374,8 +435,16 @@ def main():
         a1.record(stream)
         torch.cuda.synchronize()
         t_expl = a0.elapsed_time(a1) / reps
-        # GPU implicit apply (two substitutions per subdomain with the staged factor, no F)
+        # GPU implicit apply (two substitutions per subdomain with the staged factor, no F);
+        # its up-front cost is the factor staging (sc_prepare_factor), timed here
+        for _ in range(2):
+            plan.prepare_factor(Ls)
+        torch.cuda.synchronize()
+        a0.record(stream)
         plan.prepare_factor(Ls)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        t_stage = a0.elapsed_time(a1)
         for _ in range(3):
             plan.apply_implicit(lam_d, q_d)
         torch.cuda.synchronize()
@@ -394,15 +463,13 @@ def main():
         q_impl = ic.apply(lam_d.cpu().numpy())
         agree = float(np.linalg.norm(q_d.cpu().numpy() - q_impl) / np.linalg.norm(q_impl))
 
-        def kstar(t_asm):
-            d = t_impl - t_expl
-            return int(t_asm // d) + 1 if d > 0 else None
+        def kstar(t_asm, t_imp, t_up=0.0):
+            d = t_imp - t_expl
+            return int(max(t_asm - t_up, 0.0) // d) + 1 if d > 0 else None
 
-        # vs GPU implicit: the implicit method pays only the factor staging (prep) up front
-        d_gpu = t_impl_gpu - t_expl
-        k_gpu = int((ms_step - ms_prep) // d_gpu) + 1 if d_gpu > 0 else None
-        amort = {"iters": kstar(ms_step), "iters_e2e": kstar(e2e["ms_per_step"]) if e2e else None,
-                 "iters_vs_gpu_implicit": k_gpu, "t_apply_implicit_gpu_ms": t_impl_gpu,
+        amort = {"iters": kstar(ms_step, t_impl), "iters_e2e": kstar(e2e["ms_per_step"], t_impl) if e2e else None,
+                 "iters_vs_gpu_implicit": kstar(ms_step, t_impl_gpu, t_stage), "t_apply_implicit_gpu_ms": t_impl_gpu,
+                 "t_factor_staging_gpu_ms": t_stage,
                  "implicit_gpu_vs_explicit_rel_diff": float(np.linalg.norm(q_impl_gpu - q_d.cpu().numpy()) /
                                                             np.linalg.norm(q_d.cpu().numpy())),
                  "t_assembly_ms": ms_step, "t_apply_explicit_gpu_ms": t_expl, "t_apply_implicit_cpu_ms": t_impl,
@@ -412,29 +479,32 @@ def main():
     if not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
         v, done, wall = cpu_oracle_sample(P, args.cpu_budget, threads)
-        cpu = {"value": v, "unit": "subdomains/s", "cores": threads, "kind": "oracle",
+        cpu = {"value": v, "unit": "subdomains/s", "cores": threads, "kind": "oracle", "cpu_model": cpu_model(),
                "sample": f"{done} subdomains of {args.config} ({wall:.1f}s, one subdomain per host thread)"}
-    clocks = clk.summary()
+    per_config = per_config_lines(args, peaks) if world == 1 and args.per_config else None
     line = {
         "metric": METRIC, "value": value, "unit": "subdomains/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
-        "scaling": "strong" if shard_info else "weak",
+        "scaling": "weak" if (args.weak and world > 1) else "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": CFG_DESC[args.config], "name": args.config, "subdomains_per_gpu": nsub,
                    "skip": args.skip, "tile_cols": st["tile_cols"], "panel_cols": st["panel_cols"],
+                   "trsm_kernel": {1: "cta", 2: "warp"}.get(st["trsm_kernel"]),
                    "x_strip": {1: "shared", 2: "global"}.get(st["x_strip"], "?"),
                    "trsm_tasks_2cta": st["trsm_tasks_2cta"],
-                   "parallelism": f"subdomain-sharded x{world} (no collective in assembly)",
-                   "shard": shard_info,
+                   "parallelism": (f"replica batch per rank x{world}" if (args.weak and world > 1) else
+                                   f"one batch LPT-sharded over {world} rank(s), no collective in assembly"),
+                   "shard": shard_info, "nccl_ranks": world, "per_rank_ms": per_rank_ms,
+                   "rank_imbalance_measured": max(per_rank_ms) / (sum(per_rank_ms) / len(per_rank_ms)),
                    "l2": f"inputs larger than L2: L values {st['bytes_L_values'] / 1e9:.2f} GB, "
                          f"X {st['bytes_X'] / 1e9:.2f} GB, F {8 * sum(m * m for m in plan.m) / 1e9:.2f} GB per GPU"},
         "gflops_useful": useful_job / (ms_step / 1e3) / 1e9,
         "gflops_executed": executed_job / (ms_step / 1e3) / 1e9,
         "fp64_frac_useful": useful_job / world / (ms_step / 1e3) / 1e12 / peaks["fp64_tflops"],
-        "phase_ms": {"prep": ms_prep, "trsm": ms_trsm, "syrk": ms_syrk},
+        "phase_ms": phases,
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "amortization": amort,
         "gpu_launches": args.steps * plan.launches_per_assemble,
-        "clocks": clocks, "plan_s": t_plan,
+        "clocks": clocks, "plan_s": t_plan, "per_config": per_config,
         "paper_context": {"a100_sep_opt_ms_per_subdomain": PAPER_A100_MS.get(args.config),
                           "note": "PAPER.md Fig. 8, A100, triangles/tets; context only"},
     }

@@ -123,6 +123,9 @@ typedef struct {
   int64_t trsm_tasks_2cta;   /* TRSM tiles in the small-strip class (own launch, two CTAs per SM)   */
   int32_t trsm_kernel;       /* SC_TRSM_CTA or SC_TRSM_WARP: the TRSM kernel the plan chose         */
   int32_t pad0;
+  double bytes_X_reach;      /* X tile-exact: sum over RHS tiles of (rows of the panels in the tile's
+                                own reach) x T x 8 B (SURVEY §8.1 a2 "tile-exact"); the TRSM's
+                                algorithmic X bytes                                                   */
 } sc_stats;
 
 /* Fill `opt` with defaults: precision 64, skip EXACT, tile/panel auto, device 0. */

@@ -494,6 +494,7 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
         in_tile[(size_t)p] = J;
         C.steps.push_back({p, strip_base[(size_t)p], C.greach[q].off, 0, 0});
         const Panel& P = C.panels[(size_t)p];
+        C.x_reach_doubles += (double)P.kw * T;
         if (warp) {  // 8x8 triangle blocks (I >= K) + 8-row blocks of R_p, k padded to 8
           const double kw8 = (P.kw + 7) / 8, nRB = (P.nR + 7) / 8;
           C.fl_trsm_exec += 2.0 * T * (32.0 * kw8 * (kw8 + 1) + 64.0 * nRB * kw8);
@@ -1066,6 +1067,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     S.syrk_segments += (int64_t)C.segs.size();
     S.bytes_apply += 8.0 * (double)C.m * (C.m + 1) / 2.0 + 8.0 * 3.0 * C.m;
     S.bytes_panels += 8.0 * (double)C.pb_doubles;
+    S.bytes_X_reach += 8.0 * C.x_reach_doubles;
     S.panels += (int64_t)C.panels.size();
   }
   P.ntrsm_small = (int32_t)trsm_small.size();

@@ -177,6 +177,7 @@ struct ClassPlan {
   double fl_trsm_useful = 0, fl_syrk_useful = 0, fl_trsm_env = 0, fl_syrk_env = 0;
   double fl_trsm_dense = 0, fl_syrk_dense = 0, fl_trsm_sparse = 0;
   double fl_trsm_exec = 0, fl_syrk_exec = 0, fl_prep_exec = 0;
+  double x_reach_doubles = 0;      // sum over tiles of own-reach rows x T
 };
 
 // Per-launch parameters of the TRSM kernel: first task, L-block ring bytes and shared strip capacity

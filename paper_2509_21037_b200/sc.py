@@ -53,7 +53,8 @@ class Stats(ctypes.Structure):
                                                "flops_syrk_executed", "bytes_L_values", "bytes_F_lower", "bytes_X",
                                                "device_bytes", "bytes_apply", "bytes_panels")] + \
                [("panels", ctypes.c_int64), ("group_cols", ctypes.c_int32), ("x_strip", ctypes.c_int32),
-                ("trsm_tasks_2cta", ctypes.c_int64), ("trsm_kernel", ctypes.c_int32), ("pad0", ctypes.c_int32)]
+                ("trsm_tasks_2cta", ctypes.c_int64), ("trsm_kernel", ctypes.c_int32), ("pad0", ctypes.c_int32),
+                ("bytes_X_reach", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
