@@ -282,7 +282,7 @@ def per_config_lines(args, peaks):
     from paper_2509_21037_b200 import SCPlan
     from synth import config_problem
     out = {}
-    for cfg in [c for c in args.per_config.split(",") if c and c != args.config]:
+    for cfg in [c for c in args.per_config.split(",") if c in CFG_DESC and c != args.config]:
         P = config_problem(cfg)
         t0 = time.perf_counter()
         plan = SCPlan(P.subdomains, n_lambda=P.n_lambda, device=torch.cuda.current_device())
@@ -497,7 +497,8 @@ def main():
                    "shard": shard_info, "nccl_ranks": world, "per_rank_ms": per_rank_ms,
                    "rank_imbalance_measured": max(per_rank_ms) / (sum(per_rank_ms) / len(per_rank_ms)),
                    "l2": f"inputs larger than L2: L values {st['bytes_L_values'] / 1e9:.2f} GB, "
-                         f"X {st['bytes_X'] / 1e9:.2f} GB, F {8 * sum(m * m for m in plan.m) / 1e9:.2f} GB per GPU"},
+                         f"X {st['bytes_X'] / 1e9:.2f} GB, F lower tiles "
+                         f"{8 * 4096 * sum(((m + 63) // 64) * ((m + 63) // 64 + 1) // 2 for m in plan.m) / 1e9:.2f} GB per GPU"},
         "gflops_useful": useful_job / (ms_step / 1e3) / 1e9,
         "gflops_executed": executed_job / (ms_step / 1e3) / 1e9,
         "fp64_frac_useful": useful_job / world / (ms_step / 1e3) / 1e12 / peaks["fp64_tflops"],

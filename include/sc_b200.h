@@ -77,7 +77,12 @@ enum { SC_SKIP_NONE = 0,      /* no B~ sparsity: every column solved from row 0 
 enum { SC_STRIP_AUTO = 0, SC_STRIP_SHARED = 1, SC_STRIP_GLOBAL = 2 };
 
 typedef struct {
-  int32_t precision;         /* 64 (FP64).  Other values -> SC_ERR_INVALID_ARG in this version     */
+  int32_t precision;         /* 64: L values, X and F' in FP64.  32 (optional FP32 mode, SURVEY §8.3
+                                reading 1, "assembly-only FP32"): the caller passes FP32 L values
+                                (its FP64 factor rounded), X and F' are stored in FP32, halving
+                                their bytes; the arithmetic stays FP64 DMMA (no FP32 refactoring),
+                                so F agrees with the FP64 oracle to ~1e-7 (bar 1e-4).  sc_get_F /
+                                sc_get_X still return doubles.  Y-mode TRSM only.                   */
   int32_t skip;              /* SC_SKIP_*                                                          */
   int32_t tile_cols;         /* T: RHS column-tile width 8, 16, 32 or 64; 0 = automatic (widest whose
                                 X strip fits in shared memory, 32 or 16; 32 for global strips)       */
@@ -138,10 +143,10 @@ void sc_options_default(sc_options* opt);
 sc_status sc_plan_create(const sc_subdomain_desc* sd, int32_t nsub, const sc_options* opt, sc_plan_t* out);
 
 /* Preprocessing stage: assemble every F_i of the plan from the L values.
-   L_values: HOST array of nsub DEVICE pointers; L_values[i] points to nnz(L_i) doubles in the CSC
-   order of sd[i].L_colptr/L_rowidx.  They must stay valid until the work on `stream` completes.
+   L_values: HOST array of nsub DEVICE pointers; L_values[i] points to nnz(L_i) values in the CSC
+   order of sd[i].L_colptr/L_rowidx: double for precision 64, float for precision 32.  They must stay valid until the work on `stream` completes.
    Enqueues the TRSM and SYRK kernels; does not synchronise. */
-sc_status sc_assemble_batch(sc_plan_t p, const double* const* L_values, void* stream);
+sc_status sc_assemble_batch(sc_plan_t p, const void* const* L_values, void* stream);
 
 /* Same as sc_assemble_batch but the L values live in HOST memory (ideally pinned): the call copies
    them to a plan-owned device staging buffer (host->device inside the call, the paper's "copies
@@ -149,7 +154,7 @@ sc_status sc_assemble_batch(sc_plan_t p, const double* const* L_values, void* st
    to 16 chunks of subdomains; chunk k's copies run on a plan-owned copy stream while the kernels of
    chunk k-1 run on `stream`.  The host arrays must stay valid until `stream` completes.  Does not
    synchronise. */
-sc_status sc_assemble_batch_host(sc_plan_t p, const double* const* L_values_host, void* stream);
+sc_status sc_assemble_batch_host(sc_plan_t p, const void* const* L_values_host, void* stream);
 
 /* Solution stage: q[g] = sum_i sum_{a: lambda_map_i(a) = g} (F_i lambda_i)(a), lambda_i(a) =
    lambda[lambda_map_i(a)]  (eq. dualop_apply_expl per subdomain, summed additively).
@@ -160,12 +165,13 @@ sc_status sc_apply(sc_plan_t p, const double* lambda, double* q, void* stream);
 /* Factor staging only (the prep phase of sc_assemble_batch): the plan's panel buffers receive the
    supernodal factor panels of L (inverted diagonal blocks + pruned row chunks), which is what the
    implicit apply needs; F is not assembled.  Same argument rules as sc_assemble_batch. */
-sc_status sc_prepare_factor(sc_plan_t p, const double* const* L_values, void* stream);
+sc_status sc_prepare_factor(sc_plan_t p, const void* const* L_values, void* stream);
 
 /* Implicit dual-operator application (eq. dualop_apply_impl): q[g] = sum_i
    sum_{a: lambda_map_i(a) = g} (B~_i K_i^{-1} B~_i^T lambda_i)(a), computed WITHOUT F by one forward
    and one backward substitution per subdomain with the factor staged by the last
-   sc_prepare_factor / sc_assemble_batch (SC_ERR_STATE if none).  One CTA per subdomain; its work
+   sc_prepare_factor (or, for CTA-TRSM plans, sc_assemble_batch, which stages it too; the warp TRSM
+   reads L straight from the caller's CSC and stages nothing) -- SC_ERR_STATE if none.  One CTA per subdomain; its work
    vector lives in shared memory when n_i <= 25,600, else in plan-owned global memory.  lambda, q:
    DEVICE arrays of n_lambda_global doubles; q overwritten; deterministic. */
 sc_status sc_apply_implicit(sc_plan_t p, const double* lambda, double* q, void* stream);

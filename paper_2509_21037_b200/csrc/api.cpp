@@ -61,7 +61,7 @@ sc_status sc_plan_create(const sc_subdomain_desc* sd, int32_t nsub, const sc_opt
   return SC_OK;
 }
 
-sc_status sc_assemble_batch(sc_plan_t p, const double* const* L_values, void* stream) {
+sc_status sc_assemble_batch(sc_plan_t p, const void* const* L_values, void* stream) {
   if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
   if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
   if (!L_values && p->P.nsub > 0) return fail(SC_ERR_INVALID_ARG, "NULL L_values");
@@ -70,7 +70,7 @@ sc_status sc_assemble_batch(sc_plan_t p, const double* const* L_values, void* st
   return st == SC_OK ? SC_OK : fail(st, err);
 }
 
-sc_status sc_assemble_batch_host(sc_plan_t p, const double* const* L_values_host, void* stream) {
+sc_status sc_assemble_batch_host(sc_plan_t p, const void* const* L_values_host, void* stream) {
   if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
   if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
   if (!L_values_host && p->P.nsub > 0) return fail(SC_ERR_INVALID_ARG, "NULL L_values_host");
@@ -88,7 +88,7 @@ sc_status sc_apply(sc_plan_t p, const double* lambda, double* q, void* stream) {
   return st == SC_OK ? SC_OK : fail(st, err);
 }
 
-sc_status sc_prepare_factor(sc_plan_t p, const double* const* L_values, void* stream) {
+sc_status sc_prepare_factor(sc_plan_t p, const void* const* L_values, void* stream) {
   if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
   if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
   if (!L_values && p->P.nsub > 0) return fail(SC_ERR_INVALID_ARG, "NULL L_values");
@@ -130,7 +130,7 @@ sc_status sc_get_F(sc_plan_t p, int32_t i, double* F, int64_t ld) {
   for (int64_t b = 0; b < m; b++)
     for (int64_t a = 0; a < m; a++) {
       const int64_t hi = std::max(a, b), lo = std::min(a, b);
-      F[(int64_t)C.sigma[(size_t)b] * ld + C.sigma[(size_t)a]] = Fl[(size_t)(lo * m + hi)];
+      F[(int64_t)C.sigma[(size_t)b] * ld + C.sigma[(size_t)a]] = Fl[(size_t)sc::f_index((int)hi, (int)lo)];
     }
   return SC_OK;
 }

@@ -51,6 +51,28 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
+// ---- stored elements of L / X / F': double, or float in the FP32 mode (FP64 arithmetic) ---------
+__device__ __forceinline__ double ld_el(const void* p, int64_t i, bool f32) {
+  return f32 ? (double)__ldg(static_cast<const float*>(p) + i) : __ldg(static_cast<const double*>(p) + i);
+}
+template <typename ST>
+__device__ __forceinline__ double2 ld2(const ST* p) {
+  if constexpr (sizeof(ST) == 8) {
+    return *reinterpret_cast<const double2*>(p);
+  } else {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    return make_double2(v.x, v.y);
+  }
+}
+template <typename ST>
+__device__ __forceinline__ void st2(ST* p, double2 v) {
+  if constexpr (sizeof(ST) == 8) {
+    *reinterpret_cast<double2*>(p) = v;
+  } else {
+    *reinterpret_cast<float2*>(p) = make_float2((float)v.x, (float)v.y);
+  }
+}
+
 // ---- mbarrier + bulk async copy (TMA, non-tensor form) ------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -110,14 +132,15 @@ template <int U>
 struct ScatterBatch {
   double v[U];
   int32_t d[U];
-  __device__ __forceinline__ void load(const double* __restrict__ Lv, const int32_t* __restrict__ dest, int64_t q0,
+  bool f32 = false;
+  __device__ __forceinline__ void load(const void* __restrict__ Lv, const int32_t* __restrict__ dest, int64_t q0,
                                        int64_t end, int nthr) {
 #pragma unroll
     for (int u = 0; u < U; u++) {
       const int64_t q = q0 + (int64_t)u * nthr;
       d[u] = INT32_MIN;
       if (q < end) {
-        v[u] = __ldg(Lv + q);
+        v[u] = ld_el(Lv, q, f32);
         d[u] = __ldg(dest + q);
       }
     }
@@ -137,7 +160,7 @@ struct ScatterBatch {
   }
 };
 template <int LDD, int U>
-__device__ __forceinline__ void scatter_rest(ScatterBatch<U>& sb, const double* __restrict__ Lv,
+__device__ __forceinline__ void scatter_rest(ScatterBatch<U>& sb, const void* __restrict__ Lv,
                                              const int32_t* __restrict__ dest, double* __restrict__ PB, double* D,
                                              const Panel& pn, int t, int nthr) {
   for (int64_t q0 = pn.csc_begin + t;;) {
@@ -254,7 +277,7 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0)
   const Panel pn = P.panels[task.y];
   const int cls = P.sub_cls[sub];
   const int32_t* __restrict__ dest = P.dest + P.cls_csc_off[cls];
-  const double* __restrict__ Lv = P.Lptr[sub];
+  const void* __restrict__ Lv = P.Lptr[sub];
   double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
   const int kw = pn.kw, kw4 = pn.kw4;
   int npad = 8;  // triangle padded to npad = 8 * 2^k >= kw with a unit diagonal
@@ -264,6 +287,7 @@ __global__ void __launch_bounds__(kThreads) prep_panel_kernel(DevPlan P, int t0)
     for (int q = tid; q < npad * kLdT / 2; q += kThreads) D2[q] = make_double2(0.0, 0.0);
   }
   ScatterBatch<4> sb;
+  sb.f32 = P.fp32;
   sb.load(Lv, dest, pn.csc_begin + tid, pn.csc_end, kThreads);
   // Y mode: every chunk position the scatter does not write (padding, explicit zeros of merged
   // supernodes) is zero since the plan zero-filled the panel buffer and nothing else writes there;
@@ -367,10 +391,11 @@ __global__ void __launch_bounds__(32 * SmallCfg<NPAD>::WARPS) prep_small_kernel(
   const int sub = task.x;
   const Panel pn = P.panels[task.y];
   const int32_t* __restrict__ dest = P.dest + P.cls_csc_off[P.sub_cls[sub]];
-  const double* __restrict__ Lv = P.Lptr[sub];
+  const void* __restrict__ Lv = P.Lptr[sub];
   double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
   const int kw = pn.kw, kw4 = pn.kw4;
   ScatterBatch<SC_PREP_U> sb;
+  sb.f32 = P.fp32;
   sb.load(Lv, dest, pn.csc_begin + lane, pn.csc_end, 32);
   for (int q = lane; q < NPAD * LD / 2; q += 32) reinterpret_cast<double2*>(D)[q] = make_double2(0.0, 0.0);
   if constexpr (WMODE) zero_chunk_gaps(PB, pn, lane, 32);  // (Y mode: zero since plan creation)
@@ -641,9 +666,13 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
   const Tile tile = P.tiles[task.y];
   const double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
   double* Xs;
+  float* Xf = nullptr;  // global strip of an FP32 plan
+  const bool f32 = GS && P.fp32;
   int LDX;
   if constexpr (GS) {
-    Xs = P.X + P.sub_X_base[sub] + P.groups[tile.group].x_off + tile.col_in_group;
+    const int64_t off = P.sub_X_base[sub] + P.groups[tile.group].x_off + tile.col_in_group;
+    Xs = static_cast<double*>(P.X) + off;
+    Xf = static_cast<float*>(P.X) + off;
     LDX = P.G;
   } else {
     Xs = reinterpret_cast<double*>(smem_raw + L.strip);
@@ -656,6 +685,13 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
     } else {
       return Cfg::idx(row, col);
     }
+  };
+  // strip element access (the global strip of an FP32 plan holds floats)
+  auto xld = [&](int e) -> double { return f32 ? (double)Xf[e] : Xs[e]; };
+  auto xld2 = [&](int e) -> double2 { return f32 ? ld2(Xf + e) : ld2(Xs + e); };
+  auto xst2 = [&](int e, double2 v) {
+    if (f32) st2(Xf + e, v);
+    else st2(Xs + e, v);
   };
 
   if (tid == 0) {
@@ -677,7 +713,7 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
   if constexpr (GS) {  // the tile's T columns of every group-strip row
     for (int q = tid; q < tile.strip_rows * (T / 2); q += CT) {
       const int r = q / (T / 2), j = 2 * (q - r * (T / 2));
-      *reinterpret_cast<double2*>(Xs + (int64_t)r * LDX + j) = make_double2(0.0, 0.0);
+      xst2(r * LDX + j, make_double2(0.0, 0.0));
     }
   } else {
     double2* X2 = reinterpret_cast<double2*>(Xs);
@@ -687,7 +723,8 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
   consumer_sync<CT>();
   for (int q = tile.binit_begin + tid; q < tile.binit_end; q += CT) {
     const BInit bi = P.binit[q];
-    Xs[xi(bi.strip_row, bi.col)] = bi.val;
+    if (f32) Xf[xi(bi.strip_row, bi.col)] = (float)bi.val;
+    else Xs[xi(bi.strip_row, bi.col)] = bi.val;
   }
   consumer_sync<CT>();
 
@@ -707,10 +744,10 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
   };
   double* Ys = reinterpret_cast<double*>(smem_raw + L.ys);  // Y mode only: 64 x LDX, swizzled
   Group Gt;
-  double* Xg = nullptr;         // this tile's columns of its group strip (shared-strip mode)
+  int64_t xg_off = 0;           // this tile's columns of its group strip (shared-strip mode)
   if constexpr (!GS) {
     Gt = P.groups[tile.group];
-    Xg = P.X + P.sub_X_base[sub] + Gt.x_off + tile.col_in_group;
+    xg_off = P.sub_X_base[sub] + Gt.x_off + tile.col_in_group;
   }
   int b = 0;  // block counter (same order as the producer)
   for (int s = tile.step_begin; s < tile.step_end; s++, b++) {
@@ -724,14 +761,14 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
     // global strip has no zero pad rows past the last panel: rows >= kw are read as 0.
     double yf[KS][WN];
     {
-      const double* xb = Xs + (row0 + t4) * LDX;
+      const int xb = (row0 + t4) * LDX;
 #pragma unroll
       for (int j = 0; j < WN; j++) {
         const int xcol = xi(row0 + t4, (bc0 + j) * 8 + g) - (row0 + t4) * LDX;
 #pragma unroll
         for (int ks = 0; ks < KS; ks++) {
           if (ks % 4 == 0 && 4 * ks >= kw4) break;
-          yf[ks][j] = (4 * ks < kw4 && (!GS || 4 * ks + t4 < kw)) ? xb[(4 * ks) * LDX + xcol] : 0.0;
+          yf[ks][j] = (4 * ks < kw4 && (!GS || 4 * ks + t4 < kw)) ? xld(xb + (4 * ks) * LDX + xcol) : 0.0;
         }
       }
     }
@@ -832,9 +869,7 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
           for (int i = 0; i < WM; i++)
 #pragma unroll
             for (int j = 0; j < WN; j++)
-              R.xold[i][j] = (R.sr[i] == 0xFFFF)
-                                 ? make_double2(0.0, 0.0)
-                                 : *reinterpret_cast<const double2*>(Xs + xi(R.sr[i], (bc0 + j) * 8 + 2 * t4));
+              R.xold[i][j] = (R.sr[i] == 0xFFFF) ? make_double2(0.0, 0.0) : xld2(xi(R.sr[i], (bc0 + j) * 8 + 2 * t4));
         }
       }
       if (R.on) {
@@ -875,16 +910,20 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
             s0 += R.acc[h][i][j][0];
             s1 += R.acc[h][i][j][1];
           }
-          double2* p = reinterpret_cast<double2*>(Xs + xi(R.sr[i], (bc0 + j) * 8 + 2 * t4));
+          const int e = xi(R.sr[i], (bc0 + j) * 8 + 2 * t4);
           double2 v;
           if constexpr (GS) {
             v = R.xold[i][j];
           } else {
-            v = *p;
+            v = *reinterpret_cast<const double2*>(Xs + e);
           }
           v.x -= s0;
           v.y -= s1;
-          *p = v;
+          if constexpr (GS) {
+            xst2(e, v);
+          } else {
+            *reinterpret_cast<double2*>(Xs + e) = v;
+          }
         }
       }
     };
@@ -913,13 +952,14 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
       if (r < kw) {
 #pragma unroll
         for (int j = 0; j < WN; j++) {
-          double* dst;
+          const double2 v = make_double2(yn[i][j][0], yn[i][j][1]);
           if constexpr (GS) {
-            dst = Xs + xi(row0 + r, (bc0 + j) * 8 + 2 * t4);
+            xst2(xi(row0 + r, (bc0 + j) * 8 + 2 * t4), v);
           } else {
-            dst = Xg + (int64_t)(pn.grow + r) * P.G + (bc0 + j) * 8 + 2 * t4;
+            const int64_t e = xg_off + (int64_t)(pn.grow + r) * P.G + (bc0 + j) * 8 + 2 * t4;
+            if (P.fp32) st2(static_cast<float*>(P.X) + e, v);
+            else st2(static_cast<double*>(P.X) + e, v);
           }
-          *reinterpret_cast<double2*>(dst) = make_double2(yn[i][j][0], yn[i][j][1]);
         }
       }
     }
@@ -949,8 +989,9 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-__device__ __forceinline__ double gather_l(const double* __restrict__ Lv, int32_t q) {
-  return q >= 0 ? __ldg(Lv + q) : 0.0;
+template <typename ST>
+__device__ __forceinline__ double gather_l(const ST* __restrict__ Lv, int32_t q) {
+  return q >= 0 ? (double)__ldg(Lv + q) : 0.0;
 }
 
 #ifndef SC_WARP_MINB
@@ -958,8 +999,10 @@ __device__ __forceinline__ double gather_l(const double* __restrict__ Lv, int32_
 #endif
 constexpr int kWarpTri = 10 * 64;  // staged triangle values per warp: <= 10 8x8 blocks (kw <= 32)
 
-__device__ __forceinline__ void cp_async8(void* dst, const void* src, int src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes)
+template <int BYTES>
+__device__ __forceinline__ void cp_async_el(void* dst, const void* src, int src_bytes) {  // 4 or 8 bytes
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES),
+               "r"(src_bytes)
                : "memory");
 }
 
@@ -980,9 +1023,9 @@ __device__ __forceinline__ void warp_r_idx(const int32_t* __restrict__ gr, const
     for (int k2 = 0; k2 < KSMAX / 2; k2++) q[r * (KSMAX / 2) + k2] = (on && 2 * k2 < KS) ? __ldg(gi + k2) : make_int2(-1, -1);
   }
 }
-template <int NB, int KSMAX, int NRBB, int LDY>
-__device__ __forceinline__ void warp_r_run(const double* __restrict__ Lv, const int32_t* __restrict__ gr,
-                                          const uint16_t* __restrict__ srw, double* __restrict__ Xs, const int G,
+template <int NB, int KSMAX, int NRBB, int LDY, typename ST>
+__device__ __forceinline__ void warp_r_run(const ST* __restrict__ Lv, const int32_t* __restrict__ gr,
+                                          const uint16_t* __restrict__ srw, ST* __restrict__ Xs, const int G,
                                           const double* __restrict__ Ys, const int nRB, const int KS, const int lane,
                                           int2 (&q)[8], int (&row)[4]) {
   const int g = lane >> 2, t = lane & 3;
@@ -1000,8 +1043,7 @@ __device__ __forceinline__ void warp_r_run(const double* __restrict__ Lv, const 
       }
 #pragma unroll
       for (int j = 0; j < NB; j++)
-        xo[r][j] = rc[r] != 0xFFFF ? *reinterpret_cast<const double2*>(Xs + (int64_t)rc[r] * G + 8 * j + 2 * t)
-                                   : make_double2(0.0, 0.0);
+        xo[r][j] = rc[r] != 0xFFFF ? ld2(Xs + (int64_t)rc[r] * G + 8 * j + 2 * t) : make_double2(0.0, 0.0);
     }
     if (R0 + NRBB < nRB) warp_r_idx<KSMAX, NRBB>(gr, srw, R0 + NRBB, nRB, KS, lane, q, row);
 #pragma unroll
@@ -1018,20 +1060,22 @@ __device__ __forceinline__ void warp_r_run(const double* __restrict__ Lv, const 
     for (int r = 0; r < NRBB; r++)
       if (rc[r] != 0xFFFF) {
 #pragma unroll
-        for (int j = 0; j < NB; j++) *reinterpret_cast<double2*>(Xs + (int64_t)rc[r] * G + 8 * j + 2 * t) = xo[r][j];
+        for (int j = 0; j < NB; j++) st2(Xs + (int64_t)rc[r] * G + 8 * j + 2 * t, xo[r][j]);
       }
   }
 }
 
 // Gathers of a panel's triangle values (fragment order) into Ts with cp.async (no registers held
 // while they travel; structural zeros zero-filled).
-__device__ __forceinline__ void warp_tri_gather(const double* __restrict__ Lv, const int2 (&q)[10], int ntb,
-                                                double* Ts, int lane) {
+template <typename ST>
+__device__ __forceinline__ void warp_tri_gather(const ST* __restrict__ Lv, const int2 (&q)[10], int ntb, ST* Ts,
+                                                int lane) {
+  constexpr int B = sizeof(ST);
 #pragma unroll
   for (int b = 0; b < 10; b++)
     if (b < ntb) {
-      cp_async8(Ts + 64 * b + lane, Lv + (q[b].x >= 0 ? q[b].x : 0), q[b].x >= 0 ? 8 : 0);
-      cp_async8(Ts + 64 * b + 32 + lane, Lv + (q[b].y >= 0 ? q[b].y : 0), q[b].y >= 0 ? 8 : 0);
+      cp_async_el<B>(Ts + 64 * b + lane, Lv + (q[b].x >= 0 ? q[b].x : 0), q[b].x >= 0 ? B : 0);
+      cp_async_el<B>(Ts + 64 * b + 32 + lane, Lv + (q[b].y >= 0 ? q[b].y : 0), q[b].y >= 0 ? B : 0);
     }
 }
 __device__ __forceinline__ void warp_tri_idx(const int32_t* __restrict__ gx, int ntb, int lane, int2 (&q)[10]) {
@@ -1044,7 +1088,7 @@ __device__ __forceinline__ void warp_tri_idx(const int32_t* __restrict__ gx, int
 // gathered (cp.async) as soon as the current triangle is solved; the first R batch's maps are
 // loaded before the triangle solve.  Per warp shared memory: X_p / Y (32 x LDY), the triangle
 // values (block b, k step s: Ts[64 b + 32 s + lane]) and the reciprocal pivots.
-template <int NB>
+template <int NB, typename ST>
 __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P, int t0, int ntask) {
   constexpr int T = 8 * NB, LDY = T + 4;
   __shared__ __align__(16) double wsm[4][32 * LDY + kWarpTri + 32];
@@ -1052,14 +1096,14 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
   const int wt = blockIdx.x * 4 + wid;
   if (wt >= ntask) return;
   double* __restrict__ Ys = wsm[wid];
-  double* __restrict__ Ts = Ys + 32 * LDY;
-  double* __restrict__ Rv = Ts + kWarpTri;
+  ST* __restrict__ Ts = reinterpret_cast<ST*>(Ys + 32 * LDY);  // triangle values as stored (ST)
+  double* __restrict__ Rv = Ys + 32 * LDY + kWarpTri;
   const I2 task = P.trsm_tasks[t0 + wt];
   const int sub = task.x;
   const Tile tile = P.tiles[task.y];
-  const double* __restrict__ Lv = P.Lptr[sub];
+  const ST* __restrict__ Lv = static_cast<const ST*>(P.Lptr[sub]);
   const int G = P.G;
-  double* __restrict__ Xs = P.X + P.sub_X_base[sub] + P.groups[tile.group].x_off + tile.col_in_group;
+  ST* __restrict__ Xs = static_cast<ST*>(P.X) + P.sub_X_base[sub] + P.groups[tile.group].x_off + tile.col_in_group;
   const int g = lane >> 2, t = lane & 3;
   constexpr int VPR = T / 2, RPI = 32 / VPR;  // double2 per strip row, rows per warp instruction
   const int vr0 = lane / VPR, vc2 = 2 * (lane % VPR);
@@ -1074,12 +1118,11 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
     warp_tri_gather(Lv, qt, k8 * (k8 + 1) / 2, Ts, lane);
   }
   // X init (row a2): zero the tile's columns of every group-strip row, scatter B~^T
-  for (int r = vr0; r < tile.strip_rows; r += RPI)
-    *reinterpret_cast<double2*>(Xs + (int64_t)r * G + vc2) = make_double2(0.0, 0.0);
+  for (int r = vr0; r < tile.strip_rows; r += RPI) st2(Xs + (int64_t)r * G + vc2, make_double2(0.0, 0.0));
   __syncwarp();
   for (int q = tile.binit_begin + lane; q < tile.binit_end; q += 32) {
     const BInit bi = P.binit[q];
-    Xs[(int64_t)bi.strip_row * G + bi.col] = bi.val;
+    Xs[(int64_t)bi.strip_row * G + bi.col] = (ST)bi.val;
   }
   __syncwarp();
   for (int s = tile.step_begin; s < tile.step_end; s++) {
@@ -1087,10 +1130,15 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
     const Panel pn = pn_n;
     const int kw = pn.kw, kw8 = (kw + 7) >> 3, KS = 2 * kw8;
     const int32_t* __restrict__ gx = P.gidx + pn.gx_off;
-    double* __restrict__ xp = Xs + (int64_t)st.strip_row * G;
-    // X_p -> Ys (cp.async; rows kw..8 kw8 zero-filled)
-    for (int r = vr0; r < 8 * kw8; r += RPI)
-      cp_async16(Ys + r * LDY + vc2, xp + (int64_t)(r < kw ? r : 0) * G + vc2, r < kw ? 16 : 0);
+    ST* __restrict__ xp = Xs + (int64_t)st.strip_row * G;
+    // X_p -> Ys (rows kw..8 kw8 zero-filled): cp.async for FP64 strips, converting loads for FP32
+    if constexpr (sizeof(ST) == 8) {
+      for (int r = vr0; r < 8 * kw8; r += RPI)
+        cp_async16(Ys + r * LDY + vc2, xp + (int64_t)(r < kw ? r : 0) * G + vc2, r < kw ? 16 : 0);
+    } else {
+      for (int r = vr0; r < 8 * kw8; r += RPI)
+        *reinterpret_cast<double2*>(Ys + r * LDY + vc2) = r < kw ? ld2(xp + (int64_t)r * G + vc2) : make_double2(0.0, 0.0);
+    }
     cp_async_commit();
     const bool more = s + 1 < tile.step_end;
     if (more) {  // next step's descriptors and triangle gather map
@@ -1112,7 +1160,7 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
     {  // reciprocal pivots, one row per lane
       const int K = lane >> 3, gg = lane & 7;
       const bool live = lane < kw;
-      const double d = live ? Ts[64 * warp_tri_block(K, K, kw8) + 32 * (gg >> 2) + 4 * gg + (gg & 3)] : 1.0;
+      const double d = live ? (double)Ts[64 * warp_tri_block(K, K, kw8) + 32 * (gg >> 2) + 4 * gg + (gg & 3)] : 1.0;
       if (live && (!(d > 0.0) || !isfinite(d))) flag_zero_pivot(P, sub, pn.a + lane);
       Rv[lane] = live ? 1.0 / d : 0.0;
     }
@@ -1125,8 +1173,8 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
 #pragma unroll
         for (int j = 0; j < NB; j++) x[j] = *reinterpret_cast<const double2*>(Ys + (8 * K + g) * LDY + 8 * j + 2 * t);
         for (int J = 0; J < K; J++) {
-          const double* tb = Ts + 64 * warp_tri_block(J, K, kw8);
-          const double a0 = -tb[lane], a1 = -tb[32 + lane];
+          const ST* tb = Ts + 64 * warp_tri_block(J, K, kw8);
+          const double a0 = -(double)tb[lane], a1 = -(double)tb[32 + lane];
 #pragma unroll
           for (int j = 0; j < NB; j++) {
             dmma(x[j].x, x[j].y, a0, Ys[(8 * J + t) * LDY + 8 * j + g]);
@@ -1138,7 +1186,7 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
         __syncwarp();
       }
       if (lane < T) {
-        const double* tb = Ts + 64 * warp_tri_block(K, K, kw8);
+        const ST* tb = Ts + 64 * warp_tri_block(K, K, kw8);
         double xv[8];
 #pragma unroll
         for (int i = 0; i < 8; i++) xv[i] = Ys[(8 * K + i) * LDY + lane];
@@ -1146,7 +1194,7 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
         for (int k = 0; k < 8; k++) {
           xv[k] *= Rv[8 * K + k];
 #pragma unroll
-          for (int i = k + 1; i < 8; i++) xv[i] = fma(-tb[32 * (k >> 2) + 4 * i + (k & 3)], xv[k], xv[i]);
+          for (int i = k + 1; i < 8; i++) xv[i] = fma(-(double)tb[32 * (k >> 2) + 4 * i + (k & 3)], xv[k], xv[i]);
         }
 #pragma unroll
         for (int i = 0; i < 8; i++) Ys[(8 * K + i) * LDY + lane] = xv[i];
@@ -1161,9 +1209,9 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
     cp_async_commit();
     // the solved rows are final: into the group strip
     for (int r = vr0; r < kw; r += RPI)
-      *reinterpret_cast<double2*>(xp + (int64_t)r * G + vc2) = *reinterpret_cast<const double2*>(Ys + r * LDY + vc2);
-    if (KS <= 4) warp_r_run<NB, 4, 4, LDY>(Lv, gr, srw, Xs, G, Ys, nRB, KS, lane, qr, rr);
-    else warp_r_run<NB, 8, 2, LDY>(Lv, gr, srw, Xs, G, Ys, nRB, KS, lane, qr, rr);
+      st2(xp + (int64_t)r * G + vc2, *reinterpret_cast<const double2*>(Ys + r * LDY + vc2));
+    if (KS <= 4) warp_r_run<NB, 4, 4, LDY, ST>(Lv, gr, srw, Xs, G, Ys, nRB, KS, lane, qr, rr);
+    else warp_r_run<NB, 8, 2, LDY, ST>(Lv, gr, srw, Xs, G, Ys, nRB, KS, lane, qr, rr);
     __syncwarp();  // this step's strip writes are visible to every lane of the next step
   }
   cp_async_wait<0>();
@@ -1186,16 +1234,22 @@ struct SyrkCfg {              // (G/8)^2 output blocks of 8x8 over 8 warps
   static constexpr int ACTIVE = (NB / WM) * NWC;   // warps with work (4 for G = 16)
 };
 
-template <int G>
-constexpr size_t syrk_smem_bytes() {
-  return sizeof(double) * 4 * kKC * (G + 4);  // 2 stages x (X_I chunk, X_J chunk)
+// smem row stride (elements) of a staged X chunk: conflict-free fragment loads for 8- and 4-byte
+// elements
+template <int G, typename ST>
+__host__ __device__ constexpr int syrk_ld() {
+  return G + (sizeof(ST) == 8 ? 4 : 8);
+}
+template <int G, typename ST = double>
+__host__ __device__ constexpr size_t syrk_smem_bytes() {
+  return sizeof(ST) * 4 * kKC * syrk_ld<G, ST>();  // 2 stages x (X_I chunk, X_J chunk)
 }
 
-template <int G>
+template <int G, typename ST>
 __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) {
-  constexpr int kLdG = G + 4, kGroup = G;
+  constexpr int kLdG = syrk_ld<G, ST>(), kGroup = G;
   extern __shared__ __align__(16) unsigned char syrk_smem[];
-  double* Sbuf = reinterpret_cast<double*>(syrk_smem);
+  ST* Sbuf = reinterpret_cast<ST*>(syrk_smem);
   constexpr int WM = SyrkCfg<G>::WM, WN = SyrkCfg<G>::WN, NWC = SyrkCfg<G>::NWC;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool active = warp < SyrkCfg<G>::ACTIVE;
@@ -1204,8 +1258,8 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
   const int sub = task.x;
   const Pair pr = P.pairs[task.y];
   const Group gI = P.groups[pr.I], gJ = P.groups[pr.J];
-  const double* __restrict__ XI = P.X + P.sub_X_base[sub] + gI.x_off;
-  const double* __restrict__ XJ = P.X + P.sub_X_base[sub] + gJ.x_off;
+  const ST* __restrict__ XI = static_cast<const ST*>(P.X) + P.sub_X_base[sub] + gI.x_off;
+  const ST* __restrict__ XJ = static_cast<const ST*>(P.X) + P.sub_X_base[sub] + gJ.x_off;
   const int br0 = (warp / NWC) * WM, bc0 = (warp % NWC) * WN;
   double acc[WM][WN][2];
 #pragma unroll
@@ -1221,16 +1275,16 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
     if (csg < pr.seg_end) {
       const Seg s = P.segs[csg];
       kn = min(kKC, s.len - ck0);
-      double* As = Sbuf + (2 * stage) * kKC * kLdG;
-      double* Bs = As + kKC * kLdG;
-      // thread -> (row r0 + u * RSTEP, column pair j): fixed per thread, only the row bases move
-      constexpr int CP = kGroup / 2, RSTEP = kThreads / CP, NU = kKC / RSTEP;
-      const int r0 = tid / CP, j = 2 * (tid % CP);
-      const double* srcI = XI + (int64_t)(s.offI + ck0) * kGroup + j;
-      const double* srcJ = XJ + (int64_t)(s.offJ + ck0) * kGroup + j;
+      ST* As = Sbuf + (2 * stage) * kKC * kLdG;
+      ST* Bs = As + kKC * kLdG;
+      // thread -> (row r0 + u * RSTEP, 16-byte column vector j): fixed per thread, only the row
+      // bases move
+      constexpr int VEC = 16 / sizeof(ST), CP = kGroup / VEC, RSTEP = kThreads / CP;
+      const int r0 = tid / CP, j = VEC * (tid % CP);
+      const ST* srcI = XI + (int64_t)(s.offI + ck0) * kGroup + j;
+      const ST* srcJ = XJ + (int64_t)(s.offJ + ck0) * kGroup + j;
 #pragma unroll
-      for (int u = 0; u < NU; u++) {
-        const int r = r0 + u * RSTEP;
+      for (int r = r0; r < kKC; r += RSTEP) {
         const int ok = r < kn;
         const int rr = ok ? r : 0;
         cp_async16(As + r * kLdG + j, srcI + rr * kGroup, ok ? 16 : 0);
@@ -1251,16 +1305,16 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
     kn_next = load(cur ^ 1);
     cp_async_wait<1>();
     __syncthreads();
-    const double* As = Sbuf + (2 * cur) * kKC * kLdG;
-    const double* Bs = As + kKC * kLdG;
+    const ST* As = Sbuf + (2 * cur) * kKC * kLdG;
+    const ST* Bs = As + kKC * kLdG;
     const int kn4 = (kn + 3) & ~3;
     if (active) {
       auto kstep = [&](int k) {
         double a[WM], b[WN];
 #pragma unroll
-        for (int i = 0; i < WM; i++) a[i] = As[(k + t4) * kLdG + (br0 + i) * 8 + g];
+        for (int i = 0; i < WM; i++) a[i] = (double)As[(k + t4) * kLdG + (br0 + i) * 8 + g];
 #pragma unroll
-        for (int j = 0; j < WN; j++) b[j] = Bs[(k + t4) * kLdG + (bc0 + j) * 8 + g];
+        for (int j = 0; j < WN; j++) b[j] = (double)Bs[(k + t4) * kLdG + (bc0 + j) * 8 + g];
 #pragma unroll
         for (int i = 0; i < WM; i++)
 #pragma unroll
@@ -1277,8 +1331,7 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
   }
   cp_async_wait<0>();
   if (!active) return;
-  const int m = P.sub_m[sub];
-  double* __restrict__ F = P.F + P.sub_F_base[sub];
+  ST* __restrict__ F = static_cast<ST*>(P.F) + P.sub_F_base[sub];
   const bool diag = (pr.I == pr.J);
 #pragma unroll
   for (int i = 0; i < WM; i++) {
@@ -1290,7 +1343,7 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
       for (int h = 0; h < 2; h++) {
         const int c = (bc0 + j) * 8 + 2 * t4 + h;  // column within group J
         if (c >= gJ.width || (diag && r < c)) continue;
-        F[(int64_t)(gJ.col0 + c) * m + (gI.col0 + r)] = acc[i][j][h];
+        F[f_index(gI.col0 + r, gJ.col0 + c)] = (ST)acc[i][j][h];
       }
     }
   }
@@ -1313,6 +1366,7 @@ __device__ __forceinline__ int64_t apply_tile_index(int rb, int cb) { return (in
 #endif
 constexpr int kApplyTPC = SC_APPLY_TPC;  // tiles per CTA
 
+template <typename ST>
 __global__ void __launch_bounds__(kThreads) apply_tile_kernel(DevPlan P, const double* __restrict__ lambda, int ntask) {
   constexpr int AT = kApplyTile;
   static_assert(AT == 64 && kThreads == 256, "apply tile mapping");
@@ -1326,7 +1380,7 @@ __global__ void __launch_bounds__(kThreads) apply_tile_kernel(DevPlan P, const d
   const int m = P.sub_m[sub];
   const int r0 = rb * AT, c0 = cb * AT;
   const int nr = min(AT, m - r0), nc = min(AT, m - c0);
-  const double* __restrict__ F = P.F + P.sub_F_base[sub];
+  const ST* __restrict__ F = static_cast<const ST*>(P.F) + P.sub_F_base[sub];
   const int64_t* __restrict__ slm = P.slm + P.sub_slm_off[sub];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const bool diag = (rb == cb);
@@ -1334,13 +1388,14 @@ __global__ void __launch_bounds__(kThreads) apply_tile_kernel(DevPlan P, const d
   const double xA = (rA < nr) ? __ldg(lambda + slm[r0 + rA]) : 0.0;
   const double xB = (rB < nr) ? __ldg(lambda + slm[r0 + rB]) : 0.0;
   double fa[8], fb[8], xc[8];
+  const ST* __restrict__ Ft = F + apply_tile_index(rb, cb) * AT * AT;  // packed lower tile, ld 64
 #pragma unroll
   for (int k = 0; k < 8; k++) {
     const int c = warp * 8 + k;
-    const double* col = F + (int64_t)(c0 + c) * m + r0;
+    const ST* col = Ft + (int64_t)c * AT;
     const bool cv = c < nc;
-    fa[k] = (cv && rA < nr) ? __ldg(col + rA) : 0.0;
-    fb[k] = (cv && rB < nr) ? __ldg(col + rB) : 0.0;
+    fa[k] = (cv && rA < nr) ? (double)__ldg(col + rA) : 0.0;
+    fb[k] = (cv && rB < nr) ? (double)__ldg(col + rB) : 0.0;
     xc[k] = cv ? __ldg(lambda + slm[c0 + c]) : 0.0;
   }
   double* part = P.part + P.sub_part_off[sub] + apply_tile_index(rb, cb) * 2 * AT;
@@ -1660,18 +1715,24 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, P.sub_part_off, &D.sub_part_off, err));
   TRY(upload(P, P.qg_ptr, &D.qg_ptr, err));
   TRY(upload(P, P.qg_sub_a, &D.qg_sub_a, err));
-  TRY(alloc_zero(P, P.X_doubles, &D.X, err));
-  TRY(alloc_zero(P, P.F_doubles, &D.F, err));
+  {  // X strips and F' lower tiles in the plan's storage precision
+    char* xb = nullptr;
+    char* fb = nullptr;
+    TRY(alloc_zero(P, P.X_doubles * P.esz, &xb, err));
+    TRY(alloc_zero(P, P.F_doubles * P.esz, &fb, err));
+    D.X = xb;
+    D.F = fb;
+  }
   if (!P.warp_trsm) TRY(alloc_zero(P, P.PB_doubles, &D.PB, err));  // warp TRSM: only for the implicit apply, lazily
   TRY(alloc_zero(P, P.part_doubles, &D.part, err));
   TRY(alloc_zero(P, 1 + (int64_t)P.nsub, &D.err, err));
   double** dl = nullptr;
   TRY(alloc_zero(P, std::max(P.nsub, 1), &dl, err));
   P.d_Lptr = dl;
-  D.Lptr = dl;
+  D.Lptr = reinterpret_cast<const void* const*>(dl);
   void* hp = nullptr;
   CUDA_TRY(cudaMallocHost(&hp, sizeof(double*) * (size_t)std::max(P.nsub, 1)));
-  P.h_Lptr_pinned = static_cast<const double**>(hp);
+  P.h_Lptr_pinned = static_cast<const void**>(hp);
   cudaEvent_t ev;
   CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   P.lptr_event = ev;
@@ -1680,6 +1741,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   D.T = P.T;
   D.G = P.G;
   D.wmode = P.wmode ? 1 : 0;
+  D.fp32 = P.esz == 4 ? 1 : 0;
   if (P.ntrsm_small > 0) {  // small-strip tile class: its own launch on a side stream
     CUDA_TRY(cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&P.side_stream), cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(&P.ev_fork), cudaEventDisableTiming));
@@ -1700,18 +1762,21 @@ sc_status upload_plan(Plan& P, std::string& err) {
   CUDA_TRY(smem_attr((const void*)prep_small_kernel<16, false>, SmallCfg<16>::kSmem));
   CUDA_TRY(smem_attr((const void*)prep_small_kernel<32, true>, SmallCfg<32>::kSmem));
   CUDA_TRY(smem_attr((const void*)prep_small_kernel<32, false>, SmallCfg<32>::kSmem));
-  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<16>, syrk_smem_bytes<16>()));
-  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<32>, syrk_smem_bytes<32>()));
-  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<64>, syrk_smem_bytes<64>()));
-  CUDA_TRY(cudaFuncSetAttribute((const void*)trsm_warp_kernel<1>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                (int)cudaSharedmemCarveoutMaxShared));
-  CUDA_TRY(cudaFuncSetAttribute((const void*)trsm_warp_kernel<2>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                (int)cudaSharedmemCarveoutMaxShared));
+  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<16, double>, syrk_smem_bytes<16, double>()));
+  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<32, double>, syrk_smem_bytes<32, double>()));
+  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<64, double>, syrk_smem_bytes<64, double>()));
+  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<16, float>, syrk_smem_bytes<16, float>()));
+  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<32, float>, syrk_smem_bytes<32, float>()));
+  CUDA_TRY(smem_attr((const void*)syrk_pair_kernel<64, float>, syrk_smem_bytes<64, float>()));
+  for (const void* fn : {(const void*)trsm_warp_kernel<1, double>, (const void*)trsm_warp_kernel<2, double>,
+                         (const void*)trsm_warp_kernel<1, float>, (const void*)trsm_warp_kernel<2, float>})
+    CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared));
   if (!P.warp_trsm)
     CUDA_TRY(smem_attr((const void*)(P.gs2 ? trsm_kernel_ptr_gs2(P.wmode, P.gs2) : trsm_kernel_ptr(P.T, P.gstrip, P.wmode)),
                        P.smem_trsm));
   if (P.ntrsm_small > 0) CUDA_TRY(smem_attr((const void*)trsm_kernel_ptr2(P.T, P.wmode), P.smem_trsm_small));
-  double total = 8.0 * (P.X_doubles + P.F_doubles + (P.warp_trsm ? 0 : P.PB_doubles) + P.part_doubles) + 4.0 * gidx.size();
+  double total = (double)P.esz * (P.X_doubles + P.F_doubles) + 8.0 * ((P.warp_trsm ? 0 : P.PB_doubles) + P.part_doubles) +
+                 4.0 * gidx.size();
   total += dest.size() * 4.0 + Rrows.size() * 4.0 + panels.size() * sizeof(Panel) + tiles.size() * sizeof(Tile) +
            steps.size() * sizeof(Step) + groups.size() * sizeof(Group) +
            greach.size() * sizeof(Reach) + binit.size() * sizeof(BInit) + pairs.size() * sizeof(Pair) +
@@ -1773,7 +1838,7 @@ static int task_lb(const std::vector<I2>& v, int lo, int hi, int32_t sub) {
                v.begin());
 }
 
-static sc_status set_Lptr(Plan& P, const double* const* Lptr_host, cudaStream_t stream, std::string& err) {
+static sc_status set_Lptr(Plan& P, const void* const* Lptr_host, cudaStream_t stream, std::string& err) {
   bool same = (int32_t)P.last_Lptr.size() == P.nsub;
   for (int32_t i = 0; same && i < P.nsub; i++) same = (P.last_Lptr[(size_t)i] == Lptr_host[i]);
   if (same) return SC_OK;
@@ -1826,8 +1891,13 @@ static sc_status launch_trsm_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
     const int a = all ? 0 : task_lb(P.trsm_tasks, 0, ntr, s0), b = all ? ntr : task_lb(P.trsm_tasks, 0, ntr, s1);
     if (b > a) {
       const int nb = (b - a + 3) / 4;  // 4 warps (tiles) per CTA
-      if (P.T == 8) trsm_warp_kernel<1><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
-      else trsm_warp_kernel<2><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
+      if (P.esz == 4) {
+        if (P.T == 8) trsm_warp_kernel<1, float><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
+        else trsm_warp_kernel<2, float><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
+      } else {
+        if (P.T == 8) trsm_warp_kernel<1, double><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
+        else trsm_warp_kernel<2, double><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
+      }
       CUDA_TRY(cudaGetLastError());
     }
     return SC_OK;
@@ -1868,10 +1938,18 @@ static sc_status launch_syrk_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
     const int nsy = (int)P.syrk_tasks.size();
     const int a = all ? 0 : task_lb(P.syrk_tasks, 0, nsy, s0), b = all ? nsy : task_lb(P.syrk_tasks, 0, nsy, s1);
     if (b > a) {
-      switch (P.G) {
-        case 16: syrk_pair_kernel<16><<<b - a, kThreads, syrk_smem_bytes<16>(), stream>>>(P.dev, a); break;
-        case 32: syrk_pair_kernel<32><<<b - a, kThreads, syrk_smem_bytes<32>(), stream>>>(P.dev, a); break;
-        default: syrk_pair_kernel<64><<<b - a, kThreads, syrk_smem_bytes<64>(), stream>>>(P.dev, a); break;
+      if (P.esz == 4) {
+        switch (P.G) {
+          case 16: syrk_pair_kernel<16, float><<<b - a, kThreads, syrk_smem_bytes<16, float>(), stream>>>(P.dev, a); break;
+          case 32: syrk_pair_kernel<32, float><<<b - a, kThreads, syrk_smem_bytes<32, float>(), stream>>>(P.dev, a); break;
+          default: syrk_pair_kernel<64, float><<<b - a, kThreads, syrk_smem_bytes<64, float>(), stream>>>(P.dev, a); break;
+        }
+      } else {
+        switch (P.G) {
+          case 16: syrk_pair_kernel<16, double><<<b - a, kThreads, syrk_smem_bytes<16, double>(), stream>>>(P.dev, a); break;
+          case 32: syrk_pair_kernel<32, double><<<b - a, kThreads, syrk_smem_bytes<32, double>(), stream>>>(P.dev, a); break;
+          default: syrk_pair_kernel<64, double><<<b - a, kThreads, syrk_smem_bytes<64, double>(), stream>>>(P.dev, a); break;
+        }
       }
       CUDA_TRY(cudaGetLastError());
     }
@@ -1935,7 +2013,7 @@ static sc_status launch_overlapped(Plan& P, cudaStream_t stream, std::string& er
   return SC_OK;
 }
 
-sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_v, std::string& err) {
+sc_status launch_assemble(Plan& P, const void* const* Lptr_host, void* stream_v, std::string& err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   CUDA_TRY(cudaSetDevice(P.opt.device));
   sc_status st = set_Lptr(P, Lptr_host, stream, err);
@@ -1951,7 +2029,7 @@ sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream_
 // subdomains; chunk k's pinned-host -> device copies run on a plan-owned copy stream while the
 // kernels of chunk k-1 run on `stream` (one event per chunk), so the H2D transfer (PCIe-bound) hides
 // the assembly.
-sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* stream_v, std::string& err) {
+sc_status assemble_host_pipelined(Plan& P, const void* const* Lhost, void* stream_v, std::string& err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   CUDA_TRY(cudaSetDevice(P.opt.device));
   for (int32_t i = 0; i < P.nsub; i++)
@@ -1963,8 +2041,8 @@ sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* str
     P.Lstage_off.assign((size_t)P.nsub + 1, 0);
     for (int32_t i = 0; i < P.nsub; i++) P.Lstage_off[(size_t)i + 1] = P.Lstage_off[(size_t)i] + P.sub_nnz[(size_t)i];
     void* d = nullptr;
-    CUDA_TRY(cudaMalloc(&d, std::max<size_t>(8 * (size_t)P.Lstage_off.back(), 16)));
-    P.d_Lstage = static_cast<double*>(d);
+    CUDA_TRY(cudaMalloc(&d, std::max<size_t>((size_t)P.esz * (size_t)P.Lstage_off.back(), 16)));
+    P.d_Lstage = d;
   }
   if (!P.copy_stream) {
     CUDA_TRY(cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&P.copy_stream), cudaStreamNonBlocking));
@@ -1976,8 +2054,8 @@ sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* str
     CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     P.ev_chunk.push_back(e);
   }
-  std::vector<const double*> dptrs((size_t)P.nsub);
-  for (int32_t i = 0; i < P.nsub; i++) dptrs[(size_t)i] = P.d_Lstage + P.Lstage_off[(size_t)i];
+  std::vector<const void*> dptrs((size_t)P.nsub);
+  for (int32_t i = 0; i < P.nsub; i++) dptrs[(size_t)i] = static_cast<char*>(P.d_Lstage) + P.esz * P.Lstage_off[(size_t)i];
   sc_status st = set_Lptr(P, dptrs.data(), stream, err);
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
@@ -1994,9 +2072,9 @@ sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* str
     std::vector<size_t> sizes;
     for (int32_t i = s0; i < s1; i++)
       if (P.sub_nnz[(size_t)i] > 0) {
-        dsts.push_back(P.d_Lstage + P.Lstage_off[(size_t)i]);
-        srcs.push_back(const_cast<double*>(Lhost[i]));
-        sizes.push_back(8 * (size_t)P.sub_nnz[(size_t)i]);
+        dsts.push_back(static_cast<char*>(P.d_Lstage) + P.esz * P.Lstage_off[(size_t)i]);
+        srcs.push_back(const_cast<void*>(Lhost[i]));
+        sizes.push_back((size_t)P.esz * (size_t)P.sub_nnz[(size_t)i]);
       }
     if (!dsts.empty()) {
       cudaMemcpyAttributes attr{};
@@ -2020,7 +2098,8 @@ sc_status launch_apply(Plan& P, const double* lambda, double* q, void* stream_v,
   P.last_stream = stream_v;
   const int na = (int)P.apply_tasks.size();
   if (na > 0) {
-    apply_tile_kernel<<<(na + kApplyTPC - 1) / kApplyTPC, kThreads, 0, stream>>>(P.dev, lambda, na);
+    if (P.esz == 4) apply_tile_kernel<float><<<(na + kApplyTPC - 1) / kApplyTPC, kThreads, 0, stream>>>(P.dev, lambda, na);
+    else apply_tile_kernel<double><<<(na + kApplyTPC - 1) / kApplyTPC, kThreads, 0, stream>>>(P.dev, lambda, na);
     CUDA_TRY(cudaGetLastError());
   }
   if (P.n_lambda > 0) {
@@ -2031,7 +2110,7 @@ sc_status launch_apply(Plan& P, const double* lambda, double* q, void* stream_v,
   return SC_OK;
 }
 
-sc_status launch_prepare(Plan& P, const double* const* Lptr_host, void* stream_v, std::string& err) {
+sc_status launch_prepare(Plan& P, const void* const* Lptr_host, void* stream_v, std::string& err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   CUDA_TRY(cudaSetDevice(P.opt.device));
   sc_status st = set_Lptr(P, Lptr_host, stream, err);
@@ -2108,12 +2187,23 @@ static sc_status device_check_sub(Plan& P, int32_t i, std::string& err) {
   return SC_OK;
 }
 
+// `count` stored elements from element offset `off` of a device array in the plan's precision, as doubles
+static sc_status copy_elements(Plan& P, const void* base, int64_t off, int64_t count, double* out, std::string& err) {
+  if (P.esz == 8) {
+    CUDA_TRY(cudaMemcpy(out, static_cast<const double*>(base) + off, 8 * (size_t)count, cudaMemcpyDeviceToHost));
+    return SC_OK;
+  }
+  std::vector<float> tmp((size_t)count);
+  CUDA_TRY(cudaMemcpy(tmp.data(), static_cast<const float*>(base) + off, 4 * (size_t)count, cudaMemcpyDeviceToHost));
+  for (int64_t k = 0; k < count; k++) out[k] = (double)tmp[(size_t)k];
+  return SC_OK;
+}
+
 sc_status copy_F_lower(Plan& P, int32_t i, std::vector<double>& out, std::string& err) {
   TRY(device_check_sub(P, i, err));
-  int64_t m = P.sub_m[(size_t)i];
-  out.resize((size_t)(m * m));
-  if (m > 0)
-    CUDA_TRY(cudaMemcpy(out.data(), P.dev.F + P.sub_F_base[(size_t)i], 8 * (size_t)(m * m), cudaMemcpyDeviceToHost));
+  const int64_t m = P.sub_m[(size_t)i], len = f_tiles((int)m) * kApplyTile * kApplyTile;
+  out.resize((size_t)len);
+  if (m > 0) TRY(copy_elements(P, P.dev.F, P.sub_F_base[(size_t)i], len, out.data(), err));
   return SC_OK;
 }
 
@@ -2122,7 +2212,7 @@ sc_status copy_X_strips(Plan& P, int32_t i, std::vector<double>& out, std::strin
   const ClassPlan& C = P.classes[(size_t)P.sub_cls[(size_t)i]];
   out.resize((size_t)C.x_doubles);
   if (C.x_doubles > 0)
-    CUDA_TRY(cudaMemcpy(out.data(), P.dev.X + P.sub_X_base[(size_t)i], 8 * (size_t)C.x_doubles, cudaMemcpyDeviceToHost));
+    TRY(copy_elements(P, P.dev.X, P.sub_X_base[(size_t)i], C.x_doubles, out.data(), err));
   return SC_OK;
 }
 

@@ -689,7 +689,8 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
 
 sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options& opt, Plan& P, std::string& err) {
   if (nsub < 0 || (nsub > 0 && !sd)) FAIL(SC_ERR_INVALID_ARG, "sd is NULL or nsub < 0");
-  if (opt.precision != 64) FAIL(SC_ERR_INVALID_ARG, "only precision = 64 (FP64) is supported");
+  if (opt.precision != 64 && opt.precision != 32) FAIL(SC_ERR_INVALID_ARG, "precision must be 64 or 32");
+  P.esz = opt.precision == 32 ? 4 : 8;
   if (opt.skip < 0 || opt.skip > 2) FAIL(SC_ERR_INVALID_ARG, "skip must be 0, 1 or 2");
   if (!(opt.tile_cols == 0 || opt.tile_cols == 8 || opt.tile_cols == 16 || opt.tile_cols == 32 || opt.tile_cols == 64))
     FAIL(SC_ERR_INVALID_ARG, "tile_cols must be 0, 8, 16, 32 or 64");
@@ -746,6 +747,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   P.wmode = false;
   if (const char* e = std::getenv("SC_OVERLAP")) P.overlap = std::atoi(e);
   if (const char* e = std::getenv("SC_TRSM_MODE")) P.wmode = e[0] == 'W';
+  if (P.esz == 4 && P.wmode) FAIL(SC_ERR_INVALID_ARG, "precision 32 supports the Y-mode TRSM only");
   if (const char* e = std::getenv("SC_GROUP")) G0 = std::atoi(e);
   if (!(G0 == 16 || G0 == 32 || G0 == 64)) FAIL(SC_ERR_INVALID_ARG, "SC_GROUP must be 16, 32 or 64");
   // classes are independent: analysed on all host cores
@@ -1019,7 +1021,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     P.sub_X_base.push_back(P.X_doubles);
     P.X_doubles += C.x_doubles;
     P.sub_F_base.push_back(P.F_doubles);
-    P.F_doubles += (int64_t)C.m * C.m;
+    P.F_doubles += f_tiles(C.m) * kApplyTile * kApplyTile;
     P.sub_PB_base.push_back(P.PB_doubles);
     P.PB_doubles += C.pb_doubles;
     P.sub_part_off.push_back(P.part_doubles);

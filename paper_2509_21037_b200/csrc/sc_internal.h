@@ -142,6 +142,18 @@ struct I2 {
 
 // Apply: one 64 x 64 tile (row block rb >= column block cb) of the lower F' of subdomain sub.
 constexpr int kApplyTile = 64;
+// F' storage (SURVEY §8.1 a4/a5 "lower tiles"): per subdomain only the lower 64 x 64 tiles (rb >= cb),
+// tile (rb, cb) at position rb (rb + 1) / 2 + cb, each column-major with ld 64 (the diagonal tiles'
+// upper halves stay unused); about half of an m x m square.
+SC_HD inline int64_t f_tiles(int m) {
+  const int64_t nab = (m + kApplyTile - 1) / kApplyTile;
+  return nab * (nab + 1) / 2;
+}
+SC_HD inline int64_t f_index(int r, int c) {  // r >= c
+  const int rb = r / kApplyTile, cb = c / kApplyTile;
+  return ((int64_t)rb * (rb + 1) / 2 + cb) * (kApplyTile * kApplyTile) + (int64_t)(c % kApplyTile) * kApplyTile +
+         (r % kApplyTile);
+}
 struct ApplyTask {
   int32_t sub, rb, cb, pad;
 };
@@ -209,10 +221,10 @@ struct DevPlan {
   double* upart;                   // implicit apply: per (subdomain, stepped column) result, sub_slm_off
   double* xv;                      // implicit apply: per subdomain work vector (n doubles) if not in smem
   const int64_t* sub_X_base;       // per subdomain, doubles
-  const int64_t* sub_F_base;       // per subdomain, doubles (F' lower, column-major, ld = m)
+  const int64_t* sub_F_base;       // per subdomain, elements (F' lower 64 x 64 tiles, f_index)
   const int64_t* sub_PB_base;      // per subdomain panel buffer, doubles
   const int32_t* sub_m;
-  const double* const* Lptr;       // per subdomain L values (device)
+  const void* const* Lptr;         // per subdomain L values (device; double, or float when fp32)
   const I2* prep_tasks;            // (sub, global panel), panels wider than kSmallPanel
   const I2* prep_small_tasks;      // (sub, global panel), panels of <= kSmallPanel columns, bucketed
                                    //   by padded width 8 / 16 / 32 (Plan::small_begin)
@@ -224,8 +236,8 @@ struct DevPlan {
   const int64_t* sub_part_off;     // per subdomain offset into apply partial buffer
   const int64_t* qg_ptr;           // CSR over global multipliers: contributions
   const int64_t* qg_sub_a;         // (sub << 32) | a
-  double* X;
-  double* F;
+  void* X;                         // X group strips: double, or float when fp32
+  void* F;                         // F' lower tiles: double, or float when fp32
   double* PB;                      // panel buffers
   double* part;
   unsigned long long* err;         // sticky device error: [0] = ((sub+1) << 32) | col, [1+sub] = col+1
@@ -233,6 +245,7 @@ struct DevPlan {
   int32_t nsub, max_n, T, G;
   int32_t factor_ready;            // (host-side bookkeeping mirrors Plan::factor_ready)
   int32_t wmode;                         // 1: chunks hold W_p = L[R_p,p] inv(L_pp) (W mode), 0: L (Y mode)
+  int32_t fp32;                          // precision 32: L, X and F' stored in FP32 (FP64 arithmetic)
 };
 
 struct Plan {
@@ -263,11 +276,12 @@ struct Plan {
   bool on_device = false;
   DevPlan dev{};
   std::vector<void*> allocations;
-  const double** h_Lptr_pinned = nullptr;   // pinned staging for the per-call pointer array
+  const void** h_Lptr_pinned = nullptr;     // pinned staging for the per-call pointer array
   double** d_Lptr = nullptr;
-  std::vector<const double*> last_Lptr;
+  std::vector<const void*> last_Lptr;
+  int32_t esz = 8;                         // bytes per stored element of L / X / F' (8, or 4 when fp32)
   void* lptr_event = nullptr;              // cudaEvent_t of the last pointer upload
-  double* d_Lstage = nullptr;              // staging for sc_assemble_batch_host
+  void* d_Lstage = nullptr;                // staging for sc_assemble_batch_host
   std::vector<int64_t> Lstage_off;
   void* last_stream = nullptr;
   void* tev[4] = {nullptr, nullptr, nullptr, nullptr};  // optional timing events (sc_set_timing_events)
@@ -293,13 +307,13 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
 // kernels.cu
 sc_status upload_plan(Plan& P, std::string& err);
 void free_plan_device(Plan& P);
-sc_status launch_assemble(Plan& P, const double* const* Lptr_host, void* stream, std::string& err);
+sc_status launch_assemble(Plan& P, const void* const* Lptr_host, void* stream, std::string& err);
 sc_status launch_apply(Plan& P, const double* lambda, double* q, void* stream, std::string& err);
-sc_status launch_prepare(Plan& P, const double* const* Lptr_host, void* stream, std::string& err);
+sc_status launch_prepare(Plan& P, const void* const* Lptr_host, void* stream, std::string& err);
 sc_status launch_apply_implicit(Plan& P, const double* lambda, double* q, void* stream, std::string& err);
 sc_status device_check(Plan& P, std::string& err);
 sc_status copy_F_lower(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
 sc_status copy_X_strips(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
-sc_status assemble_host_pipelined(Plan& P, const double* const* Lhost, void* stream, std::string& err);
+sc_status assemble_host_pipelined(Plan& P, const void* const* Lhost, void* stream, std::string& err);
 
 }  // namespace sc

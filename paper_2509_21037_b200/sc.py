@@ -134,7 +134,7 @@ class SCPlan:
 
     def __init__(self, subdomains: Sequence, *, n_lambda: int = 0, skip: int = SKIP_EXACT, tile_cols: int = 0,
                  panel_cols: int = 0, device: int = 0, x_strip: int = STRIP_AUTO,
-                 trsm_kernel: int = TRSM_AUTO):
+                 trsm_kernel: int = TRSM_AUTO, precision: int = 64):
         L = lib()
         keep: List[np.ndarray] = []
 
@@ -166,6 +166,8 @@ class SCPlan:
         L.sc_options_default(ctypes.byref(opt))
         opt.skip, opt.tile_cols, opt.panel_cols, opt.x_strip = skip, tile_cols, panel_cols, x_strip
         opt.trsm_kernel = trsm_kernel
+        opt.precision = int(precision)
+        self.precision = int(precision)
         opt.n_lambda_global, opt.device = int(n_lambda), int(device)
         self.device = device
         self.n_lambda = int(n_lambda)
@@ -175,27 +177,34 @@ class SCPlan:
         self.nsub = len(subdomains)
 
     # -- preprocessing
-    def assemble(self, L_values: Sequence, stream=None):
-        """L_values: per subdomain a CUDA float64 tensor (or raw device pointer int) of nnz(L) values."""
+    def _value_ptrs(self, L_values: Sequence):
+        """Pointer array of the per-subdomain L values; tensors must have the plan's element type
+        (float64, or float32 for precision 32)."""
         ptrs = (_P * max(self.nsub, 1))()
+        want = 8 if self.precision == 64 else 4
         for i, t in enumerate(L_values):
-            ptrs[i] = t if isinstance(t, int) else t.data_ptr()
-        _check(lib().sc_assemble_batch(self._h, ptrs, _stream_handle(stream)))
+            if isinstance(t, int):
+                ptrs[i] = t
+                continue
+            esz = t.element_size() if hasattr(t, "element_size") else t.itemsize
+            if esz != want:
+                raise TypeError(f"L_values[{i}]: {want}-byte elements expected for precision {self.precision}")
+            ptrs[i] = t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+        return ptrs
+
+    def assemble(self, L_values: Sequence, stream=None):
+        """L_values: per subdomain a CUDA tensor (float64, or float32 for precision 32) or a raw device
+        pointer (int) of nnz(L) values."""
+        _check(lib().sc_assemble_batch(self._h, self._value_ptrs(L_values), _stream_handle(stream)))
 
     def assemble_host(self, L_values: Sequence[np.ndarray], stream=None):
         """L values in host memory (pinned torch tensors or numpy arrays); copied H2D inside the call."""
-        ptrs = (_P * max(self.nsub, 1))()
-        for i, t in enumerate(L_values):
-            ptrs[i] = t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
-        _check(lib().sc_assemble_batch_host(self._h, ptrs, _stream_handle(stream)))
+        _check(lib().sc_assemble_batch_host(self._h, self._value_ptrs(L_values), _stream_handle(stream)))
 
     # -- solution
     def prepare_factor(self, L_values: Sequence, stream=None):
         """Stage the factor panels only (no F): what apply_implicit needs."""
-        ptrs = (_P * max(self.nsub, 1))()
-        for i, t in enumerate(L_values):
-            ptrs[i] = t if isinstance(t, int) else t.data_ptr()
-        _check(lib().sc_prepare_factor(self._h, ptrs, _stream_handle(stream)))
+        _check(lib().sc_prepare_factor(self._h, self._value_ptrs(L_values), _stream_handle(stream)))
 
     def apply_implicit(self, lam, q, stream=None):
         """q <- sum_i scatter(B~_i K_i^{-1} B~_i^T gather(lam)) without F (two substitutions per subdomain)."""

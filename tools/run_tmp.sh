@@ -1,7 +1,5 @@
 cd $GRAFT_REPO_ROOT
-mkdir -p gpurun_out/sanitizer
-for CFG in cfg1 t3e; do for TOOL in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $TOOL --print-limit 20 python tools/sanitize_run.py $CFG > gpurun_out/sanitizer/${TOOL}_${CFG}.txt 2>&1
-  echo "exit $?" >> gpurun_out/sanitizer/${TOOL}_${CFG}.txt
-done; done
-timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+timeout 1800 python -m pytest tests -q -m gpu -x --durations=8 > gpurun_out/t_all.log 2>&1
+B="timeout 300 python bench.py --config cfg2 --steps 10 --warmup 3 --no-cpu-baseline --no-amortization --no-e2e --per-config none"
+$B > gpurun_out/f_base.json 2> gpurun_out/f_base.err
+timeout 300 python bench.py --config cfg2 --steps 10 --warmup 3 --no-cpu-baseline --no-amortization --no-e2e --per-config none > gpurun_out/f_base2.json 2>&1
