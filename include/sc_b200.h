@@ -176,6 +176,44 @@ sc_status sc_prepare_factor(sc_plan_t p, const void* const* L_values, void* stre
    DEVICE arrays of n_lambda_global doubles; q overwritten; deterministic. */
 sc_status sc_apply_implicit(sc_plan_t p, const double* lambda, double* q, void* stream);
 
+/* ---- Solution stage: PCPG on the FETI dual problem -------------------------------
+   Solves  [F -G; -G^T O] [lambda; alpha] = [d; -e]  (eq. tfetidualproblem) by the
+   projected conjugate gradient method with the identity preconditioner ("PCPG": "In each
+   iteration, the operator F is applied"): lambda_0 = G (G^T G)^{-1} e, projector
+   P = I - G (G^T G)^{-1} G^T, CG on w = P (d - F lambda), stop when ||w|| <= rtol ||P d||.  Each
+   iteration applies F once through sc_apply (this plan's partial) + `allreduce` over ranks, and P
+   once (G^T x per subdomain + allreduce of the coarse vector, dense (G^T G)^{-1}, G y + allreduce).
+   All vector arithmetic runs in this library's kernels and is deterministic; dual vectors are
+   replicated on every rank.  Needs an assembled F (sc_assemble_batch).  Synchronises. */
+typedef void (*sc_allreduce_fn)(double* buf, int64_t n, void* ctx); /* in-place SUM of a device
+                                                                       buffer over all ranks      */
+typedef struct {
+  int32_t nc;                /* coarse dimension: columns of G = B R over ALL ranks' subdomains; 0 =
+                                no projector (plain CG on F from the given lambda)                  */
+  const int32_t* k;          /* host, nsub: columns k_i of R_i (basis of ker K_i) of this plan's
+                                subdomains (heat: 1, elasticity: 6)                                 */
+  const int64_t* off;        /* host, nsub: first global coarse index of subdomain i's columns      */
+  const double* const* Rt;   /* host array of nsub DEVICE pointers: B~_i R_i (m_i x k_i, column-major,
+                                rows in the ORIGINAL local multiplier order); must stay valid        */
+  const double* GtG_inv;     /* DEVICE, nc x nc dense (G^T G)^{-1} (symmetric)                       */
+} sc_coarse;
+typedef struct {
+  double rtol;               /* relative tolerance on ||P r|| / ||P d||                             */
+  int32_t max_it;
+  double* alpha;             /* DEVICE nc or NULL: alpha = (G^T G)^{-1} G^T (F lambda - d)            */
+} sc_pcpg_opts;
+typedef struct {
+  int32_t iterations;        /* out                                                                 */
+  double rel_residual;       /* out: final ||P r|| / ||P d||                                         */
+  double* history;           /* optional HOST array: relative residual before each iteration        */
+  int32_t history_len;
+} sc_pcpg_result;
+/* d: DEVICE n_lambda_global; e: HOST nc (ignored if nc == 0); lambda: DEVICE n_lambda_global,
+   output (input initial guess only when nc == 0).  allreduce may be NULL on one rank. */
+sc_status sc_pcpg(sc_plan_t p, const double* d, const double* e, double* lambda, const sc_coarse* coarse,
+                  const sc_pcpg_opts* opts, sc_allreduce_fn allreduce, void* ctx, sc_pcpg_result* res,
+                  void* stream);
+
 /* Synchronise the plan's last stream and report a sticky device error (SC_ERR_ZERO_PIVOT). */
 sc_status sc_check(sc_plan_t p);
 

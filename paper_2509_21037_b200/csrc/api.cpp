@@ -106,6 +106,25 @@ sc_status sc_apply_implicit(sc_plan_t p, const double* lambda, double* q, void* 
   return st == SC_OK ? SC_OK : fail(st, err);
 }
 
+sc_status sc_pcpg(sc_plan_t p, const double* d, const double* e, double* lambda, const sc_coarse* coarse,
+                  const sc_pcpg_opts* opts, sc_allreduce_fn allreduce, void* ctx, sc_pcpg_result* res, void* stream) {
+  if (!p || !opts) return fail(SC_ERR_INVALID_ARG, "NULL plan or opts");
+  if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
+  if (p->P.n_lambda > 0 && (!d || !lambda)) return fail(SC_ERR_INVALID_ARG, "NULL d or lambda");
+  if (coarse && coarse->nc > 0 &&
+      ((!coarse->k || !coarse->off || !coarse->Rt || !coarse->GtG_inv) && p->P.nsub > 0))
+    return fail(SC_ERR_INVALID_ARG, "incomplete sc_coarse");
+  if (coarse && coarse->nc > 0 && !e) return fail(SC_ERR_INVALID_ARG, "NULL e");
+  if (coarse && coarse->nc > 0)
+    for (int32_t i = 0; i < p->P.nsub; i++)
+      if (coarse->k[i] < 0 || coarse->off[i] < 0 || coarse->off[i] + coarse->k[i] > coarse->nc)
+        return fail(SC_ERR_INVALID_ARG, "sc_coarse: subdomain columns outside [0, nc)");
+  if (!(opts->rtol >= 0) || opts->max_it < 0) return fail(SC_ERR_INVALID_ARG, "bad rtol / max_it");
+  std::string err;
+  sc_status st = sc::pcpg_solve(p->P, d, e, lambda, coarse, *opts, allreduce, ctx, res, stream, err);
+  return st == SC_OK ? SC_OK : fail(st, err);
+}
+
 sc_status sc_check(sc_plan_t p) {
   if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
   if (!p->P.on_device) return SC_OK;

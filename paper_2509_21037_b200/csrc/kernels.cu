@@ -1712,6 +1712,7 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, P.apply_tasks, &D.apply_tasks, err));
   TRY(upload(P, P.sub_slm_off, &D.sub_slm_off, err));
   TRY(upload(P, P.slm, &D.slm, err));
+  TRY(upload(P, P.ssig, &D.ssig, err));
   TRY(upload(P, P.sub_part_off, &D.sub_part_off, err));
   TRY(upload(P, P.qg_ptr, &D.qg_ptr, err));
   TRY(upload(P, P.qg_sub_a, &D.qg_sub_a, err));

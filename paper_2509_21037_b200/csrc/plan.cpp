@@ -1041,6 +1041,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
     for (int32_t rb = 0; rb < nab; rb++)
       for (int32_t cb = 0; cb <= rb; cb++) P.apply_tasks.push_back({i, rb, cb, 0});
     P.sub_slm_off.push_back((int64_t)P.slm.size());
+    P.ssig.insert(P.ssig.end(), C.sigma.begin(), C.sigma.end());
     if (sd[i].lambda_map) {
       for (int32_t a = 0; a < C.m; a++) {
         int64_t g = sd[i].lambda_map[C.sigma[(size_t)a]];

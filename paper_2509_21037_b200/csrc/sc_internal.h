@@ -233,6 +233,7 @@ struct DevPlan {
   const ApplyTask* apply_tasks;
   const int64_t* sub_slm_off;      // per subdomain offset into slm (stepped lambda map)
   const int64_t* slm;              // lambda_map[sigma[a]] per subdomain, concatenated
+  const int32_t* ssig;             // sigma[a] (original local column of stepped a), same layout
   const int64_t* sub_part_off;     // per subdomain offset into apply partial buffer
   const int64_t* qg_ptr;           // CSR over global multipliers: contributions
   const int64_t* qg_sub_a;         // (sub << 32) | a
@@ -269,6 +270,7 @@ struct Plan {
   std::vector<ApplyTask> apply_tasks;
   std::vector<int64_t> sub_X_base, sub_F_base, sub_PB_base, sub_part_off, sub_slm_off;
   std::vector<int64_t> slm, qg_ptr, qg_sub_a;
+  std::vector<int32_t> ssig;
   int64_t X_doubles = 0, F_doubles = 0, PB_doubles = 0, part_doubles = 0;
   int32_t max_n = 0, max_strip_rows = 0;
   sc_stats stats{};
@@ -315,5 +317,10 @@ sc_status device_check(Plan& P, std::string& err);
 sc_status copy_F_lower(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
 sc_status copy_X_strips(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
 sc_status assemble_host_pipelined(Plan& P, const void* const* Lhost, void* stream, std::string& err);
+
+// pcpg.cu
+sc_status pcpg_solve(Plan& P, const double* d, const double* e_host, double* lambda, const sc_coarse* cs,
+                     const sc_pcpg_opts& o, sc_allreduce_fn allreduce, void* ctx, sc_pcpg_result* res, void* stream,
+                     std::string& err);
 
 }  // namespace sc

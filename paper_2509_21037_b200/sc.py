@@ -60,9 +60,32 @@ class Stats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class Coarse(ctypes.Structure):
+    _fields_ = [("nc", ctypes.c_int32), ("k", _P), ("off", _P), ("Rt", _P), ("GtG_inv", _P)]
+
+
+class PcpgOpts(ctypes.Structure):
+    _fields_ = [("rtol", ctypes.c_double), ("max_it", ctypes.c_int32), ("alpha", _P)]
+
+
+class PcpgResult(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("rel_residual", ctypes.c_double), ("history", _P),
+                ("history_len", ctypes.c_int32)]
+
+
+ALLREDUCE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p)
+
+
+class _DeviceBuf:
+    """Zero-copy view of a device buffer handed to the all-reduce callback (CUDA array interface)."""
+
+    def __init__(self, ptr: int, n: int):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": "<f8", "data": (ptr, False), "version": 3}
+
+
 _lib = None
 
-EXPORTS = ["sc_options_default", "sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply",
+EXPORTS = ["sc_pcpg", "sc_options_default", "sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply",
            "sc_check", "sc_get_F", "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_plan_subdomain_costs",
            "sc_set_timing_events", "sc_launches_per_assemble",
            "sc_launches_per_apply", "sc_plan_destroy", "sc_last_error", "sc_prepare_factor", "sc_apply_implicit",
@@ -100,6 +123,9 @@ def lib():
     L.sc_launches_per_apply.restype = ctypes.c_int32
     L.sc_plan_destroy.argtypes = [_P]
     L.sc_plan_destroy.restype = None
+    L.sc_pcpg.argtypes = [_P, _P, _P, _P, ctypes.POINTER(Coarse), ctypes.POINTER(PcpgOpts), ALLREDUCE_FN, _P,
+                          ctypes.POINTER(PcpgResult), _P]
+    L.sc_pcpg.restype = ctypes.c_int
     L.sc_last_error.argtypes = []
     L.sc_last_error.restype = ctypes.c_char_p
     for f in ("sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply", "sc_check", "sc_get_F",
@@ -220,6 +246,42 @@ class SCPlan:
         self.apply(lam, q, stream)
         if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
             dist.all_reduce(q, op=dist.ReduceOp.SUM, group=group)
+
+    def pcpg(self, d, lam, *, e=None, coarse=None, rtol: float = 1e-10, max_it: int = 1000, alpha=None,
+             group=None, history: int = 0, stream=None):
+        """PCPG on the FETI dual problem (sc_pcpg): d, lam device float64 tensors (n_lambda); e host
+        array (nc) of R^T f; coarse = dict(nc, k (per subdomain of this plan), off, Rt (device tensors
+        B~_i R_i, m_i x k_i, column-major, original multiplier order), GtG_inv (device nc x nc));
+        alpha: optional device tensor (nc) receiving alpha.  For N > 1 ranks the partial F p, G^T x
+        and G y are summed with torch.distributed.all_reduce (NCCL).  Returns (iterations, final
+        relative residual, residual history)."""
+        import torch
+        import torch.distributed as dist
+        keep = []
+        cs = None
+        if coarse is not None and int(coarse["nc"]) > 0:
+            k = np.ascontiguousarray(coarse["k"], dtype=np.int32)
+            off = np.ascontiguousarray(coarse["off"], dtype=np.int64)
+            rt = (_P * max(self.nsub, 1))(*[t.data_ptr() for t in coarse["Rt"]])
+            keep += [k, off, rt, coarse["Rt"], coarse["GtG_inv"]]
+            cs = Coarse(int(coarse["nc"]), k.ctypes.data, off.ctypes.data, ctypes.cast(rt, _P),
+                        coarse["GtG_inv"].data_ptr())
+        e_arr = None
+        if e is not None:
+            e_arr = np.ascontiguousarray(e, dtype=np.float64)
+            keep.append(e_arr)
+        opts = PcpgOpts(float(rtol), int(max_it), None if alpha is None else alpha.data_ptr())
+        hist = np.zeros(max(history, 1))
+        res = PcpgResult(0, 0.0, hist.ctypes.data if history else None, int(history))
+        cb = ALLREDUCE_FN()
+        if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+            def _allreduce(ptr, n, ctx):
+                dist.all_reduce(torch.as_tensor(_DeviceBuf(ptr, n), device="cuda"), group=group)
+            cb = ALLREDUCE_FN(_allreduce)
+        _check(lib().sc_pcpg(self._h, d.data_ptr(), None if e_arr is None else e_arr.ctypes.data, lam.data_ptr(),
+                             ctypes.byref(cs) if cs is not None else None, ctypes.byref(opts), cb, None,
+                             ctypes.byref(res), _stream_handle(stream)))
+        return res.iterations, res.rel_residual, hist[:min(history, res.iterations + 1)] if history else None
 
     # -- queries
     def check(self):

@@ -20,4 +20,6 @@ from .mesh import (  # noqa: F401
     config_problem,
     chain_1d_problem,
     custom_problem,
+    kernel_basis,
+    subdomain_K,
 )

@@ -456,6 +456,31 @@ def config_problem(name: str, **kw) -> Problem:
     return make_problem(name=name, **args)
 
 
+def subdomain_K(problem: Problem, sd: Subdomain) -> sp.csr_matrix:
+    """Unregularised K_i of a subdomain of a per-subdomain-coefficient problem (natural DOF order)."""
+    h = 1.0 / (problem.S * problem.E)
+    return (assemble_subdomain(problem.dim, problem.E, problem.physics, None, h) * sd.kappa).tocsr()
+
+
+def kernel_basis(problem: Problem, sd: Subdomain) -> np.ndarray:
+    """R_i: basis of ker K_i ("R_i containing the basis vectors of Ker K_i") in the
+    natural DOF order: constants for heat, the 6 rigid-body modes (3 translations, 3 rotations
+    about the subdomain's corner) for elasticity."""
+    N = problem.E + 1
+    d = problem.dim
+    if problem.physics == "heat":
+        return np.ones((sd.n, 1))
+    g = np.indices([N] * d).reshape(d, -1)[::-1].astype(np.float64)  # g[k] = coordinate along axis k, x fastest
+    x, y, z = g[0], g[1], g[2]
+    R = np.zeros((sd.n, 6))
+    for c in range(3):
+        R[c::3, c] = 1.0
+    R[0::3, 3], R[1::3, 3] = -y, x       # rotation about z
+    R[1::3, 4], R[2::3, 4] = -z, y       # rotation about x
+    R[0::3, 5], R[2::3, 5] = z, -x       # rotation about y
+    return R
+
+
 def chain_1d_problem(n: int) -> Problem:
     """1D chain K = tridiag(-1,2,-1) (SPD without regularisation), B~^T = [e_1, e_n], identity
     ordering.  Closed form F = [[n,1],[1,n]]/(n+1) (SURVEY §8.3 pins)."""
