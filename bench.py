@@ -235,6 +235,52 @@ def time_assembly(plan, Ls, steps, warmup, world, clock_index=None):
     return start.elapsed_time(stop), phases, clk.summary()
 
 
+def time_factor(plan, P, steps, warmup, peaks):
+    """Device numeric factorization: sc_factorize_batch (device K -> device L) timed with
+    CUDA events over `steps` calls, and the device-resident preprocessing factorize + assemble.
+    Returns (summary dict, device K tensors, device L tensors)."""
+    import torch
+    t0 = time.perf_counter()
+    plan.factor_attach([sd.K_lower()[:2] for sd in P.subdomains])
+    t_sym = time.perf_counter() - t0
+    st = plan.stats()
+    Kd = [torch.from_numpy(sd.K_lower()[2]).cuda() for sd in P.subdomains]
+    Lo = [torch.empty(int(sd.L_colptr[-1]), dtype=torch.float64, device="cuda") for sd in P.subdomains]
+    stream = torch.cuda.current_stream()
+    for _ in range(warmup):
+        plan.factorize(Kd, Lo)
+    torch.cuda.synchronize()
+    plan.check()
+    e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+    e0.record(stream)
+    for _ in range(steps):
+        plan.factorize(Kd, Lo)
+    e1.record(stream)
+    for _ in range(steps):
+        plan.factorize(Kd, Lo)
+        plan.assemble(Lo)
+    e2.record(stream)
+    torch.cuda.synchronize()
+    plan.check()
+    ms_f = e0.elapsed_time(e1) / steps
+    ms_fa = e1.elapsed_time(e2) / steps
+    nsub = len(P.subdomains)
+    worst = max(float((Lo[i] - torch.from_numpy(P.subdomains[i].L_values).cuda()).abs().max()) /
+                float(np.abs(P.subdomains[i].L_values).max()) for i in (0, nsub // 2, nsub - 1))
+    out = {"ms": ms_f, "subdomains_per_s": nsub / (ms_f / 1e3),
+           "gflops_useful": st["flops_factor_useful"] / (ms_f / 1e3) / 1e9,
+           "fp64_frac_useful": st["flops_factor_useful"] / (ms_f / 1e3) / 1e12 / peaks["fp64_tflops"],
+           "flops_useful": st["flops_factor_useful"], "flops_executed": st["flops_factor_executed"],
+           "bytes_K": st["bytes_K_values"], "bytes_L": st["bytes_L_values"], "tasks": st["factor_tasks"],
+           "max_level": st["factor_max_level"], "symbolic_s": t_sym,
+           "preprocessing_ms": ms_fa, "preprocessing_subdomains_per_s": nsub / (ms_fa / 1e3),
+           "L_vs_host_factor_max_rel_diff": worst,
+           "kernel": "factor_kernel (left-looking supernodal, warp per 32-row frame, DMMA updates)",
+           "note": "preprocessing = sc_factorize_batch + sc_assemble_batch (P:326-328 two-stage factorization; "
+                   "P:2563-2570 factorization share)"}
+    return out, Kd, Lo
+
+
 def roofline_for(st, phases, ms_step, peaks, cfg):
     """Dominant kernel of the step vs the roof its algorithmic intensity selects:
        prep: bytes = L values read once;
@@ -293,12 +339,15 @@ def per_config_lines(args, peaks):
         ms_total, phases, clocks = time_assembly(plan, Ls, steps, 3, 1)
         ms_step = ms_total / steps
         useful = st["flops_trsm_useful"] + st["flops_syrk_useful"]
+        fac, Kd, Lo = time_factor(plan, P, steps, 2, peaks)
+        del Kd, Lo
         out[cfg] = {"workload": CFG_DESC[cfg], "subdomains": len(P.subdomains), "steps": steps, "warmup": 3,
                     "value": len(P.subdomains) / (ms_step / 1e3), "unit": "subdomains/s", "ms_per_step": ms_step,
                     "phase_ms": phases, "gflops_useful": useful / (ms_step / 1e3) / 1e9,
                     "fp64_frac_useful": useful / (ms_step / 1e3) / 1e12 / peaks["fp64_tflops"],
                     "roofline": roofline_for(st, phases, ms_step, peaks, cfg), "clocks": clocks, "plan_s": t_plan,
-                    "tile_cols": st["tile_cols"], "trsm_kernel": {1: "cta", 2: "warp"}.get(st["trsm_kernel"])}
+                    "tile_cols": st["tile_cols"], "trsm_kernel": {1: "cta", 2: "warp"}.get(st["trsm_kernel"]),
+                    "factor": fac}
         del Ls, plan
         torch.cuda.empty_cache()
     return out
@@ -328,6 +377,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-amortization", action="store_true")
+    ap.add_argument("--no-factor", action="store_true", help="skip the device factorization (f4) timing / K-fed e2e")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
@@ -377,27 +427,33 @@ def main():
     useful_job, executed_job = float(fl[0]), float(fl[1])
     value = nsub_job / (ms_step / 1e3)
 
-    # e2e through the public API with HOST inputs: pinned L values -> H2D inside the call ->
-    # assemble -> one explicit apply q = F lambda (solution stage, NCCL all-reduce for N > 1) -> D2H of q
-    e2e = None
-    if not args.no_e2e:
-        hostL = [torch.from_numpy(np.ascontiguousarray(sd.L_values)).pin_memory() for sd in P.subdomains]
-        lam_h = torch.from_numpy(np.random.default_rng(0).standard_normal(P.n_lambda)).pin_memory()
-        lam_d = torch.empty(P.n_lambda, dtype=torch.float64, device="cuda")
-        q_d = torch.empty_like(lam_d)
-        q_h = torch.empty(P.n_lambda, dtype=torch.float64).pin_memory()
+    # device numeric factorization (f4) and the host-fed end-to-end paths through the public API:
+    #   e2e        pinned K values (lower triangle) -> H2D inside sc_factorize_assemble_host -> device
+    #              factorization -> assembly -> one explicit apply (NCCL all-reduce for N > 1) -> D2H of q
+    #   e2e_from_L pinned L values -> H2D inside sc_assemble_batch_host -> assembly -> apply -> D2H of q
+    factor = None
+    if not args.no_factor:
+        factor, Kd, Lo = time_factor(plan, P, args.steps, args.warmup, peaks)
+        del Kd, Lo
+    lam_h = torch.from_numpy(np.random.default_rng(0).standard_normal(P.n_lambda)).pin_memory()
+    lam_d = torch.empty(P.n_lambda, dtype=torch.float64, device="cuda")
+    q_d = torch.empty_like(lam_d)
+    q_h = torch.empty(P.n_lambda, dtype=torch.float64).pin_memory()
+
+    def e2e_run(step_fn, h2d_inputs, includes):
         for _ in range(args.warmup):
-            plan.assemble_host(hostL)
+            step_fn()
             lam_d.copy_(lam_h, non_blocking=True)
             plan.apply_global(lam_d, q_d)
             q_h.copy_(q_d, non_blocking=True)
         torch.cuda.synchronize()
+        plan.check()
         if world > 1:
             dist.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            plan.assemble_host(hostL)
+            step_fn()
             lam_d.copy_(lam_h, non_blocking=True)
             plan.apply_global(lam_d, q_d)
             q_h.copy_(q_d, non_blocking=True)
@@ -406,10 +462,24 @@ def main():
         te = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        h2d = int(sum(8 * sd.L_values.size for sd in P.subdomains) + 8 * P.n_lambda)
-        e2e = {"value": nsub_job / (te.item() / 1e3), "unit": "subdomains/s", "ms_per_step": te.item(),
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * P.n_lambda,
-               "includes": "pinned H2D of this rank's L values + assemble + 1 sc_apply (+NCCL all-reduce) + D2H of q"}
+        return {"value": nsub_job / (te.item() / 1e3), "unit": "subdomains/s", "ms_per_step": te.item(),
+                "h2d_bytes_per_step": int(h2d_inputs + 8 * P.n_lambda), "d2h_bytes_per_step": 8 * P.n_lambda,
+                "includes": includes}
+
+    e2e = e2e_L = None
+    if not args.no_e2e:
+        hostL = [torch.from_numpy(np.ascontiguousarray(sd.L_values)).pin_memory() for sd in P.subdomains]
+        e2e_L = e2e_run(lambda: plan.assemble_host(hostL), sum(8 * sd.L_values.size for sd in P.subdomains),
+                        "pinned H2D of this rank's L values + assemble + 1 sc_apply (+NCCL all-reduce) + D2H of q")
+        del hostL
+        if factor is not None:
+            hostK = [torch.from_numpy(sd.K_lower()[2]).pin_memory() for sd in P.subdomains]
+            e2e = e2e_run(lambda: plan.factorize_assemble_host(hostK), sum(8 * k.numel() for k in hostK),
+                          "pinned H2D of this rank's K values (lower triangle) + device numeric factorization + "
+                          "assemble + 1 sc_apply (+NCCL all-reduce) + D2H of q (sc_factorize_assemble_host)")
+            del hostK
+        else:
+            e2e = e2e_L
 
     if rank != 0:
         if world > 1:
@@ -467,7 +537,7 @@ def main():
             d = t_imp - t_expl
             return int(max(t_asm - t_up, 0.0) // d) + 1 if d > 0 else None
 
-        amort = {"iters": kstar(ms_step, t_impl), "iters_e2e": kstar(e2e["ms_per_step"], t_impl) if e2e else None,
+        amort = {"iters": kstar(ms_step, t_impl), "iters_e2e": kstar(e2e_L["ms_per_step"], t_impl) if e2e_L else None,
                  "iters_vs_gpu_implicit": kstar(ms_step, t_impl_gpu, t_stage), "t_apply_implicit_gpu_ms": t_impl_gpu,
                  "t_factor_staging_gpu_ms": t_stage,
                  "implicit_gpu_vs_explicit_rel_diff": float(np.linalg.norm(q_impl_gpu - q_d.cpu().numpy()) /
@@ -503,7 +573,8 @@ def main():
         "gflops_executed": executed_job / (ms_step / 1e3) / 1e9,
         "fp64_frac_useful": useful_job / world / (ms_step / 1e3) / 1e12 / peaks["fp64_tflops"],
         "phase_ms": phases,
-        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "amortization": amort,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_from_L": e2e_L, "factor": factor,
+        "amortization": amort,
         "gpu_launches": args.steps * plan.launches_per_assemble,
         "clocks": clocks, "plan_s": t_plan, "per_config": per_config,
         "paper_context": {"a100_sep_opt_ms_per_subdomain": PAPER_A100_MS.get(args.config),

@@ -131,6 +131,14 @@ typedef struct {
   double bytes_X_reach;      /* X tile-exact: sum over RHS tiles of (rows of the panels in the tile's
                                 own reach) x T x 8 B (SURVEY §8.1 a2 "tile-exact"); the TRSM's
                                 algorithmic X bytes                                                   */
+  /* device factorization (sc_factor_attach; zero before it) */
+  double flops_factor_useful;   /* sum_k cc_k^2 over the columns of L (textbook Cholesky count)      */
+  double flops_factor_executed; /* what factor_kernel computes (dense frames, relaxed-panel zeros)    */
+  double bytes_K_values;        /* 8 nnz(K lower), summed: the factorization's compulsory input       */
+  int64_t factor_tasks;         /* warp tasks (frames) of one sc_factorize_batch                       */
+  int64_t factor_panels;        /* factor panels (<= 32 columns), summed over subdomains              */
+  int32_t factor_max_level;     /* longest elimination-tree chain of factor panels (critical path)     */
+  int32_t pad1;
 } sc_stats;
 
 /* Fill `opt` with defaults: precision 64, skip EXACT, tile/panel auto, device 0. */
@@ -175,6 +183,49 @@ sc_status sc_prepare_factor(sc_plan_t p, const void* const* L_values, void* stre
    vector lives in shared memory when n_i <= 25,600, else in plan-owned global memory.  lambda, q:
    DEVICE arrays of n_lambda_global doubles; q overwritten; deterministic. */
 sc_status sc_apply_implicit(sc_plan_t p, const double* lambda, double* q, void* stream);
+
+/* ---- Numeric factorization on the device ---------------------------------------
+   PAPER.md P:326-328 (§2.2): the factorization is done in two stages, a symbolic one (once per
+   pattern: here sc_plan_create + sc_factor_attach, on the host) and a numeric one (whenever K_i
+   changes: sc_factorize_batch, on the device); P:2563-2570 (§4.5) puts the numeric factorization at
+   about 1/2.3 of the explicit preprocessing.  Computes the L_i of sc_subdomain_desc, i.e. P K_reg,i P^T =
+   L_i L_i^T with the same pattern and CSC order, so its output feeds sc_assemble_batch unchanged, from the
+   values of K_reg,i.  Method: left-looking supernodal Cholesky over panels of <= 32 columns (its own
+   partition), one warp per 32-row frame of a panel, DMMA updates from the finished descendant panels,
+   the diagonal block factored and inverted in the warp, the rows below it multiplied by the inverse.
+   Deterministic (fixed update order, no atomics on values). */
+typedef struct {
+  const int64_t* K_colptr;   /* n+1: CSC of the LOWER triangle (diagonal included) of K_reg,i in the
+                                ORIGINAL DOF numbering (before perm), rows strictly ascending; every
+                                diagonal entry present                                              */
+  const int32_t* K_rowidx;   /* nnz(K_i) = K_colptr[n]                                               */
+} sc_K_pattern;
+
+/* Symbolic stage of the device factorization: K[i] describes subdomain i of the plan (n as in its
+   sc_subdomain_desc).  Validates that perm(K_i) lies inside the pattern of L_i (else
+   SC_ERR_PATTERN), that subdomains of one pattern class share the K pattern (else SC_ERR_PATTERN),
+   builds the factor panels, update lists and the task order (topological: by elimination-tree level
+   within chunks of subdomains), uploads them and allocates the factor workspace (sc_stats
+   device_bytes grows).  The caller may free K after the call.  Calling it again replaces the
+   previous factorization plan.  On a host-only plan (device < 0) only the symbolic stage runs (its
+   sc_stats counters are filled; sc_factorize_* then return SC_ERR_STATE). */
+sc_status sc_factor_attach(sc_plan_t p, const sc_K_pattern* K, int32_t nsub);
+
+/* Numeric factorization: K_values: HOST array of nsub DEVICE pointers, K_values[i] -> nnz(K_i)
+   doubles in the order of K[i].K_rowidx; L_values: HOST array of nsub DEVICE pointers receiving
+   nnz(L_i) values (double, or float for precision 32; arithmetic FP64) in the CSC order of
+   sd[i].L_colptr/L_rowidx; entries of L that are structurally zero in the panel are written as 0.
+   A non-positive or non-finite pivot raises the plan's sticky SC_ERR_ZERO_PIVOT (reset by the next
+   factorize / assemble); that subdomain's L is undefined.  Enqueued on `stream`, no synchronisation.
+   SC_ERR_STATE without sc_factor_attach. */
+sc_status sc_factorize_batch(sc_plan_t p, const void* const* K_values, void* const* L_values, void* stream);
+
+/* Host-fed end-to-end preprocessing: K values in HOST memory (ideally pinned) -> H2D copy of K (about
+   nnz(K lower) / nnz(L) of the bytes sc_assemble_batch_host moves) -> device factorization into a
+   plan-owned L buffer -> assembly of every F_i.  Pipelined over chunks of subdomains (copies of chunk
+   k on a plan-owned copy stream while chunk k-1 factorizes and assembles on `stream`).  The host
+   arrays must stay valid until `stream` completes.  Does not synchronise. */
+sc_status sc_factorize_assemble_host(sc_plan_t p, const void* const* K_values_host, void* stream);
 
 /* ---- Solution stage: PCPG on the FETI dual problem -------------------------------
    Solves  [F -G; -G^T O] [lambda; alpha] = [d; -e]  (eq. tfetidualproblem) by the

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsc_b200.so")
-SOURCES = ["plan.cpp", "kernels.cu", "pcpg.cu", "api.cpp"]
+SOURCES = ["plan.cpp", "factor_plan.cpp", "kernels.cu", "factor.cu", "pcpg.cu", "api.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

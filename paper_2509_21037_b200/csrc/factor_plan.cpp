@@ -1,0 +1,305 @@
+// factor_plan.cpp — symbolic stage of the device numeric factorization.
+//
+// PAPER.md P:326-328 (§2.2): "the factorization is done in two stages: the symbolic factorization
+// ... performed only once ... and the numeric factorization" whenever the values change.  The
+// pattern of L_i is already known (sc_plan_create validated it as a Cholesky fill pattern); this
+// file derives, per pattern class, what the left-looking supernodal numeric factorization in
+// factor.cu needs:
+//   1. factor panels of <= 32 columns (partition_panels: maximal supernodes, wide ones split, small
+//      consecutive ones merged; rows below each panel R_p);
+//   2. per panel p the list of descendant panels d that update it (R_d meets the columns of p), with
+//      the index ranges of R_d inside p's columns [s0, s1) and below them [s1, nR_d);
+//   3. levels (0 = no descendant, else 1 + max over the descendants) and frames: the diagonal block
+//      plus one frame per 32 rows of R_p -- one warp task each;
+//   4. K entries -> frame positions (perm applied, each entry moved to the lower triangle of
+//      P K P^T; an entry outside the pattern of L is a pattern error) and L entries -> frame
+//      positions (the output scatter in the caller's CSC order);
+//   5. the task order: chunks of subdomains, inside a chunk by (level, subdomain, panel, frame), so
+//      every dependency precedes its dependants in the queue (the kernel's deadlock-freedom argument).
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "sc_internal.h"
+
+namespace sc {
+
+namespace {
+
+#define FFAIL(code, msg) \
+  do {                   \
+    err = (msg);         \
+    return (code);       \
+  } while (0)
+
+sc_status analyse_factor_class(const ClassPlan& C, const sc_K_pattern& K, FactorClass& F, std::string& err) {
+  const int32_t n = C.n;
+  const int64_t* cp = C.colptr.data();
+  const int32_t* ri = C.rowidx.data();
+  std::vector<int32_t> parent((size_t)n, -1);
+  for (int32_t c = 0; c < n; c++)
+    if (cp[c + 1] - cp[c] > 1) parent[(size_t)c] = ri[cp[c] + 1];
+  std::vector<PanelPart> parts;
+  partition_panels(n, cp, ri, parent, kFW, parts);
+  std::vector<int32_t> poc((size_t)n, -1);
+  for (size_t k = 0; k < parts.size(); k++) {
+    FPanel p{};
+    p.a = parts[k].a;
+    p.kw = parts[k].b - parts[k].a;
+    p.kw8 = (p.kw + 7) & ~7;
+    p.nR = (int32_t)parts[k].R.size();
+    p.R_off = (int32_t)F.Rrows.size();
+    F.Rrows.insert(F.Rrows.end(), parts[k].R.begin(), parts[k].R.end());
+    for (int32_t c = p.a; c < parts[k].b; c++) poc[(size_t)c] = (int32_t)k;
+    F.panels.push_back(p);
+  }
+  const int32_t np = (int32_t)F.panels.size();
+  // 2. update lists: walk R_d and group its rows by the panel they fall in
+  std::vector<std::vector<FUpd>> lists((size_t)np);
+  for (int32_t d = 0; d < np; d++) {
+    const FPanel& dn = F.panels[(size_t)d];
+    const int32_t* R = F.Rrows.data() + dn.R_off;
+    int32_t k = 0;
+    while (k < dn.nR) {
+      const int32_t p = poc[(size_t)R[k]];
+      const int32_t b = F.panels[(size_t)p].a + F.panels[(size_t)p].kw;
+      const int32_t s0 = k;
+      while (k < dn.nR && R[k] < b) k++;
+      lists[(size_t)p].push_back(FUpd{d, s0, k, 0});
+    }
+  }
+  // 3. levels, frames, workspace layout, flop counts
+  int64_t w = 0;
+  for (int32_t p = 0; p < np; p++) {
+    FPanel& pn = F.panels[(size_t)p];
+    pn.upd_begin = (int32_t)F.upd.size();
+    int32_t lev = 0;
+    for (const FUpd& u : lists[(size_t)p]) {
+      lev = std::max(lev, F.panels[(size_t)u.d].level + 1);
+      F.upd.push_back(u);
+      const FPanel& dn = F.panels[(size_t)u.d];
+      // executed: rows of d in this panel and below x columns of d in this panel x 2 kw_d
+      F.flops += 2.0 * dn.kw * (double)(dn.nR - u.s0) * (double)(u.s1 - u.s0);
+    }
+    pn.upd_end = (int32_t)F.upd.size();
+    pn.level = lev;
+    F.max_level = std::max(F.max_level, lev);
+    pn.frame_begin = (int32_t)F.frames.size();
+    pn.nframe = 1 + (pn.nR + kFW - 1) / kFW;
+    for (int32_t f = 0; f < pn.nframe; f++) {
+      FFrame fr{};
+      fr.panel = p;
+      fr.r0 = f == 0 ? -1 : (f - 1) * kFW;
+      fr.nrow = f == 0 ? pn.kw : std::min(kFW, pn.nR - (f - 1) * kFW);
+      F.frames.push_back(fr);
+    }
+    pn.w_off = w;
+    w += (int64_t)pn.nR * pn.kw;
+    pn.inv_off = w;
+    w += (int64_t)pn.kw8 * pn.kw8;
+    F.flops += (double)pn.kw * pn.kw * pn.kw / 3.0 * 2.0 + 2.0 * pn.nR * (double)pn.kw * pn.kw;
+  }
+  F.w_doubles = w;
+  for (int32_t c = 0; c < n; c++) {
+    const double cc = (double)(cp[c + 1] - cp[c]);
+    F.flops_useful += cc * cc;
+  }
+  // 4. entry maps
+  std::vector<int32_t> iperm((size_t)n);
+  for (int32_t k = 0; k < n; k++) iperm[(size_t)C.perm[(size_t)k]] = k;
+  auto locate = [&](int32_t r, int32_t c, int32_t& frame, int32_t& pos) -> bool {  // r >= c, permuted
+    const int32_t p = poc[(size_t)c];
+    const FPanel& pn = F.panels[(size_t)p];
+    if (r < pn.a + pn.kw) {
+      frame = pn.frame_begin;
+      pos = (r - pn.a) * kFW + (c - pn.a);
+      return true;
+    }
+    const int32_t* R = F.Rrows.data() + pn.R_off;
+    const int32_t k = (int32_t)(std::lower_bound(R, R + pn.nR, r) - R);
+    if (k >= pn.nR || R[k] != r) return false;
+    frame = pn.frame_begin + 1 + k / kFW;
+    pos = (k % kFW) * kFW + (c - pn.a);
+    return true;
+  };
+  const int64_t nK = K.K_colptr[n];
+  F.nnzK = nK;
+  std::vector<std::vector<FEnt>> kf(F.frames.size()), lf(F.frames.size());
+  for (int32_t j = 0; j < n; j++)
+    for (int64_t q = K.K_colptr[j]; q < K.K_colptr[j + 1]; q++) {
+      const int32_t i = K.K_rowidx[q];
+      const int32_t pi = iperm[(size_t)i], pj = iperm[(size_t)j];
+      const int32_t r = std::max(pi, pj), c = std::min(pi, pj);
+      int32_t fr, pos;
+      const bool inL = std::binary_search(ri + cp[c], ri + cp[c + 1], r);
+      if (!inL || !locate(r, c, fr, pos))
+        FFAIL(SC_ERR_PATTERN, "K entry (" + std::to_string(i) + ", " + std::to_string(j) +
+                                  ") lies outside the pattern of L (permuted (" + std::to_string(r) + ", " +
+                                  std::to_string(c) + "))");
+      kf[(size_t)fr].push_back(FEnt{(int32_t)q, pos});
+    }
+  for (int32_t c = 0; c < n; c++)
+    for (int64_t q = cp[c]; q < cp[c + 1]; q++) {
+      int32_t fr, pos;
+      if (!locate(ri[q], c, fr, pos)) FFAIL(SC_ERR_PATTERN, "internal: L entry outside its factor panel");
+      lf[(size_t)fr].push_back(FEnt{(int32_t)q, pos});
+    }
+  std::vector<int32_t> mark((size_t)kFW * kFW, -1);
+  for (size_t f = 0; f < F.frames.size(); f++) {
+    for (const FEnt& e : kf[f]) {  // each lower position of P K P^T at most once (no duplicate entries)
+      if (mark[(size_t)e.pos] == (int32_t)f) FFAIL(SC_ERR_PATTERN, "K has a duplicate entry (after perm / transpose)");
+      mark[(size_t)e.pos] = (int32_t)f;
+    }
+    F.frames[f].k_begin = (int32_t)F.kent.size();
+    F.kent.insert(F.kent.end(), kf[f].begin(), kf[f].end());
+    F.frames[f].k_end = (int32_t)F.kent.size();
+    F.frames[f].l_begin = (int32_t)F.lent.size();
+    F.lent.insert(F.lent.end(), lf[f].begin(), lf[f].end());
+    F.frames[f].l_end = (int32_t)F.lent.size();
+  }
+  // every diagonal of P K P^T must be present (a missing one is a structurally singular K)
+  {
+    std::vector<char> hasd((size_t)n, 0);
+    for (int32_t j = 0; j < n; j++)
+      for (int64_t q = K.K_colptr[j]; q < K.K_colptr[j + 1]; q++)
+        if (K.K_rowidx[q] == j) hasd[(size_t)j] = 1;
+    for (int32_t j = 0; j < n; j++)
+      if (!hasd[(size_t)j]) FFAIL(SC_ERR_PATTERN, "K diagonal entry " + std::to_string(j) + " missing");
+  }
+  return SC_OK;
+}
+
+sc_status validate_K(const sc_K_pattern& K, int32_t n, int32_t i, std::string& err) {
+  const std::string who = "subdomain " + std::to_string(i) + ": ";
+  if (!K.K_colptr || (n > 0 && !K.K_rowidx)) FFAIL(SC_ERR_INVALID_ARG, who + "NULL K pattern");
+  if (K.K_colptr[0] != 0) FFAIL(SC_ERR_PATTERN, who + "K_colptr[0] != 0");
+  if (K.K_colptr[n] > INT32_MAX) FFAIL(SC_ERR_INVALID_ARG, who + "nnz(K) exceeds 2^31");
+  for (int32_t j = 0; j < n; j++) {
+    if (K.K_colptr[j + 1] < K.K_colptr[j]) FFAIL(SC_ERR_PATTERN, who + "K_colptr not monotone");
+    for (int64_t q = K.K_colptr[j]; q < K.K_colptr[j + 1]; q++) {
+      const int32_t r = K.K_rowidx[q];
+      if (r < j || r >= n) FFAIL(SC_ERR_PATTERN, who + "K entry not in the lower triangle / out of range");
+      if (q > K.K_colptr[j] && r <= K.K_rowidx[q - 1]) FFAIL(SC_ERR_PATTERN, who + "K rows not strictly ascending");
+    }
+  }
+  return SC_OK;
+}
+
+bool same_K(const sc_K_pattern& a, const sc_K_pattern& b, int32_t n) {
+  if (a.K_colptr[n] != b.K_colptr[n]) return false;
+  if (std::memcmp(a.K_colptr, b.K_colptr, sizeof(int64_t) * (size_t)(n + 1)) != 0) return false;
+  return a.K_rowidx == b.K_rowidx ||
+         std::memcmp(a.K_rowidx, b.K_rowidx, sizeof(int32_t) * (size_t)a.K_colptr[n]) == 0;
+}
+
+}  // namespace
+
+sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::string& err) {
+  if (nsub != P.nsub) FFAIL(SC_ERR_INVALID_ARG, "sc_factor_attach: nsub differs from the plan's");
+  if (nsub > 0 && !kp) FFAIL(SC_ERR_INVALID_ARG, "sc_factor_attach: NULL K");
+  FactorPlan& F = P.fac;
+  const int32_t ncls = (int32_t)P.classes.size();
+  std::vector<int32_t> rep((size_t)ncls, -1);
+  for (int32_t i = 0; i < nsub; i++) {
+    const int32_t c = P.sub_cls[(size_t)i];
+    sc_status st = validate_K(kp[i], P.sub_n[(size_t)i], i, err);
+    if (st != SC_OK) return st;
+    if (rep[(size_t)c] < 0) {
+      rep[(size_t)c] = i;
+    } else if (!same_K(kp[rep[(size_t)c]], kp[i], P.sub_n[(size_t)i])) {
+      FFAIL(SC_ERR_PATTERN, "subdomain " + std::to_string(i) + ": K pattern differs from subdomain " +
+                                std::to_string(rep[(size_t)c]) + " of the same L/B pattern class");
+    }
+  }
+  F.classes.assign((size_t)ncls, FactorClass());
+  for (int32_t c = 0; c < ncls; c++) {
+    if (rep[(size_t)c] < 0) continue;
+    sc_status st = analyse_factor_class(P.classes[(size_t)c], kp[rep[(size_t)c]], F.classes[(size_t)c], err);
+    if (st != SC_OK) {
+      err = "subdomain " + std::to_string(rep[(size_t)c]) + ": " + err;
+      return st;
+    }
+  }
+  // globalise
+  F.panels.clear();
+  F.Rrows.clear();
+  F.upd.clear();
+  F.frames.clear();
+  F.kent.clear();
+  F.lent.clear();
+  F.cls_panel0.assign((size_t)ncls + 1, 0);
+  for (int32_t c = 0; c < ncls; c++) {
+    const FactorClass& fc = F.classes[(size_t)c];
+    const int32_t p0 = (int32_t)F.panels.size(), r0 = (int32_t)F.Rrows.size(), u0 = (int32_t)F.upd.size();
+    const int32_t f0 = (int32_t)F.frames.size(), k0 = (int32_t)F.kent.size(), l0 = (int32_t)F.lent.size();
+    F.cls_panel0[(size_t)c] = p0;
+    for (FPanel pn : fc.panels) {
+      pn.R_off += r0;
+      pn.upd_begin += u0;
+      pn.upd_end += u0;
+      pn.frame_begin += f0;
+      F.panels.push_back(pn);
+    }
+    F.Rrows.insert(F.Rrows.end(), fc.Rrows.begin(), fc.Rrows.end());
+    for (FUpd u : fc.upd) {
+      u.d += p0;
+      F.upd.push_back(u);
+    }
+    for (FFrame fr : fc.frames) {
+      fr.panel += p0;
+      fr.k_begin += k0;
+      fr.k_end += k0;
+      fr.l_begin += l0;
+      fr.l_end += l0;
+      F.frames.push_back(fr);
+    }
+    F.kent.insert(F.kent.end(), fc.kent.begin(), fc.kent.end());
+    F.lent.insert(F.lent.end(), fc.lent.begin(), fc.lent.end());
+  }
+  F.cls_panel0[(size_t)ncls] = (int32_t)F.panels.size();
+  // per-subdomain workspace and flags
+  F.sub_W_base.assign((size_t)nsub + 1, 0);
+  F.sub_flag_base.assign((size_t)nsub + 1, 0);
+  F.sub_nnzK.assign((size_t)nsub, 0);
+  F.flops = F.flops_useful = F.bytes_K = 0;
+  for (int32_t i = 0; i < nsub; i++) {
+    const FactorClass& fc = F.classes[(size_t)P.sub_cls[(size_t)i]];
+    F.sub_W_base[(size_t)i + 1] = F.sub_W_base[(size_t)i] + fc.w_doubles;
+    F.sub_flag_base[(size_t)i + 1] = F.sub_flag_base[(size_t)i] + (int64_t)fc.panels.size();
+    F.sub_nnzK[(size_t)i] = fc.nnzK;
+    F.flops += fc.flops;
+    F.flops_useful += fc.flops_useful;
+    F.bytes_K += 8.0 * (double)fc.nnzK;
+  }
+  F.W_doubles = F.sub_W_base[(size_t)nsub];
+  F.nflags = F.sub_flag_base[(size_t)nsub];
+  // 5. task order: chunks of subdomains (the host-fed pipeline's granularity, also an L2-locality
+  // window), inside a chunk by (level, subdomain, panel, frame)
+  const int32_t nchunk = std::max<int32_t>(1, std::min<int32_t>(16, nsub / 64));
+  F.chunk_sub.assign((size_t)nchunk + 1, 0);
+  F.task_chunk.assign((size_t)nchunk + 1, 0);
+  F.tasks.clear();
+  for (int32_t k = 0; k < nchunk; k++) {
+    const int32_t s0 = (int32_t)((int64_t)nsub * k / nchunk), s1 = (int32_t)((int64_t)nsub * (k + 1) / nchunk);
+    F.chunk_sub[(size_t)k] = s0;
+    F.chunk_sub[(size_t)k + 1] = s1;
+    int32_t maxlev = 0;
+    for (int32_t i = s0; i < s1; i++) maxlev = std::max(maxlev, F.classes[(size_t)P.sub_cls[(size_t)i]].max_level);
+    for (int32_t lev = 0; lev <= maxlev; lev++)
+      for (int32_t i = s0; i < s1; i++) {
+        const int32_t c = P.sub_cls[(size_t)i];
+        const int32_t p0 = F.cls_panel0[(size_t)c], p1 = F.cls_panel0[(size_t)c + 1];
+        for (int32_t p = p0; p < p1; p++) {
+          const FPanel& pn = F.panels[(size_t)p];
+          if (pn.level != lev) continue;
+          for (int32_t f = 0; f < pn.nframe; f++) F.tasks.push_back(FTask{i, pn.frame_begin + f});
+        }
+      }
+    F.task_chunk[(size_t)k + 1] = (int64_t)F.tasks.size();
+  }
+  if (F.tasks.size() > (size_t)INT32_MAX) FFAIL(SC_ERR_INVALID_ARG, "too many factorization tasks");
+  return SC_OK;
+}
+
+}  // namespace sc

@@ -1793,6 +1793,7 @@ void free_plan_device(Plan& P) {
   if (P.opt.device < 0) return;
   cudaSetDevice(P.opt.device);
   cudaDeviceSynchronize();
+  free_factor_device(P);
   for (void* p : P.allocations) cudaFree(p);
   P.allocations.clear();
   if (P.h_Lptr_pinned) cudaFreeHost((void*)P.h_Lptr_pinned);
@@ -2030,14 +2031,10 @@ sc_status launch_assemble(Plan& P, const void* const* Lptr_host, void* stream_v,
 // subdomains; chunk k's pinned-host -> device copies run on a plan-owned copy stream while the
 // kernels of chunk k-1 run on `stream` (one event per chunk), so the H2D transfer (PCIe-bound) hides
 // the assembly.
-sc_status assemble_host_pipelined(Plan& P, const void* const* Lhost, void* stream_v, std::string& err) {
+// Plan-owned device staging of every subdomain's L values (host-fed paths): allocate it once, point
+// the plan's L table at it, reset the sticky errors.  dptrs receives the per-subdomain staging pointers.
+sc_status assemble_stage_begin(Plan& P, std::vector<void*>& dptrs, void* stream_v, std::string& err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
-  CUDA_TRY(cudaSetDevice(P.opt.device));
-  for (int32_t i = 0; i < P.nsub; i++)
-    if (P.sub_nnz[(size_t)i] > 0 && !Lhost[i]) {
-      err = "L_values_host[" + std::to_string(i) + "] is NULL";
-      return SC_ERR_INVALID_ARG;
-    }
   if (!P.d_Lstage) {
     P.Lstage_off.assign((size_t)P.nsub + 1, 0);
     for (int32_t i = 0; i < P.nsub; i++) P.Lstage_off[(size_t)i + 1] = P.Lstage_off[(size_t)i] + P.sub_nnz[(size_t)i];
@@ -2049,40 +2046,59 @@ sc_status assemble_host_pipelined(Plan& P, const void* const* Lhost, void* strea
     CUDA_TRY(cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&P.copy_stream), cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(&P.ev_start), cudaEventDisableTiming));
   }
+  dptrs.assign((size_t)P.nsub, nullptr);
+  for (int32_t i = 0; i < P.nsub; i++) dptrs[(size_t)i] = static_cast<char*>(P.d_Lstage) + P.esz * P.Lstage_off[(size_t)i];
+  std::vector<const void*> cp(dptrs.begin(), dptrs.end());
+  sc_status st = set_Lptr(P, cp.data(), stream, err);
+  if (st != SC_OK) return st;
+  P.last_stream = stream_v;
+  P.factor_ready = !P.warp_trsm;  // the warp TRSM does not stage the factor panels
+  CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
+  return SC_OK;
+}
+
+sc_status assemble_range(Plan& P, int32_t s0, int32_t s1, void* stream, std::string& err) {
+  return launch_range(P, s0, s1, static_cast<cudaStream_t>(stream), false, err);
+}
+
+sc_status assemble_host_pipelined(Plan& P, const void* const* Lhost, void* stream_v, std::string& err) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  CUDA_TRY(cudaSetDevice(P.opt.device));
+  for (int32_t i = 0; i < P.nsub; i++)
+    if (P.sub_nnz[(size_t)i] > 0 && !Lhost[i]) {
+      err = "L_values_host[" + std::to_string(i) + "] is NULL";
+      return SC_ERR_INVALID_ARG;
+    }
+  std::vector<void*> dptrs;
+  sc_status st = assemble_stage_begin(P, dptrs, stream_v, err);
+  if (st != SC_OK) return st;
   const int32_t nchunk = std::max<int32_t>(1, std::min<int32_t>(16, P.nsub / 64));
   while ((int32_t)P.ev_chunk.size() < nchunk) {
     cudaEvent_t e;
     CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     P.ev_chunk.push_back(e);
   }
-  std::vector<const void*> dptrs((size_t)P.nsub);
-  for (int32_t i = 0; i < P.nsub; i++) dptrs[(size_t)i] = static_cast<char*>(P.d_Lstage) + P.esz * P.Lstage_off[(size_t)i];
-  sc_status st = set_Lptr(P, dptrs.data(), stream, err);
-  if (st != SC_OK) return st;
-  P.last_stream = stream_v;
-  P.factor_ready = !P.warp_trsm;  // the warp TRSM does not stage the factor panels
-  CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream);
   // the staging buffer is reused: copies wait for everything enqueued on `stream` before this call
   CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_start), stream));
   CUDA_TRY(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(P.ev_start), 0));
   for (int32_t k = 0; k < nchunk; k++) {
     const int32_t s0 = (int32_t)((int64_t)P.nsub * k / nchunk), s1 = (int32_t)((int64_t)P.nsub * (k + 1) / nchunk);
-    // one batched call per chunk (per-copy launch overhead would otherwise cap the PCIe rate)
-    std::vector<void*> dsts, srcs;
-    std::vector<size_t> sizes;
-    for (int32_t i = s0; i < s1; i++)
-      if (P.sub_nnz[(size_t)i] > 0) {
-        dsts.push_back(static_cast<char*>(P.d_Lstage) + P.esz * P.Lstage_off[(size_t)i]);
-        srcs.push_back(const_cast<void*>(Lhost[i]));
-        sizes.push_back((size_t)P.esz * (size_t)P.sub_nnz[(size_t)i]);
+    // one cudaMemcpyAsync per run of host-contiguous subdomains (the staging side is contiguous)
+    int32_t i = s0;
+    while (i < s1) {
+      if (P.sub_nnz[(size_t)i] == 0) { i++; continue; }
+      const char* src = static_cast<const char*>(Lhost[i]);
+      size_t bytes = (size_t)P.esz * (size_t)P.sub_nnz[(size_t)i];
+      int32_t j = i + 1;
+      while (j < s1 && P.sub_nnz[(size_t)j] > 0 && static_cast<const char*>(Lhost[j]) == src + bytes &&
+             P.Lstage_off[(size_t)j] == P.Lstage_off[(size_t)i] + (int64_t)(bytes / P.esz)) {
+        bytes += (size_t)P.esz * (size_t)P.sub_nnz[(size_t)j];
+        j++;
       }
-    if (!dsts.empty()) {
-      cudaMemcpyAttributes attr{};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-      size_t attr_idx = 0, fail_idx = 0;
-      CUDA_TRY(cudaMemcpyBatchAsync(dsts.data(), srcs.data(), sizes.data(), dsts.size(), &attr, &attr_idx, 1, &fail_idx, cs));
+      CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(P.d_Lstage) + P.esz * P.Lstage_off[(size_t)i], src, bytes,
+                               cudaMemcpyHostToDevice, cs));
+      i = j;
     }
     cudaEvent_t e = static_cast<cudaEvent_t>(P.ev_chunk[(size_t)k]);
     CUDA_TRY(cudaEventRecord(e, cs));

@@ -126,36 +126,16 @@ int relax_wsmall() {
   return e ? std::atoi(e) : 16;
 }
 
-// Steps 2-7 for one class.
-sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, int skip, bool gstrip,
-                        int32_t strip_limit, bool warp, ClassPlan& C, std::string& err) {
-  const int32_t n = d.n, m = d.m;
-  C.n = n;
-  C.m = m;
-  C.colptr.assign(d.L_colptr, d.L_colptr + n + 1);
-  C.perm.resize((size_t)n);
-  for (int32_t k = 0; k < n; k++) C.perm[(size_t)k] = d.perm ? d.perm[k] : k;
-  const int64_t* cp = d.L_colptr;
-  const int32_t* ri = d.L_rowidx;
-  auto cc = [&](int32_t c) { return (int32_t)(cp[c + 1] - cp[c]); };
+}  // namespace
 
-  // --- 2. etree + closure check + maximal supernodes
-  std::vector<int32_t> parent((size_t)n, -1);
-  for (int32_t c = 0; c < n; c++)
-    if (cc(c) > 1) parent[(size_t)c] = ri[cp[c] + 1];
-  {
-    // struct(c) \ {c, parent(c)} must be a subset of struct(parent(c)) (Cholesky fill pattern)
-    std::vector<int32_t> mark((size_t)n, -1);
-    for (int32_t c = 0; c < n; c++) {
-      int32_t p = parent[(size_t)c];
-      if (p < 0) continue;
-      for (int64_t q = cp[p]; q < cp[p + 1]; q++) mark[(size_t)ri[q]] = c;
-      for (int64_t q = cp[c] + 2; q < cp[c + 1]; q++)
-        if (mark[(size_t)ri[q]] != c)
-          FAIL(SC_ERR_PATTERN, "L pattern is not a Cholesky fill pattern (column " + std::to_string(c) +
-                                   " row " + std::to_string(ri[q]) + " not in the structure of its etree parent)");
-    }
-  }
+// Maximal supernodes (chains j -> j+1 with equal row structure below) cut into factor panels of <= PW
+// columns: wide supernodes split evenly, runs of small consecutive supernodes merged into one dense
+// panel while the merged trapezoid stays mostly non-zero (<= SC_RELAX_ZMAX explicit zeros) or tiny
+// (<= SC_RELAX_WSMALL columns) -- relaxed amalgamation.  R = the panel's pruned below-diagonal rows
+// (P:494), the union of its columns' rows below the panel.  Returns the number of supernodes.
+int32_t partition_panels(int32_t n, const int64_t* cp, const int32_t* ri, const std::vector<int32_t>& parent, int PW,
+                         std::vector<PanelPart>& out) {
+  auto cc = [&](int32_t c) { return (int32_t)(cp[c + 1] - cp[c]); };
   std::vector<int32_t> sn_c0, sn_c1;
   for (int32_t c = 0; c < n;) {
     int32_t c0 = c;
@@ -164,41 +144,20 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     sn_c0.push_back(c0);
     sn_c1.push_back(c);
   }
-  C.nsup = (int32_t)sn_c0.size();
-
-  // --- panels: split wide supernodes at PW columns, merge runs of small consecutive supernodes
-  // while the merged dense trapezoid stays mostly non-zero (or tiny)
+  const int32_t nsup = (int32_t)sn_c0.size();
   const double zmax = relax_zmax();
   const int wsmall = relax_wsmall();
-  struct Open {
-    int32_t a = -1, b = -1, merged = 0;
-    std::vector<int32_t> R;
-    double nnz = 0;
-  } open;
-  std::vector<int32_t> panel_of_col((size_t)n, -1);
+  PanelPart open;
+  double open_nnz = 0;
   auto close_open = [&]() {
     if (open.a < 0) return;
-    Panel p{};
-    p.a = open.a;
-    p.kw = open.b - open.a;
-    p.relaxed = open.merged;
-    p.nR = (int32_t)open.R.size();
-    p.R_off = (int32_t)C.Rrows.size();
-    C.Rrows.insert(C.Rrows.end(), open.R.begin(), open.R.end());
-    for (int32_t c = open.a; c < open.b; c++) panel_of_col[(size_t)c] = (int32_t)C.panels.size();
-    C.panels.push_back(p);
-    open = Open();
+    out.push_back(open);
+    open = PanelPart();
+    open_nnz = 0;
   };
-  auto snode_R = [&](int32_t c0, int32_t c1) {  // rows of the supernode's columns below c1
-    std::vector<int32_t> R;
-    int32_t last = c1 - 1;
-    for (int64_t q = cp[last] + 1; q < cp[last + 1]; q++) R.push_back(ri[q]);
-    (void)c0;
-    return R;
-  };
-  for (int32_t s = 0; s < C.nsup; s++) {
+  for (int32_t s = 0; s < nsup; s++) {
     const int32_t c0 = sn_c0[(size_t)s], c1 = sn_c1[(size_t)s], w = c1 - c0;
-    std::vector<int32_t> Rs = snode_R(c0, c1);
+    std::vector<int32_t> Rs(ri + cp[c1 - 1] + 1, ri + cp[c1]);  // rows of the supernode below c1
     double nnz_s = 0;
     for (int32_t c = c0; c < c1; c++) nnz_s += cc(c);
     if (w > PW) {
@@ -225,12 +184,12 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
       std::set_union(tail.begin(), tail.end(), Rs.begin(), Rs.end(), std::back_inserter(R2));
       const double w2 = (double)(c1 - open.a);
       const double dense = w2 * (w2 + 1) / 2 + w2 * (double)R2.size();
-      const double nnz2 = open.nnz + nnz_s;
+      const double nnz2 = open_nnz + nnz_s;
       const double zf = 1.0 - nnz2 / dense;
       if (w2 <= PW && (zf <= zmax || w2 <= wsmall)) {
         open.b = c1;
         open.R.swap(R2);
-        open.nnz = nnz2;
+        open_nnz = nnz2;
         open.merged = 1;
         continue;
       }
@@ -239,9 +198,60 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
     open.a = c0;
     open.b = c1;
     open.R = Rs;
-    open.nnz = nnz_s;
+    open_nnz = nnz_s;
   }
   close_open();
+  return nsup;
+}
+
+namespace {
+
+// Steps 2-7 for one class.
+sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, int skip, bool gstrip,
+                        int32_t strip_limit, bool warp, ClassPlan& C, std::string& err) {
+  const int32_t n = d.n, m = d.m;
+  C.n = n;
+  C.m = m;
+  C.colptr.assign(d.L_colptr, d.L_colptr + n + 1);
+  C.rowidx.assign(d.L_rowidx, d.L_rowidx + d.L_colptr[n]);
+  C.perm.resize((size_t)n);
+  for (int32_t k = 0; k < n; k++) C.perm[(size_t)k] = d.perm ? d.perm[k] : k;
+  const int64_t* cp = d.L_colptr;
+  const int32_t* ri = d.L_rowidx;
+  auto cc = [&](int32_t c) { return (int32_t)(cp[c + 1] - cp[c]); };
+
+  // --- 2. etree + closure check + maximal supernodes
+  std::vector<int32_t> parent((size_t)n, -1);
+  for (int32_t c = 0; c < n; c++)
+    if (cc(c) > 1) parent[(size_t)c] = ri[cp[c] + 1];
+  {
+    // struct(c) \ {c, parent(c)} must be a subset of struct(parent(c)) (Cholesky fill pattern)
+    std::vector<int32_t> mark((size_t)n, -1);
+    for (int32_t c = 0; c < n; c++) {
+      int32_t p = parent[(size_t)c];
+      if (p < 0) continue;
+      for (int64_t q = cp[p]; q < cp[p + 1]; q++) mark[(size_t)ri[q]] = c;
+      for (int64_t q = cp[c] + 2; q < cp[c + 1]; q++)
+        if (mark[(size_t)ri[q]] != c)
+          FAIL(SC_ERR_PATTERN, "L pattern is not a Cholesky fill pattern (column " + std::to_string(c) +
+                                   " row " + std::to_string(ri[q]) + " not in the structure of its etree parent)");
+    }
+  }
+  std::vector<PanelPart> parts;
+  C.nsup = partition_panels(n, cp, ri, parent, PW, parts);
+  for (auto& pp : parts) {
+    Panel p{};
+    p.a = pp.a;
+    p.kw = pp.b - pp.a;
+    p.relaxed = pp.merged;
+    p.nR = (int32_t)pp.R.size();
+    p.R_off = (int32_t)C.Rrows.size();
+    C.Rrows.insert(C.Rrows.end(), pp.R.begin(), pp.R.end());
+    C.panels.push_back(p);
+  }
+  std::vector<int32_t> panel_of_col((size_t)n, -1);
+  for (size_t k = 0; k < C.panels.size(); k++)
+    for (int32_t c = C.panels[k].a; c < C.panels[k].a + C.panels[k].kw; c++) panel_of_col[(size_t)c] = (int32_t)k;
 
   // --- panel-buffer layout and the CSC -> panel-buffer scatter map
   int64_t pb = 0;

@@ -163,6 +163,7 @@ struct ClassPlan {
   int32_t n = 0, m = 0, nsup = 0;
   uint64_t hash = 0;
   std::vector<int64_t> colptr;     // copy of L_colptr (n+1)
+  std::vector<int32_t> rowidx;     // copy of L_rowidx (nnz(L)): the device factorization's symbolic input
   std::vector<int32_t> perm;       // perm[new] = old
   std::vector<int32_t> dest;       // per CSC entry: >= 0 panel-buffer offset (below rows),
                                    //   < 0: -1 - (col_in_panel * 64 + row_in_panel) (triangle)
@@ -190,6 +191,98 @@ struct ClassPlan {
   double fl_trsm_dense = 0, fl_syrk_dense = 0, fl_trsm_sparse = 0;
   double fl_trsm_exec = 0, fl_syrk_exec = 0, fl_prep_exec = 0;
   double x_reach_doubles = 0;      // sum over tiles of own-reach rows x T
+};
+
+// ---- Numeric factorization on the device (§2.2 "two-stage
+// factorization": symbolic once, numeric whenever K changes).  Left-looking supernodal Cholesky of
+// P K_reg P^T over factor panels of <= 32 columns (a partition of its own, independent of the TRSM's).
+constexpr int kFW = 32;         // factor panel width cap = frame rows = frame columns
+// Factor panel: columns [a, a+kw), below-diagonal rows R = fRrows[R_off .. R_off+nR) (ascending).
+// Workspace per subdomain (doubles from the subdomain's base): the finished L[R, panel] at w_off
+// (nR x kw, column-major, ld nR) and inv(L_pp) at inv_off (kw8 x kw8, column-major, zero padded).
+struct FPanel {
+  int32_t a, kw, nR, R_off;
+  int32_t upd_begin, upd_end;      // descendant updates of this panel (global indices into fupd)
+  int32_t frame_begin, nframe;     // 1 diagonal frame + ceil(nR / 32) row frames (global indices)
+  int64_t w_off, inv_off;
+  int32_t level, kw8;              // level: 0 = no descendants, else 1 + max over its descendants
+};
+// Descendant panel d updates panel p: rows R_d[s0, s1) lie in [a_p, a_p + kw_p) (the columns of p),
+// rows R_d[s1, nR_d) below it (a subset of R_p by the closure of the fill pattern).
+struct FUpd {
+  int32_t d, s0, s1, pad;          // d: global factor-panel index
+};
+// Frame = one warp task: the diagonal block (r0 = -1, rows = the panel's columns) or 32 consecutive
+// rows R_p[r0, r0 + nrow) of a panel.  K / L entries of the frame: (value index within the subdomain's
+// CSC array, frame position row * 32 + col).
+struct FFrame {
+  int32_t panel, r0, nrow, pad;
+  int32_t k_begin, k_end, l_begin, l_end;
+};
+struct FEnt {
+  int32_t q, pos;
+};
+struct FTask {
+  int32_t sub, frame;              // frame: global index
+};
+
+// Host symbolic data of the device factorization, per pattern class.
+struct FactorClass {
+  std::vector<FPanel> panels;      // class-local indices until globalised
+  std::vector<int32_t> Rrows;
+  std::vector<FUpd> upd;
+  std::vector<FFrame> frames;
+  std::vector<FEnt> kent, lent;
+  int64_t nnzK = 0, w_doubles = 0;
+  int32_t max_level = 0;
+  double flops = 0;                // executed factorization flops per subdomain (updates + diag + TRSM)
+  double flops_useful = 0;         // sum_k cc_k^2 (column counts of L): the textbook Cholesky count
+};
+
+// Device view of the factorization plan.
+struct DevFactor {
+  const FPanel* panels;
+  const int32_t* Rrows;            // concatenated per class; FPanel::R_off globalised
+  const FUpd* upd;
+  const FFrame* frames;            // FFrame::k_* / l_* global indices into kent / lent
+  const FEnt* kent;
+  const FEnt* lent;
+  const FTask* tasks;
+  const int32_t* sub_cls;
+  const int64_t* sub_W_base;       // doubles
+  const int64_t* sub_flag_base;    // per subdomain: first flag (one per factor panel of its class)
+  const int32_t* cls_panel0;       // per class first global factor panel
+  const void* const* Kptr;         // per subdomain K values (device, double)
+  void* const* Lout;               // per subdomain L values out (device; double, or float when fp32)
+  double* W;
+  int32_t* flags;                  // per (sub, panel): completed frames + 0x10000 once the diagonal is done
+  int32_t* queue;                  // task counters (one per launch slot)
+  unsigned long long* err;
+  int32_t fp32, pad;
+};
+
+struct FactorPlan {
+  bool ready = false;
+  std::vector<FactorClass> classes;
+  std::vector<FPanel> panels;      // global
+  std::vector<int32_t> Rrows;
+  std::vector<FUpd> upd;
+  std::vector<FFrame> frames;
+  std::vector<FEnt> kent, lent;
+  std::vector<FTask> tasks;
+  std::vector<int64_t> task_chunk; // chunk c = tasks [task_chunk[c], task_chunk[c+1]) of subdomains
+  std::vector<int32_t> chunk_sub;  //   [chunk_sub[c], chunk_sub[c+1]) (host-fed pipeline granularity)
+  std::vector<int64_t> sub_W_base, sub_flag_base, sub_nnzK;
+  std::vector<int32_t> cls_panel0;
+  int64_t W_doubles = 0, nflags = 0;
+  double flops = 0, flops_useful = 0, bytes_K = 0;
+  DevFactor dev{};
+  std::vector<void*> allocations;
+  void** h_ptrs = nullptr;         // pinned: nsub K pointers then nsub L pointers
+  void** d_ptrs = nullptr;
+  void* ptr_event = nullptr;
+  void* d_Kstage = nullptr;        // host-fed path: K values staging
+  std::vector<int64_t> Kstage_off;
 };
 
 // Per-launch parameters of the TRSM kernel: first task, L-block ring bytes and shared strip capacity
@@ -301,9 +394,16 @@ struct Plan {
   void* copy_stream = nullptr;   // host-fed pipeline (sc_assemble_batch_host): H2D copies
   void* ev_start = nullptr;
   std::vector<void*> ev_chunk;
+  FactorPlan fac;                // device numeric factorization (sc_factor_attach)
 };
 
 // plan.cpp
+struct PanelPart {
+  int32_t a = -1, b = -1, merged = 0;  // columns [a, b); merged: relaxed (several supernodes)
+  std::vector<int32_t> R;              // rows below the panel, ascending
+};
+int32_t partition_panels(int32_t n, const int64_t* cp, const int32_t* ri, const std::vector<int32_t>& parent, int PW,
+                         std::vector<PanelPart>& out);
 sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options& opt, Plan& P, std::string& err);
 
 // kernels.cu
@@ -317,6 +417,15 @@ sc_status device_check(Plan& P, std::string& err);
 sc_status copy_F_lower(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
 sc_status copy_X_strips(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
 sc_status assemble_host_pipelined(Plan& P, const void* const* Lhost, void* stream, std::string& err);
+sc_status assemble_stage_begin(Plan& P, std::vector<void*>& dptrs, void* stream, std::string& err);
+sc_status assemble_range(Plan& P, int32_t s0, int32_t s1, void* stream, std::string& err);
+
+// factor_plan.cpp / factor.cu (device numeric factorization)
+sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::string& err);
+sc_status upload_factor_plan(Plan& P, std::string& err);
+void free_factor_device(Plan& P);
+sc_status launch_factorize(Plan& P, const void* const* Kptr, void* const* Lout, void* stream, std::string& err);
+sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* stream, std::string& err);
 
 // pcpg.cu
 sc_status pcpg_solve(Plan& P, const double* d, const double* e_host, double* lambda, const sc_coarse* cs,

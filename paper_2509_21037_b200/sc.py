@@ -54,10 +54,17 @@ class Stats(ctypes.Structure):
                                                "device_bytes", "bytes_apply", "bytes_panels")] + \
                [("panels", ctypes.c_int64), ("group_cols", ctypes.c_int32), ("x_strip", ctypes.c_int32),
                 ("trsm_tasks_2cta", ctypes.c_int64), ("trsm_kernel", ctypes.c_int32), ("pad0", ctypes.c_int32),
-                ("bytes_X_reach", ctypes.c_double)]
+                ("bytes_X_reach", ctypes.c_double), ("flops_factor_useful", ctypes.c_double),
+                ("flops_factor_executed", ctypes.c_double), ("bytes_K_values", ctypes.c_double),
+                ("factor_tasks", ctypes.c_int64), ("factor_panels", ctypes.c_int64),
+                ("factor_max_level", ctypes.c_int32), ("pad1", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class KPattern(ctypes.Structure):
+    _fields_ = [("K_colptr", _P), ("K_rowidx", _P)]
 
 
 class Coarse(ctypes.Structure):
@@ -89,7 +96,7 @@ EXPORTS = ["sc_pcpg", "sc_options_default", "sc_plan_create", "sc_assemble_batch
            "sc_check", "sc_get_F", "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_plan_subdomain_costs",
            "sc_set_timing_events", "sc_launches_per_assemble",
            "sc_launches_per_apply", "sc_plan_destroy", "sc_last_error", "sc_prepare_factor", "sc_apply_implicit",
-           "sc_launches_per_apply_implicit"]
+           "sc_launches_per_apply_implicit", "sc_factor_attach", "sc_factorize_batch", "sc_factorize_assemble_host"]
 
 
 def lib():
@@ -126,10 +133,14 @@ def lib():
     L.sc_pcpg.argtypes = [_P, _P, _P, _P, ctypes.POINTER(Coarse), ctypes.POINTER(PcpgOpts), ALLREDUCE_FN, _P,
                           ctypes.POINTER(PcpgResult), _P]
     L.sc_pcpg.restype = ctypes.c_int
+    L.sc_factor_attach.argtypes = [_P, ctypes.POINTER(KPattern), ctypes.c_int32]
+    L.sc_factorize_batch.argtypes = [_P, ctypes.POINTER(_P), ctypes.POINTER(_P), _P]
+    L.sc_factorize_assemble_host.argtypes = [_P, ctypes.POINTER(_P), _P]
     L.sc_last_error.argtypes = []
     L.sc_last_error.restype = ctypes.c_char_p
     for f in ("sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply", "sc_check", "sc_get_F",
-              "sc_prepare_factor", "sc_apply_implicit",
+              "sc_prepare_factor", "sc_apply_implicit", "sc_factor_attach", "sc_factorize_batch",
+              "sc_factorize_assemble_host",
               "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_set_timing_events", "sc_plan_subdomain_costs"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -226,6 +237,36 @@ class SCPlan:
     def assemble_host(self, L_values: Sequence[np.ndarray], stream=None):
         """L values in host memory (pinned torch tensors or numpy arrays); copied H2D inside the call."""
         _check(lib().sc_assemble_batch_host(self._h, self._value_ptrs(L_values), _stream_handle(stream)))
+
+    # -- device numeric factorization (SURVEY f4)
+    def factor_attach(self, K_patterns: Sequence):
+        """K_patterns: per subdomain (K_colptr, K_rowidx) of the LOWER triangle of K_reg in the original
+        DOF numbering (e.g. scipy tril(K).tocsc() indptr / indices)."""
+        keep = []
+        pats = (KPattern * max(self.nsub, 1))()
+        for i, (cp, ri) in enumerate(K_patterns):
+            a = np.ascontiguousarray(cp, dtype=np.int64)
+            b = np.ascontiguousarray(ri, dtype=np.int32)
+            keep += [a, b]
+            pats[i].K_colptr, pats[i].K_rowidx = a.ctypes.data, b.ctypes.data
+        _check(lib().sc_factor_attach(self._h, pats, self.nsub))
+        self.nnzK = [int(cp[-1]) for cp, _ in K_patterns]
+
+    def factorize(self, K_values: Sequence, L_out: Sequence, stream=None):
+        """K_values: per subdomain a CUDA float64 tensor (or device pointer) of nnz(K) values; L_out:
+        CUDA tensors (float64, or float32 for precision 32) of nnz(L) values, written."""
+        kp = (_P * max(self.nsub, 1))()
+        for i, t in enumerate(K_values):
+            kp[i] = t if isinstance(t, int) else t.data_ptr()
+        _check(lib().sc_factorize_batch(self._h, kp, self._value_ptrs(L_out), _stream_handle(stream)))
+
+    def factorize_assemble_host(self, K_values: Sequence, stream=None):
+        """K values in host memory (pinned float64 tensors or numpy arrays): H2D copy of K, device
+        factorization, assembly -- all inside the call."""
+        kp = (_P * max(self.nsub, 1))()
+        for i, t in enumerate(K_values):
+            kp[i] = t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+        _check(lib().sc_factorize_assemble_host(self._h, kp, _stream_handle(stream)))
 
     # -- solution
     def prepare_factor(self, L_values: Sequence, stream=None):

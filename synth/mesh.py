@@ -162,6 +162,10 @@ def assemble_subdomain(d: int, E: int, physics: str, elem_coef: Optional[np.ndar
     n = (E + 1) ** d * dpn
     K = sp.coo_matrix((vals, (rows, cols)), shape=(n, n)).tocsr()
     K.sum_duplicates()
+    # exactly symmetric with a symmetric stored pattern (the union of both triangles; sums that cancel
+    # to round-off stay stored, as in a connectivity-based FEM pattern), so every consumer (oracle,
+    # host factor, device factorization) sees the same matrix whichever triangle it reads
+    K = ((K + K.T) * 0.5).tocsr()
     K.sort_indices()
     return K
 
@@ -268,6 +272,14 @@ class Subdomain:
         if self._L_own is not None:
             return self._L_own
         return self._L_ref_values * np.sqrt(self.kappa)
+
+    def K_lower(self):
+        """(colptr int64, rowidx int32, values float64): CSC of the lower triangle of K_reg in the
+        natural DOF order -- the input of the device factorization (sc_factor_attach / factorize)."""
+        T = sp.tril(self.K_reg).tocsc()
+        T.sort_indices()
+        return (np.ascontiguousarray(T.indptr, dtype=np.int64), np.ascontiguousarray(T.indices, dtype=np.int32),
+                np.ascontiguousarray(T.data, dtype=np.float64))
 
     def Bt_dense(self) -> np.ndarray:
         Bt = np.zeros((self.n, self.m))

@@ -22,7 +22,8 @@ root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 dst = sys.argv[3] if len(sys.argv) > 3 else os.path.join(root, "profiles")
 os.makedirs(dst, exist_ok=True)
 
-PHASE = {"prep_panel_kernel": "prep", "prep_small_kernel": "prep", "trsm_smem_kernel": "trsm", "syrk_pair_kernel": "syrk"}
+PHASE = {"prep_panel_kernel": "prep", "prep_small_kernel": "prep", "trsm_smem_kernel": "trsm", "trsm_warp_kernel": "trsm",
+         "syrk_pair_kernel": "syrk"}
 
 
 def to_bytes(s):

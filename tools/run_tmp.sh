@@ -1,2 +1,6 @@
-cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_pcpg.py -q -x > gpurun_out/t_pcpg.log 2>&1
+#!/bin/bash
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_factor.py -q > gpurun_out/t_factor.log 2>&1; echo "rc=$?" >> gpurun_out/t_factor.log
+timeout 900 python bench.py --cpu-budget 5 > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err; echo "rc=$?" >> gpurun_out/bench_default.err
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
