@@ -170,18 +170,21 @@ sc_status sc_assemble_batch_host(sc_plan_t p, const void* const* L_values_host, 
    sum; multi-GPU callers all-reduce q over ranks (torch.distributed / NCCL).  Deterministic. */
 sc_status sc_apply(sc_plan_t p, const double* lambda, double* q, void* stream);
 
-/* Factor staging only (the prep phase of sc_assemble_batch): the plan's panel buffers receive the
-   supernodal factor panels of L (inverted diagonal blocks + pruned row chunks), which is what the
-   implicit apply needs; F is not assembled.  Same argument rules as sc_assemble_batch. */
+/* Factor staging for the implicit apply: copies the L values into the plan's supernodal factor
+   workspace (panels of <= 32 columns: the rows below each diagonal block, and the inverse of the
+   block), building the panel structure from the L pattern on first use; F is not assembled.  Same
+   argument rules as sc_assemble_batch.  A non-positive or non-finite diagonal raises the sticky
+   SC_ERR_ZERO_PIVOT.  (sc_factorize_batch / sc_factorize_assemble_host fill the same workspace.) */
 sc_status sc_prepare_factor(sc_plan_t p, const void* const* L_values, void* stream);
 
 /* Implicit dual-operator application (eq. dualop_apply_impl): q[g] = sum_i
    sum_{a: lambda_map_i(a) = g} (B~_i K_i^{-1} B~_i^T lambda_i)(a), computed WITHOUT F by one forward
-   and one backward substitution per subdomain with the factor staged by the last
-   sc_prepare_factor (or, for CTA-TRSM plans, sc_assemble_batch, which stages it too; the warp TRSM
-   reads L straight from the caller's CSC and stages nothing) -- SC_ERR_STATE if none.  One CTA per subdomain; its work
-   vector lives in shared memory when n_i <= 25,600, else in plan-owned global memory.  lambda, q:
-   DEVICE arrays of n_lambda_global doubles; q overwritten; deterministic. */
+   and one backward substitution per subdomain with the factor in the workspace (the last
+   sc_prepare_factor, sc_factorize_batch or sc_factorize_assemble_host; SC_ERR_STATE if none).  One
+   warp task per (subdomain, factor panel), scheduled by elimination-tree level with per-panel
+   completion flags, so independent panels of all subdomains run concurrently.  lambda, q: DEVICE
+   arrays of n_lambda_global doubles; q overwritten; deterministic (fixed summation orders, no
+   atomics on values). */
 sc_status sc_apply_implicit(sc_plan_t p, const double* lambda, double* q, void* stream);
 
 /* ---- Numeric factorization on the device ---------------------------------------

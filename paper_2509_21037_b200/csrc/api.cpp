@@ -108,14 +108,13 @@ sc_status sc_apply_implicit(sc_plan_t p, const double* lambda, double* q, void* 
 
 sc_status sc_factor_attach(sc_plan_t p, const sc_K_pattern* K, int32_t nsub) {
   if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  if (!K && nsub > 0) return fail(SC_ERR_INVALID_ARG, "NULL K");
   std::string err;
   sc_status st;
   try {
+    if (p->P.fac.ready) p->P.stats.device_bytes -= 8.0 * (double)(p->P.fac.W_doubles + p->P.fac.sub_x_base.back());
     sc::free_factor_device(p->P);
-    if (!p->P.fac.tasks.empty() || !p->P.fac.classes.empty()) {
-      if (p->P.fac.ready) p->P.stats.device_bytes -= 8.0 * (double)p->P.fac.W_doubles;
-      p->P.fac = sc::FactorPlan();
-    }
+    p->P.fac = sc::FactorPlan();
     st = sc::build_factor_plan(p->P, K, nsub, err);
     if (st == SC_OK && p->P.on_device) st = sc::upload_factor_plan(p->P, err);  // host-only: symbolic + stats
   } catch (const std::bad_alloc&) {
@@ -132,7 +131,7 @@ sc_status sc_factor_attach(sc_plan_t p, const sc_K_pattern* K, int32_t nsub) {
   S.flops_factor_useful = F.flops_useful;
   S.flops_factor_executed = F.flops;
   S.bytes_K_values = F.bytes_K;
-  S.factor_tasks = (int64_t)F.tasks.size();
+  S.factor_tasks = F.task_chunk.empty() ? 0 : F.task_chunk[0];
   S.factor_panels = 0;
   S.factor_max_level = 0;
   for (int32_t i = 0; i < p->P.nsub; i++) {
@@ -140,13 +139,13 @@ sc_status sc_factor_attach(sc_plan_t p, const sc_K_pattern* K, int32_t nsub) {
     S.factor_panels += (int64_t)fc.panels.size();
     S.factor_max_level = std::max(S.factor_max_level, fc.max_level);
   }
-  if (p->P.on_device) S.device_bytes += 8.0 * (double)F.W_doubles;
+  if (p->P.on_device) S.device_bytes += 8.0 * (double)(F.W_doubles + F.sub_x_base.back());
   return SC_OK;
 }
 
 sc_status sc_factorize_batch(sc_plan_t p, const void* const* K_values, void* const* L_values, void* stream) {
   if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
-  if (!p->P.fac.ready) return fail(SC_ERR_STATE, "no factorization plan (sc_factor_attach)");
+  if (!p->P.fac.ready || !p->P.fac.has_K) return fail(SC_ERR_STATE, "no factorization plan (sc_factor_attach)");
   if ((!K_values || !L_values) && p->P.nsub > 0) return fail(SC_ERR_INVALID_ARG, "NULL K_values or L_values");
   std::string err;
   sc_status st = sc::launch_factorize(p->P, K_values, L_values, stream, err);
@@ -155,7 +154,7 @@ sc_status sc_factorize_batch(sc_plan_t p, const void* const* K_values, void* con
 
 sc_status sc_factorize_assemble_host(sc_plan_t p, const void* const* K_values_host, void* stream) {
   if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
-  if (!p->P.fac.ready) return fail(SC_ERR_STATE, "no factorization plan (sc_factor_attach)");
+  if (!p->P.fac.ready || !p->P.fac.has_K) return fail(SC_ERR_STATE, "no factorization plan (sc_factor_attach)");
   if (!K_values_host && p->P.nsub > 0) return fail(SC_ERR_INVALID_ARG, "NULL K_values_host");
   std::string err;
   sc_status st = sc::factorize_assemble_host(p->P, K_values_host, stream, err);

@@ -45,6 +45,12 @@ namespace {
   } while (0)
 
 constexpr int kFWarps = 4;              // warps per CTA (independent workers)
+#ifndef SC_FPREFETCH
+#define SC_FPREFETCH 0                  // software-pipelined k loop of the updates (costs spills at 128 regs)
+#endif
+#ifndef SC_FMINB
+#define SC_FMINB 4                      // CTAs per SM the factor kernel's registers are sized for
+#endif
 constexpr int kSLd = kFW + 1;           // per-warp frame buffer: 32 x 33 doubles (column 32: 1 / l_jj)
 constexpr int kFSmem = kFWarps * kFW * kSLd * 8;
 
@@ -53,102 +59,170 @@ __device__ __forceinline__ void fdmma(double& c0, double& c1, double a, double b
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
-__device__ __forceinline__ int ld_acquire(const int* p) {
+// Completion flags: producers write their results, __threadfence(), then add to the flag (release
+// pattern).  Consumers spin with relaxed loads (no L1 invalidation per poll -- an ld.acquire costs a
+// CCTL.IVALL each time) and, once every flag a warp needs is set, one fence.acq_rel.gpu completes the
+// acquire pattern; the data itself is read with ld.global.cg (L2).
+__device__ __forceinline__ int ld_relaxed(const int* p) {
   int v;
-  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// index of v in the ascending R[lo, hi), or -1
-__device__ __forceinline__ int find_row(const int32_t* R, int lo, int hi, int v) {
-  int h = hi;
-  while (lo < h) {
-    const int mid = (lo + h) >> 1;
-    if (__ldg(R + mid) < v) lo = mid + 1;
-    else h = mid;
-  }
-  return (lo < hi && __ldg(R + lo) == v) ? lo : -1;
-}
-
-__global__ void __launch_bounds__(32 * kFWarps, 4) factor_kernel(DevFactor F, int64_t t0, int64_t t1, int slot) {
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFactor F, int64_t t0, int64_t t1, int slot,
+                                                                 int stage) {
   extern __shared__ double fsm[];
+  __shared__ int frow_s[kFWarps][kFW], rmap_s[kFWarps][kFW], cmap_s[kFWarps][kFW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
   double* S = fsm + warp * kFW * kSLd;
+  int* frow = frow_s[warp];
+  int* rmap = rmap_s[warp];
+  int* cmap = cmap_s[warp];
   for (;;) {
     int64_t task = 0;
     if (lane == 0) task = t0 + atomicAdd(F.queue + slot, 1);
     task = __shfl_sync(~0u, task, 0);
     if (task >= t1) break;
     const FTask tk = F.tasks[task];
-    const FFrame fr = F.frames[tk.frame];
+    for (int fi = 0; fi < tk.nf; fi++) {
+    const FFrame fr = F.frames[tk.frame + fi];
     const FPanel pn = F.panels[fr.panel];
     const int sub = tk.sub;
     int* flags = F.flags + (F.sub_flag_base[sub] - F.cls_panel0[F.sub_cls[sub]]);  // indexed by global panel
     double* W = F.W + F.sub_W_base[sub];
     const bool diag = fr.r0 < 0;
     const int kw = pn.kw, nI = (fr.nrow + 7) >> 3, nJ = pn.kw8 >> 3;
-    const int rv = lane < fr.nrow ? (diag ? pn.a + lane : __ldg(F.Rrows + pn.R_off + fr.r0 + lane)) : -1;
+    // the frame's row values (ascending), for the row lookups of the descendants' rows
+    frow[lane] = lane < fr.nrow ? (diag ? pn.a + lane : __ldg(F.Rrows + pn.R_off + fr.r0 + lane)) : INT32_MAX;
     double acc[4][4][2];
 #pragma unroll
     for (int I = 0; I < 4; I++)
 #pragma unroll
       for (int J = 0; J < 4; J++) acc[I][J][0] = acc[I][J][1] = 0.0;
 
-    // ---- updates from the finished descendant panels (left-looking)
-    for (int u = pn.upd_begin; u < pn.upd_end; u++) {
-      const FUpd U = F.upd[u];
-      const FPanel dn = F.panels[U.d];
-      if (lane == 0) {
+    // ---- updates from the finished descendant panels (left-looking), 32 list entries at a time:
+    // lane l loads entry l's descriptor and its panel, waits (acquire) for that panel; then the
+    // entries are processed in list order (deterministic)
+    for (int u0 = fr.u_begin; u0 < (stage ? fr.u_begin : fr.u_end); u0 += 32) {
+      const int nu = min(32, fr.u_end - u0);
+      FFUpd U{};
+      int dkw = 0, dnR = 0, dR = 0;
+      int64_t dw = 0;
+      if (lane < nu) {
+        U = F.fupd[u0 + lane];
+        const FPanel dn = F.panels[U.d];
+        dkw = dn.kw;
+        dnR = dn.nR;
+        dR = dn.R_off;
+        dw = dn.w_off;
         const int* fl = flags + U.d;
-        while ((ld_acquire(fl) & 0xFFFF) < dn.nframe) __nanosleep(100);
+        while ((ld_relaxed(fl) & 0xFFFF) < dn.nframe) __nanosleep(32);
       }
       __syncwarp();
-      const int32_t* Rd = F.Rrows + dn.R_off;
-      const int lo = diag ? U.s0 : U.s1, hi = diag ? U.s1 : dn.nR;
-      const int ridx = (rv >= 0 && lo < hi) ? find_row(Rd, lo, hi, rv) : -1;
-      const int cidx = lane < kw ? find_row(Rd, U.s0, U.s1, pn.a + lane) : -1;
-      const unsigned rm = __ballot_sync(~0u, ridx >= 0), cm = __ballot_sync(~0u, cidx >= 0);
-      if (!rm || !cm) continue;
-      const double* Wd = W + dn.w_off;
-      const int ldd = dn.nR;
-      int ri[4], ci[4];
+      if (lane == 0) fence_acq_rel();
+      __syncwarp();
+      for (int j = 0; j < nu; j++) {
+        const int s0 = __shfl_sync(~0u, U.s0, j), s1 = __shfl_sync(~0u, U.s1, j);
+        const int k0 = __shfl_sync(~0u, U.k0, j), k1 = __shfl_sync(~0u, U.k1, j);
+        const int ukw = __shfl_sync(~0u, dkw, j), ldd = __shfl_sync(~0u, dnR, j), uR = __shfl_sync(~0u, dR, j);
+        const int64_t uw = __shfl_sync(~0u, dw, j);
+        const int32_t* Rd = F.Rrows + uR;
+        // columns: R_d[s0, s1) are columns of this panel (value - a); rows: R_d[k0, k1) -> frame rows
+        cmap[lane] = -1;
+        rmap[lane] = -1;
+        __syncwarp();
+        if (lane < s1 - s0) cmap[__ldg(Rd + s0 + lane) - pn.a] = s0 + lane;
+        if (diag) {
+          if (lane < s1 - s0) rmap[__ldg(Rd + s0 + lane) - pn.a] = s0 + lane;
+        } else {
+          for (int w0 = k0; w0 < k1; w0 += 32) {
+            if (w0 + lane < k1) {
+              const int v = __ldg(Rd + w0 + lane);
+              int lo = 0;  // first frame row >= v (frame rows ascending, padded with INT32_MAX)
 #pragma unroll
-      for (int I = 0; I < 4; I++) ri[I] = __shfl_sync(~0u, ridx, 8 * I + g);
+              for (int step = 16; step > 0; step >>= 1)
+                if (frow[lo + step - 1] < v) lo += step;
+              if (frow[lo] == v) rmap[lo] = w0 + lane;
+            }
+          }
+        }
+        __syncwarp();
+        const int ridx = rmap[lane], cidx = cmap[lane];
+        const unsigned rm = __ballot_sync(~0u, ridx >= 0), cm = __ballot_sync(~0u, cidx >= 0);
+        if (!rm || !cm) continue;
+        const double* Wd = W + uw;
+        int ri[4], ci[4];
 #pragma unroll
-      for (int J = 0; J < 4; J++) ci[J] = __shfl_sync(~0u, cidx, 8 * J + g);
-      bool ra[4], ca[4];
+        for (int I = 0; I < 4; I++) ri[I] = __shfl_sync(~0u, ridx, 8 * I + g);
 #pragma unroll
-      for (int I = 0; I < 4; I++) ra[I] = I < nI && ((rm >> (8 * I)) & 0xFFu);
+        for (int J = 0; J < 4; J++) ci[J] = __shfl_sync(~0u, cidx, 8 * J + g);
+        bool ra[4], ca[4];
 #pragma unroll
-      for (int J = 0; J < 4; J++) ca[J] = J < nJ && ((cm >> (8 * J)) & 0xFFu);
-      for (int k0 = 0; k0 < dn.kw; k0 += 4) {
-        const int kk = k0 + t;
-        const bool kv = kk < dn.kw;
-        const double* col = Wd + (int64_t)kk * ldd;
-        double a[4], b[4];
+        for (int I = 0; I < 4; I++) ra[I] = I < nI && ((rm >> (8 * I)) & 0xFFu);
 #pragma unroll
-        for (int I = 0; I < 4; I++) a[I] = (ra[I] && kv && ri[I] >= 0) ? __ldcg(col + ri[I]) : 0.0;
+        for (int J = 0; J < 4; J++) ca[J] = J < nJ && ((cm >> (8 * J)) & 0xFFu);
+        // k loop software-pipelined: the fragments of step kb + 4 are in flight during the DMMAs of kb
+        auto load = [&](int kb, double (&a)[4], double (&b)[4]) {
+          const int kk = kb + t;
+          const bool kv = kk < ukw;
+          const double* col = Wd + (int64_t)kk * ldd;
 #pragma unroll
-        for (int J = 0; J < 4; J++) b[J] = (ca[J] && kv && ci[J] >= 0) ? __ldcg(col + ci[J]) : 0.0;
+          for (int I = 0; I < 4; I++) a[I] = (ra[I] && kv && ri[I] >= 0) ? __ldcg(col + ri[I]) : 0.0;
 #pragma unroll
-        for (int I = 0; I < 4; I++)
+          for (int J = 0; J < 4; J++) b[J] = (ca[J] && kv && ci[J] >= 0) ? __ldcg(col + ci[J]) : 0.0;
+        };
+#if SC_FPREFETCH
+        double a[4], b[4], an[4], bn[4];
+        load(0, a, b);
+        for (int kb = 0; kb < ukw; kb += 4) {
+          if (kb + 4 < ukw) load(kb + 4, an, bn);
 #pragma unroll
-          for (int J = 0; J < 4; J++)
-            if (ra[I] && ca[J] && (!diag || J <= I)) fdmma(acc[I][J][0], acc[I][J][1], a[I], b[J]);
+          for (int I = 0; I < 4; I++)
+#pragma unroll
+            for (int J = 0; J < 4; J++)
+              if (ra[I] && ca[J] && (!diag || J <= I)) fdmma(acc[I][J][0], acc[I][J][1], a[I], b[J]);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            a[q] = an[q];
+            b[q] = bn[q];
+          }
+        }
+#else
+        for (int kb = 0; kb < ukw; kb += 4) {
+          double a[4], b[4];
+          load(kb, a, b);
+#pragma unroll
+          for (int I = 0; I < 4; I++)
+#pragma unroll
+            for (int J = 0; J < 4; J++)
+              if (ra[I] && ca[J] && (!diag || J <= I)) fdmma(acc[I][J][0], acc[I][J][1], a[I], b[J]);
+        }
+#endif
       }
     }
 
-    // ---- S = K entries - updates (frame layout, row-major in the warp's shared buffer)
+    // ---- S = K entries - updates (frame layout, row-major in the warp's shared buffer); stage mode:
+    // S = the frame's entries of the given L (zeros elsewhere)
     __syncwarp();
+    if (stage) {
+      for (int e = lane; e < kFW * kSLd; e += 32) S[e] = 0.0;
+      __syncwarp();
+      for (int e = fr.l_begin + lane; e < fr.l_end; e += 32) {
+        const FEnt en = F.lent[e];
+        S[(en.pos >> 5) * kSLd + (en.pos & 31)] =
+            F.fp32 ? (double)__ldg(static_cast<const float*>(F.Lin[sub]) + en.q)
+                   : __ldg(static_cast<const double*>(F.Lin[sub]) + en.q);
+      }
+    } else {
 #pragma unroll
-    for (int I = 0; I < 4; I++)
+      for (int I = 0; I < 4; I++)
 #pragma unroll
-      for (int J = 0; J < 4; J++)
-        if (I < nI && J < nJ) {
-          S[(8 * I + g) * kSLd + 8 * J + 2 * t] = -acc[I][J][0];
-          S[(8 * I + g) * kSLd + 8 * J + 2 * t + 1] = -acc[I][J][1];
-        }
-    __syncwarp();
-    {
+        for (int J = 0; J < 4; J++)
+          if (I < nI && J < nJ) {
+            S[(8 * I + g) * kSLd + 8 * J + 2 * t] = -acc[I][J][0];
+            S[(8 * I + g) * kSLd + 8 * J + 2 * t + 1] = -acc[I][J][1];
+          }
+      __syncwarp();
       const double* Kv = static_cast<const double*>(F.Kptr[sub]);
       for (int e = fr.k_begin + lane; e < fr.k_end; e += 32) {
         const FEnt en = F.kent[e];
@@ -157,9 +231,20 @@ __global__ void __launch_bounds__(32 * kFWarps, 4) factor_kernel(DevFactor F, in
     }
     __syncwarp();
 
+    if (diag && stage) {  // the triangle is given: pivots checked, reciprocals for the inverse
+      if (lane < kw) {
+        const double d = S[lane * kSLd + lane];
+        if (!(d > 0.0) || !isfinite(d)) {
+          atomicCAS(F.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + lane));
+          atomicCAS(F.err + 1 + sub, 0ull, (unsigned long long)(pn.a + lane) + 1ull);
+        }
+        S[lane * kSLd + kFW] = 1.0 / d;
+      }
+      __syncwarp();
+    }
     if (diag) {
       // ---- Cholesky of the diagonal block (right-looking, lane = row)
-      for (int j = 0; j < kw; j++) {
+      for (int j = 0; j < (stage ? 0 : kw); j++) {
         double djj = S[j * kSLd + j];
         if (!(djj > 0.0) || !isfinite(djj)) {
           if (lane == 0) {
@@ -200,11 +285,16 @@ __global__ void __launch_bounds__(32 * kFWarps, 4) factor_kernel(DevFactor F, in
         for (int i = 0; i < kFW; i++)
           if (i < pn.kw8) Winv[lane * pn.kw8 + i] = x[i];
       }
+    } else if (stage) {  // the rows of the given L go to the workspace as they are
+      double* Wp = W + pn.w_off;
+      for (int c = 0; c < kw; c++)
+        if (lane < fr.nrow) Wp[(int64_t)c * pn.nR + fr.r0 + lane] = S[lane * kSLd + c];
     } else {
       // ---- wait for the panel's own diagonal frame, then X = S inv(L_pp)^T
       if (lane == 0) {
         const int* fl = flags + fr.panel;
-        while (!(ld_acquire(fl) & 0x10000)) __nanosleep(100);
+        while (!(ld_relaxed(fl) & 0x10000)) __nanosleep(32);
+        fence_acq_rel();
       }
       __syncwarp();
       const double* Winv = W + pn.inv_off;
@@ -243,7 +333,8 @@ __global__ void __launch_bounds__(32 * kFWarps, 4) factor_kernel(DevFactor F, in
     }
     __syncwarp();
     // ---- L values of this frame into the caller's CSC array
-    if (F.fp32) {
+    if (stage) {
+    } else if (F.fp32) {
       float* Lo = static_cast<float*>(F.Lout[sub]);
       for (int e = fr.l_begin + lane; e < fr.l_end; e += 32) {
         const FEnt en = F.lent[e];
@@ -261,6 +352,184 @@ __global__ void __launch_bounds__(32 * kFWarps, 4) factor_kernel(DevFactor F, in
       __threadfence();
       atomicAdd(flags + fr.panel, diag ? 0x10001 : 1);
     }
+    }  // frames of the task
+  }
+}
+
+// ------------------------------------------------------------------------------------------------
+// Implicit apply on the factor workspace (eq. dualop_apply_impl):
+// x = P B~^T lambda_i, y = L^{-1} x (forward), z = L^{-T} y (backward), u = B~ P^T z; no F.  One warp
+// task per (subdomain, factor panel), pulled from a queue in level order (forward) or its reverse
+// (backward), with per-panel completion flags (acquire/release) like the factorization: all panels
+// of all subdomains whose dependencies are done run concurrently.  Each entry of the factor is read
+// once per direction; every sum has a fixed order (deterministic).
+//   forward  (panel p): b_c = sum over the permuted row a_p + c of B~^T lambda (CSR by row);
+//                       b -= L[cols of p, d] y_d for the descendants d (their rows R_d[s0, s1));
+//                       y_p = inv(L_pp) b.
+//   backward (panel p): v = y_p - L[R_p, p]^T z[R_p] (after the ancestors owning R_p);
+//                       z_p = inv(L_pp)^T v.
+// ------------------------------------------------------------------------------------------------
+__device__ __forceinline__ void wait_flag(const int* f, int target) {
+  while (ld_relaxed(f) < target) __nanosleep(32);
+}
+
+__global__ void __launch_bounds__(32 * kFWarps) implicit_fwd_kernel(DevFactor F, const double* __restrict__ lambda,
+                                                                    int64_t ntask) {
+  __shared__ double acc_s[kFWarps][kFW];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* acc = acc_s[warp];
+  for (;;) {
+    int64_t task = 0;
+    if (lane == 0) task = atomicAdd(F.queue + 2, 1);
+    task = __shfl_sync(~0u, task, 0);
+    if (task >= ntask) break;
+    const I2 pt = F.ptasks[task];
+    const int sub = pt.x, cls = F.sub_cls[sub];
+    const FPanel pn = F.panels[pt.y];
+    int* flags = F.flags + (F.sub_flag_base[sub] - F.cls_panel0[cls]);
+    const double* W = F.W + F.sub_W_base[sub];
+    double* x = F.xv + F.sub_x_base[sub];
+    const int kw = pn.kw;
+    double b = 0.0;
+    if (lane < kw) {
+      const int32_t* rp = F.bt_rp + F.cls_bt0[cls];
+      const int64_t* slm = F.slm + F.sub_slm_off[sub];
+      for (int e = rp[pn.a + lane]; e < rp[pn.a + lane + 1]; e++) b = fma(F.bt_v[e], __ldg(lambda + slm[F.bt_a[e]]), b);
+    }
+    acc[lane] = 0.0;
+    const FFrame fr = F.frames[pn.frame_begin];
+    for (int u0 = fr.u_begin; u0 < fr.u_end; u0 += 32) {
+      const int nu = min(32, fr.u_end - u0);
+      FFUpd U{};
+      int dkw = 0, dnR = 0, dR = 0, da = 0;
+      int64_t dw = 0;
+      if (lane < nu) {
+        U = F.fupd[u0 + lane];
+        const FPanel dn = F.panels[U.d];
+        dkw = dn.kw;
+        dnR = dn.nR;
+        dR = dn.R_off;
+        da = dn.a;
+        dw = dn.w_off;
+        wait_flag(flags + U.d, 1);
+      }
+      __syncwarp();
+      if (lane == 0) fence_acq_rel();
+      __syncwarp();
+      for (int j = 0; j < nu; j++) {
+        const int s0 = __shfl_sync(~0u, U.s0, j), s1 = __shfl_sync(~0u, U.s1, j);
+        const int ukw = __shfl_sync(~0u, dkw, j), ldd = __shfl_sync(~0u, dnR, j), uR = __shfl_sync(~0u, dR, j);
+        const int ua = __shfl_sync(~0u, da, j);
+        const int64_t uw = __shfl_sync(~0u, dw, j);
+        if (lane < s1 - s0) {
+          const double* col = W + uw + s0 + lane;
+          double v = 0.0;
+#pragma unroll
+          for (int h = 0; h < kFW; h += 16) {  // 16 loads in flight, then the fixed-order sum
+            double w[16], xk[16];
+#pragma unroll
+            for (int k = 0; k < 16; k++) {
+              w[k] = h + k < ukw ? __ldcg(col + (int64_t)(h + k) * ldd) : 0.0;
+              xk[k] = h + k < ukw ? __ldcg(x + ua + h + k) : 0.0;
+            }
+#pragma unroll
+            for (int k = 0; k < 16; k++) v = fma(w[k], xk[k], v);
+          }
+          acc[__ldg(F.Rrows + uR + s0 + lane) - pn.a] += v;
+        }
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+    const double v = lane < kw ? b - acc[lane] : 0.0;
+    const double* inv = W + pn.inv_off;  // column-major kw8 x kw8: inv[i][k] at k kw8 + i
+    double y = 0.0;
+#pragma unroll
+    for (int k = 0; k < kFW; k++) {
+      const double vk = __shfl_sync(~0u, v, k);
+      const double iv = (k < kw && lane >= k && lane < kw) ? __ldcg(inv + (int64_t)k * pn.kw8 + lane) : 0.0;
+      y = fma(iv, vk, y);
+    }
+    if (lane < kw) x[pn.a + lane] = y;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(flags + pt.y, 1);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32 * kFWarps) implicit_bwd_kernel(DevFactor F, int64_t ntask) {
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    int64_t task = 0;
+    if (lane == 0) task = atomicAdd(F.queue + 3, 1);
+    task = __shfl_sync(~0u, task, 0);
+    if (task >= ntask) break;
+    const I2 pt = F.ptasks[ntask - 1 - task];
+    const int sub = pt.x, cls = F.sub_cls[sub];
+    const FPanel pn = F.panels[pt.y];
+    int* flags = F.flags + (F.sub_flag_base[sub] - F.cls_panel0[cls]);
+    const double* W = F.W + F.sub_W_base[sub];
+    double* x = F.xv + F.sub_x_base[sub];
+    const int kw = pn.kw;
+    for (int a0 = pn.anc_begin + lane; a0 < pn.anc_end; a0 += 32) wait_flag(flags + F.anc[a0].d, 2);
+    __syncwarp();
+    if (lane == 0) fence_acq_rel();
+    __syncwarp();
+    // s_k = sum_r L[R_p[r], a + k] z[R_p[r]]: lanes over rows, 32 partial sums per lane
+    double part[kFW];
+#pragma unroll
+    for (int k = 0; k < kFW; k++) part[k] = 0.0;
+    const double* Wp = W + pn.w_off;
+    for (int r0 = 0; r0 < pn.nR; r0 += 32) {
+      const int r = r0 + lane;
+      const double z = r < pn.nR ? __ldcg(x + __ldg(F.Rrows + pn.R_off + r)) : 0.0;
+#pragma unroll
+      for (int k = 0; k < kFW; k++)
+        if (k < kw && r < pn.nR) part[k] = fma(__ldcg(Wp + (int64_t)k * pn.nR + r), z, part[k]);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kFW; k++) {
+      if (k < kw) {
+        double v = part[k];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(~0u, v, o);
+        if (lane == k) s = v;
+      }
+    }
+    const double v = lane < kw ? __ldcg(x + pn.a + lane) - s : 0.0;
+    const double* inv = W + pn.inv_off;  // z_j = sum_{i >= j} inv[i][j] v_i
+    double z = 0.0;
+#pragma unroll
+    for (int i = 0; i < kFW; i++) {
+      const double vi = __shfl_sync(~0u, v, i);
+      const double iv = (i < kw && lane <= i && lane < kw) ? __ldcg(inv + (int64_t)lane * pn.kw8 + i) : 0.0;
+      z = fma(iv, vi, z);
+    }
+    __syncwarp();
+    if (lane < kw) x[pn.a + lane] = z;
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence();
+      atomicAdd(flags + pt.y, 1);
+    }
+  }
+}
+
+// u[a] = (B~ P^T z)_a per subdomain and stepped column, into DevPlan::upart (then the plan's
+// deterministic scatter-sum over subdomains)
+__global__ void __launch_bounds__(256) implicit_gather_kernel(DevPlan P, const double* __restrict__ xv,
+                                                              const int64_t* __restrict__ sub_x_base) {
+  const int sub = blockIdx.x, cls = P.sub_cls[sub], m = P.sub_m[sub];
+  const int32_t* ibp = P.ib_ptr + P.cls_ib0[cls];
+  const double* x = xv + sub_x_base[sub];
+  double* u = P.upart + P.sub_slm_off[sub];
+  for (int a = threadIdx.x; a < m; a += blockDim.x) {
+    double s = 0.0;
+    for (int e = ibp[a]; e < ibp[a + 1]; e++) s = fma(P.ib_val[e], x[P.ib_row[e]], s);
+    u[a] = s;
   }
 }
 
@@ -310,9 +579,10 @@ int factor_grid(int64_t ntask) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(want, (int64_t)nsm * per_sm));
 }
 
-sc_status factor_range(Plan& P, int64_t t0, int64_t t1, int slot, cudaStream_t stream, std::string& err) {
+sc_status factor_range(Plan& P, int64_t t0, int64_t t1, int slot, cudaStream_t stream, std::string& err,
+                       int stage = 0) {
   if (t1 <= t0) return SC_OK;
-  factor_kernel<<<factor_grid(t1 - t0), 32 * kFWarps, kFSmem, stream>>>(P.fac.dev, t0, t1, slot);
+  factor_kernel<<<factor_grid(t1 - t0), 32 * kFWarps, kFSmem, stream>>>(P.fac.dev, t0, t1, slot, stage);
   FCUDA(cudaGetLastError());
   return SC_OK;
 }
@@ -332,6 +602,10 @@ void free_factor_device(Plan& P) {
   F.ptr_event = nullptr;
   if (F.d_Kstage) cudaFree(F.d_Kstage);
   F.d_Kstage = nullptr;
+  if (F.fstream) cudaStreamDestroy(static_cast<cudaStream_t>(F.fstream));
+  F.fstream = nullptr;
+  for (void* e : F.fev) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  F.fev.clear();
   F.d_ptrs = nullptr;
   F.ready = false;
 }
@@ -342,7 +616,7 @@ sc_status upload_factor_plan(Plan& P, std::string& err) {
   DevFactor D{};
   FTRY(fupload(F, F.panels, &D.panels, err));
   FTRY(fupload(F, F.Rrows, &D.Rrows, err));
-  FTRY(fupload(F, F.upd, &D.upd, err));
+  FTRY(fupload(F, F.fupd, &D.fupd, err));
   FTRY(fupload(F, F.frames, &D.frames, err));
   FTRY(fupload(F, F.kent, &D.kent, err));
   FTRY(fupload(F, F.lent, &D.lent, err));
@@ -351,6 +625,17 @@ sc_status upload_factor_plan(Plan& P, std::string& err) {
   FTRY(fupload(F, F.sub_W_base, &D.sub_W_base, err));
   FTRY(fupload(F, F.sub_flag_base, &D.sub_flag_base, err));
   FTRY(fupload(F, F.cls_panel0, &D.cls_panel0, err));
+  FTRY(fupload(F, F.anc, &D.anc, err));
+  FTRY(fupload(F, F.ptasks, &D.ptasks, err));
+  FTRY(fupload(F, F.bt_rp, &D.bt_rp, err));
+  FTRY(fupload(F, F.bt_a, &D.bt_a, err));
+  FTRY(fupload(F, F.bt_v, &D.bt_v, err));
+  FTRY(fupload(F, F.cls_bt0, &D.cls_bt0, err));
+  FTRY(fupload(F, F.sub_x_base, &D.sub_x_base, err));
+  FTRY(falloc(F, F.sub_x_base.back(), &D.xv, err));
+  D.Lin = P.dev.Lptr;
+  D.slm = P.dev.slm;
+  D.sub_slm_off = P.dev.sub_slm_off;
   FTRY(falloc(F, F.W_doubles, &D.W, err));
   FTRY(falloc(F, F.nflags, &D.flags, err));
   FTRY(falloc(F, kQueueSlots, &D.queue, err));
@@ -374,6 +659,19 @@ sc_status upload_factor_plan(Plan& P, std::string& err) {
   return SC_OK;
 }
 
+sc_status ensure_factor_plan(Plan& P, std::string& err) {
+  if (P.fac.ready) return SC_OK;
+  sc_status st = build_factor_plan(P, nullptr, P.nsub, err);
+  if (st == SC_OK) st = upload_factor_plan(P, err);
+  if (st != SC_OK) {
+    free_factor_device(P);
+    P.fac = FactorPlan();
+    return st;
+  }
+  P.stats.device_bytes += 8.0 * (double)(P.fac.W_doubles + P.fac.sub_x_base.back());
+  return SC_OK;
+}
+
 sc_status launch_factorize(Plan& P, const void* const* Kptr, void* const* Lout, void* stream_v, std::string& err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   FactorPlan& F = P.fac;
@@ -390,14 +688,55 @@ sc_status launch_factorize(Plan& P, const void* const* Kptr, void* const* Lout, 
   }
   FTRY(set_ptrs(P, Kptr, Lout, stream, err));
   P.last_stream = stream_v;
+  F.w_ready = true;  // the workspace holds this factorization (implicit apply)
   FCUDA(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   FCUDA(cudaMemsetAsync(F.dev.flags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nflags, 1), stream));
   FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
-  return factor_range(P, 0, (int64_t)F.tasks.size(), 0, stream, err);
+  return factor_range(P, 0, F.task_chunk[0], 0, stream, err);
 }
 
-// Host-fed pipeline: per chunk of subdomains, H2D of its K values on the copy stream, then on `stream`
-// the factorization of the chunk into the plan's L staging buffer and the chunk's assembly.
+// Stage the workspace from the plan's current L table (sc_prepare_factor): W <- L[R_p, p] and
+// inv(L_pp) for every panel, no factorization.
+sc_status launch_stage(Plan& P, void* stream_v, std::string& err) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  FactorPlan& F = P.fac;
+  FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
+  FTRY(factor_range(P, 0, F.task_chunk[0], 0, stream, err, 1));
+  F.w_ready = true;
+  return SC_OK;
+}
+
+// Implicit apply: forward and backward substitution over the workspace, then u = B~ P^T z into the
+// plan's per-(subdomain, multiplier) buffer (the caller's scatter-sum follows).
+sc_status launch_implicit_solve(Plan& P, const double* lambda, void* stream_v, std::string& err) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  FactorPlan& F = P.fac;
+  const int64_t nt = (int64_t)F.ptasks.size();
+  FCUDA(cudaMemsetAsync(F.dev.flags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nflags, 1), stream));
+  FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
+  if (nt > 0) {
+    static int nsm = 0;
+    if (!nsm) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nt + kFWarps - 1) / kFWarps, (int64_t)nsm * 8));
+    implicit_fwd_kernel<<<grid, 32 * kFWarps, 0, stream>>>(F.dev, lambda, nt);
+    FCUDA(cudaGetLastError());
+    implicit_bwd_kernel<<<grid, 32 * kFWarps, 0, stream>>>(F.dev, nt);
+    FCUDA(cudaGetLastError());
+  }
+  if (P.nsub > 0) {
+    implicit_gather_kernel<<<P.nsub, 256, 0, stream>>>(P.dev, F.dev.xv, F.dev.sub_x_base);
+    FCUDA(cudaGetLastError());
+  }
+  return SC_OK;
+}
+
+// Host-fed pipeline: per chunk of subdomains, H2D of its K values on the copy stream, its
+// factorization (into the plan's L staging buffer) on the factorization stream, its assembly on
+// `stream`; chunk k's factorization overlaps chunk k-1's assembly and chunk k+1's copies.
 sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* stream_v, std::string& err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   FactorPlan& F = P.fac;
@@ -414,17 +753,26 @@ sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* strea
     FCUDA(cudaMalloc(&d, std::max<size_t>(8 * (size_t)F.Kstage_off.back(), 16)));
     F.d_Kstage = d;
   }
+  const int32_t nchunk = (int32_t)F.chunk_sub.size() - 1;
+  if (!F.fstream) FCUDA(cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&F.fstream), cudaStreamNonBlocking));
+  while ((int32_t)F.fev.size() < nchunk) {
+    cudaEvent_t e;
+    FCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    F.fev.push_back(e);
+  }
   std::vector<void*> Lst;
   FTRY(assemble_stage_begin(P, Lst, stream_v, err));  // L staging + pointer table + error reset
   std::vector<const void*> Kd((size_t)P.nsub);
   for (int32_t i = 0; i < P.nsub; i++) Kd[(size_t)i] = static_cast<char*>(F.d_Kstage) + 8 * F.Kstage_off[(size_t)i];
   FTRY(set_ptrs(P, Kd.data(), Lst.data(), stream, err));
+  F.w_ready = true;
   FCUDA(cudaMemsetAsync(F.dev.flags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nflags, 1), stream));
   FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
-  cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream);
+  cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream), fs = static_cast<cudaStream_t>(F.fstream);
+  // everything before this call on `stream` (previous users of the staging buffers, the resets above)
   FCUDA(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_start), stream));
   FCUDA(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(P.ev_start), 0));
-  const int32_t nchunk = (int32_t)F.chunk_sub.size() - 1;
+  FCUDA(cudaStreamWaitEvent(fs, static_cast<cudaEvent_t>(P.ev_start), 0));
   while ((int32_t)P.ev_chunk.size() < nchunk) {
     cudaEvent_t e;
     FCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -449,10 +797,12 @@ sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* strea
                             cudaMemcpyHostToDevice, cs));
       i = j;
     }
-    cudaEvent_t e = static_cast<cudaEvent_t>(P.ev_chunk[(size_t)k]);
-    FCUDA(cudaEventRecord(e, cs));
-    FCUDA(cudaStreamWaitEvent(stream, e, 0));
-    FTRY(factor_range(P, F.task_chunk[(size_t)k], F.task_chunk[(size_t)k + 1], k % kQueueSlots, stream, err));
+    cudaEvent_t ec = static_cast<cudaEvent_t>(P.ev_chunk[(size_t)k]), ef = static_cast<cudaEvent_t>(F.fev[(size_t)k]);
+    FCUDA(cudaEventRecord(ec, cs));
+    FCUDA(cudaStreamWaitEvent(fs, ec, 0));
+    FTRY(factor_range(P, F.task_chunk[(size_t)k], F.task_chunk[(size_t)k + 1], 1 + k % (kQueueSlots - 1), fs, err));
+    FCUDA(cudaEventRecord(ef, fs));
+    FCUDA(cudaStreamWaitEvent(stream, ef, 0));
     FTRY(assemble_range(P, s0, s1, stream_v, err));
   }
   return SC_OK;

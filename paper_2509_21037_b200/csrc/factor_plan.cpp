@@ -17,6 +17,7 @@
 //   5. the task order: chunks of subdomains, inside a chunk by (level, subdomain, panel, frame), so
 //      every dependency precedes its dependants in the queue (the kernel's deadlock-freedom argument).
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -33,7 +34,7 @@ namespace {
     return (code);       \
   } while (0)
 
-sc_status analyse_factor_class(const ClassPlan& C, const sc_K_pattern& K, FactorClass& F, std::string& err) {
+sc_status analyse_factor_class(const ClassPlan& C, const sc_K_pattern* Kp, FactorClass& F, std::string& err) {
   const int32_t n = C.n;
   const int64_t* cp = C.colptr.data();
   const int32_t* ri = C.rowidx.data();
@@ -105,6 +106,63 @@ sc_status analyse_factor_class(const ClassPlan& C, const sc_K_pattern& K, Factor
     const double cc = (double)(cp[c + 1] - cp[c]);
     F.flops_useful += cc * cc;
   }
+  // ancestors (implicit apply, backward): the reverse of the update lists
+  {
+    std::vector<std::vector<FUpd>> al((size_t)np);
+    for (int32_t p = 0; p < np; p++)
+      for (int32_t u = F.panels[(size_t)p].upd_begin; u < F.panels[(size_t)p].upd_end; u++) {
+        const FUpd U = F.upd[(size_t)u];
+        al[(size_t)U.d].push_back(FUpd{p, U.s0, U.s1, 0});
+      }
+    for (int32_t p = 0; p < np; p++) {
+      F.panels[(size_t)p].anc_begin = (int32_t)F.anc.size();
+      F.anc.insert(F.anc.end(), al[(size_t)p].begin(), al[(size_t)p].end());
+      F.panels[(size_t)p].anc_end = (int32_t)F.anc.size();
+    }
+  }
+  // B~^T by permuted row (implicit apply, forward gather): transpose of the plan's stepped columns
+  {
+    F.bt_rp.assign((size_t)n + 1, 0);
+    for (int32_t r : C.ib_row) F.bt_rp[(size_t)r + 1]++;
+    for (int32_t r = 0; r < n; r++) F.bt_rp[(size_t)r + 1] += F.bt_rp[(size_t)r];
+    F.bt_a.assign(C.ib_row.size(), 0);
+    F.bt_v.assign(C.ib_row.size(), 0.0);
+    std::vector<int32_t> pos(F.bt_rp.begin(), F.bt_rp.end() - 1);
+    for (int32_t a = 0; a < C.m; a++)  // ascending stepped column within each row: a fixed summation order
+      for (int32_t e = C.ib_ptr[(size_t)a]; e < C.ib_ptr[(size_t)a + 1]; e++) {
+        const int32_t r = C.ib_row[(size_t)e];
+        F.bt_a[(size_t)pos[(size_t)r]] = a;
+        F.bt_v[(size_t)pos[(size_t)r]++] = C.ib_val[(size_t)e];
+      }
+  }
+  // frame update lists: for every update (d -> p) the diagonal frame gets (d, s0, s1, s0, s1); the
+  // rows R_d[s1, nR_d) are grouped by the row frame of p they fall in (two-pointer walk over R_p)
+  std::vector<std::vector<FFUpd>> fl(F.frames.size());
+  for (int32_t p = 0; p < np; p++) {
+    const FPanel& pn = F.panels[(size_t)p];
+    const int32_t* Rp = F.Rrows.data() + pn.R_off;
+    for (int32_t u = pn.upd_begin; u < pn.upd_end; u++) {
+      const FUpd U = F.upd[(size_t)u];
+      const FPanel& dn = F.panels[(size_t)U.d];
+      const int32_t* Rd = F.Rrows.data() + dn.R_off;
+      fl[(size_t)pn.frame_begin].push_back(FFUpd{U.d, U.s0, U.s1, U.s0, U.s1, 0});
+      int32_t k = U.s1;
+      int32_t ip = k < dn.nR ? (int32_t)(std::lower_bound(Rp, Rp + pn.nR, Rd[k]) - Rp) : pn.nR;
+      while (k < dn.nR && ip < pn.nR) {
+        const int32_t f = ip / kFW, fend = std::min(pn.nR, (f + 1) * kFW);
+        const int32_t k0 = k;
+        // rows of R_d up to the last row of this frame (rows of d missing from R_p are skipped later)
+        while (k < dn.nR && Rd[k] <= Rp[fend - 1]) k++;
+        if (k > k0) fl[(size_t)(pn.frame_begin + 1 + f)].push_back(FFUpd{U.d, U.s0, U.s1, k0, k, 0});
+        if (k < dn.nR) ip = (int32_t)(std::lower_bound(Rp + fend, Rp + pn.nR, Rd[k]) - Rp);
+      }
+    }
+  }
+  for (size_t f = 0; f < F.frames.size(); f++) {
+    F.frames[f].u_begin = (int32_t)F.fupd.size();
+    F.fupd.insert(F.fupd.end(), fl[f].begin(), fl[f].end());
+    F.frames[f].u_end = (int32_t)F.fupd.size();
+  }
   // 4. entry maps
   std::vector<int32_t> iperm((size_t)n);
   for (int32_t k = 0; k < n; k++) iperm[(size_t)C.perm[(size_t)k]] = k;
@@ -123,22 +181,24 @@ sc_status analyse_factor_class(const ClassPlan& C, const sc_K_pattern& K, Factor
     pos = (k % kFW) * kFW + (c - pn.a);
     return true;
   };
-  const int64_t nK = K.K_colptr[n];
-  F.nnzK = nK;
   std::vector<std::vector<FEnt>> kf(F.frames.size()), lf(F.frames.size());
-  for (int32_t j = 0; j < n; j++)
-    for (int64_t q = K.K_colptr[j]; q < K.K_colptr[j + 1]; q++) {
-      const int32_t i = K.K_rowidx[q];
-      const int32_t pi = iperm[(size_t)i], pj = iperm[(size_t)j];
-      const int32_t r = std::max(pi, pj), c = std::min(pi, pj);
-      int32_t fr, pos;
-      const bool inL = std::binary_search(ri + cp[c], ri + cp[c + 1], r);
-      if (!inL || !locate(r, c, fr, pos))
-        FFAIL(SC_ERR_PATTERN, "K entry (" + std::to_string(i) + ", " + std::to_string(j) +
-                                  ") lies outside the pattern of L (permuted (" + std::to_string(r) + ", " +
-                                  std::to_string(c) + "))");
-      kf[(size_t)fr].push_back(FEnt{(int32_t)q, pos});
-    }
+  if (Kp) {
+    const sc_K_pattern& K = *Kp;
+    F.nnzK = K.K_colptr[n];
+    for (int32_t j = 0; j < n; j++)
+      for (int64_t q = K.K_colptr[j]; q < K.K_colptr[j + 1]; q++) {
+        const int32_t i = K.K_rowidx[q];
+        const int32_t pi = iperm[(size_t)i], pj = iperm[(size_t)j];
+        const int32_t r = std::max(pi, pj), c = std::min(pi, pj);
+        int32_t fr, pos;
+        const bool inL = std::binary_search(ri + cp[c], ri + cp[c + 1], r);
+        if (!inL || !locate(r, c, fr, pos))
+          FFAIL(SC_ERR_PATTERN, "K entry (" + std::to_string(i) + ", " + std::to_string(j) +
+                                    ") lies outside the pattern of L (permuted (" + std::to_string(r) + ", " +
+                                    std::to_string(c) + "))");
+        kf[(size_t)fr].push_back(FEnt{(int32_t)q, pos});
+      }
+  }
   for (int32_t c = 0; c < n; c++)
     for (int64_t q = cp[c]; q < cp[c + 1]; q++) {
       int32_t fr, pos;
@@ -159,11 +219,11 @@ sc_status analyse_factor_class(const ClassPlan& C, const sc_K_pattern& K, Factor
     F.frames[f].l_end = (int32_t)F.lent.size();
   }
   // every diagonal of P K P^T must be present (a missing one is a structurally singular K)
-  {
+  if (Kp) {
     std::vector<char> hasd((size_t)n, 0);
     for (int32_t j = 0; j < n; j++)
-      for (int64_t q = K.K_colptr[j]; q < K.K_colptr[j + 1]; q++)
-        if (K.K_rowidx[q] == j) hasd[(size_t)j] = 1;
+      for (int64_t q = Kp->K_colptr[j]; q < Kp->K_colptr[j + 1]; q++)
+        if (Kp->K_rowidx[q] == j) hasd[(size_t)j] = 1;
     for (int32_t j = 0; j < n; j++)
       if (!hasd[(size_t)j]) FFAIL(SC_ERR_PATTERN, "K diagonal entry " + std::to_string(j) + " missing");
   }
@@ -197,12 +257,16 @@ bool same_K(const sc_K_pattern& a, const sc_K_pattern& b, int32_t n) {
 
 sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::string& err) {
   if (nsub != P.nsub) FFAIL(SC_ERR_INVALID_ARG, "sc_factor_attach: nsub differs from the plan's");
-  if (nsub > 0 && !kp) FFAIL(SC_ERR_INVALID_ARG, "sc_factor_attach: NULL K");
-  FactorPlan& F = P.fac;
+  FactorPlan& F = P.fac;  // kp == NULL: symbolic from L only (staging for the implicit apply)
+  F.has_K = kp != nullptr;
   const int32_t ncls = (int32_t)P.classes.size();
   std::vector<int32_t> rep((size_t)ncls, -1);
   for (int32_t i = 0; i < nsub; i++) {
     const int32_t c = P.sub_cls[(size_t)i];
+    if (!kp) {
+      if (rep[(size_t)c] < 0) rep[(size_t)c] = i;
+      continue;
+    }
     sc_status st = validate_K(kp[i], P.sub_n[(size_t)i], i, err);
     if (st != SC_OK) return st;
     if (rep[(size_t)c] < 0) {
@@ -215,7 +279,7 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
   F.classes.assign((size_t)ncls, FactorClass());
   for (int32_t c = 0; c < ncls; c++) {
     if (rep[(size_t)c] < 0) continue;
-    sc_status st = analyse_factor_class(P.classes[(size_t)c], kp[rep[(size_t)c]], F.classes[(size_t)c], err);
+    sc_status st = analyse_factor_class(P.classes[(size_t)c], kp ? &kp[rep[(size_t)c]] : nullptr, F.classes[(size_t)c], err);
     if (st != SC_OK) {
       err = "subdomain " + std::to_string(rep[(size_t)c]) + ": " + err;
       return st;
@@ -224,30 +288,47 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
   // globalise
   F.panels.clear();
   F.Rrows.clear();
-  F.upd.clear();
+  F.fupd.clear();
+  F.anc.clear();
+  F.bt_rp.clear();
+  F.bt_a.clear();
+  F.bt_v.clear();
+  F.cls_bt0.assign((size_t)ncls, 0);
   F.frames.clear();
   F.kent.clear();
   F.lent.clear();
   F.cls_panel0.assign((size_t)ncls + 1, 0);
   for (int32_t c = 0; c < ncls; c++) {
     const FactorClass& fc = F.classes[(size_t)c];
-    const int32_t p0 = (int32_t)F.panels.size(), r0 = (int32_t)F.Rrows.size(), u0 = (int32_t)F.upd.size();
+    const int32_t p0 = (int32_t)F.panels.size(), r0 = (int32_t)F.Rrows.size(), u0 = (int32_t)F.fupd.size();
     const int32_t f0 = (int32_t)F.frames.size(), k0 = (int32_t)F.kent.size(), l0 = (int32_t)F.lent.size();
     F.cls_panel0[(size_t)c] = p0;
+    const int32_t a0 = (int32_t)F.anc.size();
     for (FPanel pn : fc.panels) {
       pn.R_off += r0;
-      pn.upd_begin += u0;
-      pn.upd_end += u0;
       pn.frame_begin += f0;
+      pn.anc_begin += a0;
+      pn.anc_end += a0;
       F.panels.push_back(pn);
     }
-    F.Rrows.insert(F.Rrows.end(), fc.Rrows.begin(), fc.Rrows.end());
-    for (FUpd u : fc.upd) {
+    for (FUpd u : fc.anc) {
       u.d += p0;
-      F.upd.push_back(u);
+      F.anc.push_back(u);
+    }
+    F.cls_bt0[(size_t)c] = (int64_t)F.bt_rp.size();
+    const int32_t e0 = (int32_t)F.bt_a.size();
+    for (int32_t v : fc.bt_rp) F.bt_rp.push_back(v + e0);
+    F.bt_a.insert(F.bt_a.end(), fc.bt_a.begin(), fc.bt_a.end());
+    F.bt_v.insert(F.bt_v.end(), fc.bt_v.begin(), fc.bt_v.end());
+    F.Rrows.insert(F.Rrows.end(), fc.Rrows.begin(), fc.Rrows.end());
+    for (FFUpd u : fc.fupd) {
+      u.d += p0;
+      F.fupd.push_back(u);
     }
     for (FFrame fr : fc.frames) {
       fr.panel += p0;
+      fr.u_begin += u0;
+      fr.u_end += u0;
       fr.k_begin += k0;
       fr.k_end += k0;
       fr.l_begin += l0;
@@ -273,29 +354,45 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
     F.bytes_K += 8.0 * (double)fc.nnzK;
   }
   F.W_doubles = F.sub_W_base[(size_t)nsub];
+  F.sub_x_base.assign((size_t)nsub + 1, 0);
+  for (int32_t i = 0; i < nsub; i++) F.sub_x_base[(size_t)i + 1] = F.sub_x_base[(size_t)i] + P.sub_n[(size_t)i];
   F.nflags = F.sub_flag_base[(size_t)nsub];
-  // 5. task order: chunks of subdomains (the host-fed pipeline's granularity, also an L2-locality
-  // window), inside a chunk by (level, subdomain, panel, frame)
-  const int32_t nchunk = std::max<int32_t>(1, std::min<int32_t>(16, nsub / 64));
-  F.chunk_sub.assign((size_t)nchunk + 1, 0);
-  F.task_chunk.assign((size_t)nchunk + 1, 0);
+  // 5. task order, by (level, subdomain, panel, frame) over a range of subdomains: first over the
+  // whole batch (sc_factorize_batch: the critical path is the longest panel chain, every level of
+  // every subdomain is ready together), then per chunk of subdomains for the host-fed pipeline
+  // (chunk k's factorization overlaps chunk k-1's assembly); task_chunk holds absolute indices.
+  const char* me = std::getenv("SC_FACTOR_MERGE");
+  const int32_t merge = me ? std::atoi(me) : 6;  // panels with <= this many frames form one task
+  auto order = [&](int32_t s0, int32_t s1) {
+    int32_t maxlev = 0;
+    for (int32_t i = s0; i < s1; i++) maxlev = std::max(maxlev, F.classes[(size_t)P.sub_cls[(size_t)i]].max_level);
+    std::vector<std::vector<FTask>> bylev((size_t)maxlev + 1);
+    for (int32_t i = s0; i < s1; i++) {
+      const int32_t c = P.sub_cls[(size_t)i];
+      for (int32_t p = F.cls_panel0[(size_t)c]; p < F.cls_panel0[(size_t)c + 1]; p++) {
+        const FPanel& pn = F.panels[(size_t)p];
+        if (pn.nframe <= merge) {  // small panel: one warp does the diagonal and then its rows (no waits)
+          bylev[(size_t)pn.level].push_back(FTask{i, pn.frame_begin, pn.nframe, 0});
+        } else {
+          for (int32_t f = 0; f < pn.nframe; f++) bylev[(size_t)pn.level].push_back(FTask{i, pn.frame_begin + f, 1, 0});
+        }
+      }
+    }
+    for (auto& v : bylev) F.tasks.insert(F.tasks.end(), v.begin(), v.end());
+  };
   F.tasks.clear();
+  order(0, nsub);
+  F.ptasks.clear();  // implicit apply: one task per (subdomain, panel), the diagonal frames in this order
+  for (const FTask& t : F.tasks)
+    if (F.frames[(size_t)t.frame].r0 < 0) F.ptasks.push_back(I2{t.sub, F.frames[(size_t)t.frame].panel});
+  const int32_t nchunk = std::max<int32_t>(1, std::min<int32_t>(4, nsub / 64));
+  F.chunk_sub.assign((size_t)nchunk + 1, 0);
+  F.task_chunk.assign((size_t)nchunk + 1, (int64_t)F.tasks.size());
   for (int32_t k = 0; k < nchunk; k++) {
     const int32_t s0 = (int32_t)((int64_t)nsub * k / nchunk), s1 = (int32_t)((int64_t)nsub * (k + 1) / nchunk);
     F.chunk_sub[(size_t)k] = s0;
     F.chunk_sub[(size_t)k + 1] = s1;
-    int32_t maxlev = 0;
-    for (int32_t i = s0; i < s1; i++) maxlev = std::max(maxlev, F.classes[(size_t)P.sub_cls[(size_t)i]].max_level);
-    for (int32_t lev = 0; lev <= maxlev; lev++)
-      for (int32_t i = s0; i < s1; i++) {
-        const int32_t c = P.sub_cls[(size_t)i];
-        const int32_t p0 = F.cls_panel0[(size_t)c], p1 = F.cls_panel0[(size_t)c + 1];
-        for (int32_t p = p0; p < p1; p++) {
-          const FPanel& pn = F.panels[(size_t)p];
-          if (pn.level != lev) continue;
-          for (int32_t f = 0; f < pn.nframe; f++) F.tasks.push_back(FTask{i, pn.frame_begin + f});
-        }
-      }
+    order(s0, s1);
     F.task_chunk[(size_t)k + 1] = (int64_t)F.tasks.size();
   }
   if (F.tasks.size() > (size_t)INT32_MAX) FFAIL(SC_ERR_INVALID_ARG, "too many factorization tasks");

@@ -1450,91 +1450,6 @@ __global__ void __launch_bounds__(kThreads) apply_scatter_kernel(DevPlan P, doub
 //   backward, descending:       z_p = inv(L_pp)^T (y_p - L[R_p,p]^T z[R_p])   (W mode:
 //                               z_p = inv(L_pp)^T y_p - W_p^T z[R_p])
 // ------------------------------------------------------------------------------------------------
-template <bool SMEMV>
-__global__ void __launch_bounds__(kThreads) implicit_apply_kernel(DevPlan P, const double* __restrict__ lambda) {
-  extern __shared__ __align__(16) unsigned char iv_smem[];
-  __shared__ double yv[kMaxPanel], zv[kMaxPanel];
-  const int sub = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int cls = P.sub_cls[sub];
-  const int p0 = P.cls_panel0[cls], p1 = P.cls_panel0[cls + 1];
-  const int m = P.sub_m[sub];
-  int n = 0;
-  if (p1 > p0) {
-    const Panel last = P.panels[p1 - 1];
-    n = last.a + last.kw;
-  }
-  double* x = SMEMV ? reinterpret_cast<double*>(iv_smem) : P.xv + (int64_t)sub * P.max_n;
-  const double* __restrict__ PB = P.PB + P.sub_PB_base[sub];
-  const int32_t* __restrict__ ibp = P.ib_ptr + P.cls_ib0[cls];
-  const int64_t* __restrict__ slm = P.slm + P.sub_slm_off[sub];
-  for (int i = tid; i < n; i += kThreads) x[i] = 0.0;
-  __syncthreads();
-  for (int a = tid; a < m; a += kThreads) {  // x = P B~^T lambda_i
-    const double la = lambda[slm[a]];
-    for (int e = ibp[a]; e < ibp[a + 1]; e++) atomicAdd(&x[P.ib_row[e]], P.ib_val[e] * la);
-  }
-  __syncthreads();
-  for (int p = p0; p < p1; p++) {  // forward
-    const Panel pn = P.panels[p];
-    const double* inv = PB + pn.buf_off;
-    const double* ch0 = inv + (int64_t)pn.ldD * pn.kw4;
-    if (tid < pn.kw) {
-      double y = 0.0;
-#pragma unroll 8
-      for (int k = 0; k <= tid; k++) y = fma(__ldg(inv + k * pn.ldD + tid), x[pn.a + k], y);
-      yv[tid] = y;
-    }
-    __syncthreads();
-    // chunk rows: L (Y mode) times y, or W times the old x_p (W mode)
-    for (int k = tid; k < pn.nR; k += kThreads) {
-      const int c = k / kChunk, kr = k - c * kChunk;
-      const int ld = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
-      const double* col = ch0 + (int64_t)c * kLdC * pn.kw4 + kr;
-      double s = 0.0;
-#pragma unroll 8
-      for (int j = 0; j < pn.kw; j++) s = fma(__ldg(col + j * ld), P.wmode ? x[pn.a + j] : yv[j], s);
-      x[__ldg(P.Rrows + pn.R_off + k)] -= s;
-    }
-    __syncthreads();
-    if (tid < pn.kw) x[pn.a + tid] = yv[tid];
-    __syncthreads();
-  }
-  for (int p = p1 - 1; p >= p0; p--) {  // backward
-    const Panel pn = P.panels[p];
-    const double* inv = PB + pn.buf_off;
-    const double* ch0 = inv + (int64_t)pn.ldD * pn.kw4;
-    for (int j = warp; j < pn.kw; j += kThreads / 32) {  // s_j = sum_k L[R_k, j] z[R_k]
-      double s = 0.0;
-#pragma unroll 4
-      for (int k = lane; k < pn.nR; k += 32) {
-        const int c = k / kChunk, kr = k - c * kChunk;
-        const int ld = (c == pn.nchunk - 1) ? pn.ldLast : kLdC;
-        s = fma(__ldg(ch0 + (int64_t)c * kLdC * pn.kw4 + (int64_t)j * ld + kr), x[__ldg(P.Rrows + pn.R_off + k)], s);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) yv[j] = P.wmode ? s : x[pn.a + j] - s;
-    }
-    __syncthreads();
-    for (int j = warp; j < pn.kw; j += kThreads / 32) {  // z_j = sum_{r >= j} inv[r][j] v_r
-      double z = 0.0;
-      for (int r = j + lane; r < pn.kw; r += 32) z = fma(__ldg(inv + j * pn.ldD + r), P.wmode ? x[pn.a + r] : yv[r], z);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) z += __shfl_xor_sync(0xffffffffu, z, o);
-      if (lane == 0) zv[j] = P.wmode ? z - yv[j] : z;
-    }
-    __syncthreads();
-    if (tid < pn.kw) x[pn.a + tid] = zv[tid];
-    __syncthreads();
-  }
-  double* u = P.upart + P.sub_slm_off[sub];
-  for (int a = tid; a < m; a += kThreads) {  // u = B~ P^T z
-    double s = 0.0;
-    for (int e = ibp[a]; e < ibp[a + 1]; e++) s = fma(P.ib_val[e], x[P.ib_row[e]], s);
-    u[a] = s;
-  }
-}
-
 __global__ void __launch_bounds__(kThreads) implicit_scatter_kernel(DevPlan P, double* __restrict__ q, int64_t nl) {
   const int64_t gidx = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (gidx >= nl) return;
@@ -2021,7 +1936,6 @@ sc_status launch_assemble(Plan& P, const void* const* Lptr_host, void* stream_v,
   sc_status st = set_Lptr(P, Lptr_host, stream, err);
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
-  P.factor_ready = !P.warp_trsm;  // the warp TRSM does not stage the factor panels
   CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   if (P.overlap > 1 && P.nsub >= 2 * P.overlap) return launch_overlapped(P, stream, err);
   return launch_range(P, 0, P.nsub, stream, true, err);
@@ -2052,7 +1966,6 @@ sc_status assemble_stage_begin(Plan& P, std::vector<void*>& dptrs, void* stream_
   sc_status st = set_Lptr(P, cp.data(), stream, err);
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
-  P.factor_ready = !P.warp_trsm;  // the warp TRSM does not stage the factor panels
   CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   return SC_OK;
 }
@@ -2130,45 +2043,25 @@ sc_status launch_apply(Plan& P, const double* lambda, double* q, void* stream_v,
 sc_status launch_prepare(Plan& P, const void* const* Lptr_host, void* stream_v, std::string& err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   CUDA_TRY(cudaSetDevice(P.opt.device));
-  sc_status st = set_Lptr(P, Lptr_host, stream, err);
+  sc_status st = ensure_factor_plan(P, err);
+  if (st != SC_OK) return st;
+  st = set_Lptr(P, Lptr_host, stream, err);
   if (st != SC_OK) return st;
   P.last_stream = stream_v;
-  if (!P.dev.PB) {  // warp-TRSM plans stage the factor panels only for the implicit apply
-    double* pb = nullptr;
-    TRY(alloc_zero(P, P.PB_doubles, &pb, err));
-    P.dev.PB = pb;
-    P.stats.device_bytes += 8.0 * (double)P.PB_doubles;
-  }
   CUDA_TRY(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
-  st = launch_prep_range(P, 0, P.nsub, stream, err);
-  if (st == SC_OK) P.factor_ready = true;
-  return st;
+  return launch_stage(P, stream_v, err);
 }
 
 sc_status launch_apply_implicit(Plan& P, const double* lambda, double* q, void* stream_v, std::string& err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   CUDA_TRY(cudaSetDevice(P.opt.device));
-  if (!P.factor_ready) {
-    err = "no prepared factor: call sc_prepare_factor or sc_assemble_batch first";
+  if (!P.fac.ready || !P.fac.w_ready) {
+    err = "no factor in the workspace: call sc_prepare_factor or sc_factorize_batch first";
     return SC_ERR_STATE;
   }
   P.last_stream = stream_v;
-  const size_t vbytes = sizeof(double) * (size_t)P.max_n;
-  const bool in_smem = vbytes <= 200 * 1024;
-  if (!in_smem && !P.dev.xv) {
-    double* xv = nullptr;
-    TRY(alloc_zero(P, (int64_t)P.nsub * P.max_n, &xv, err));
-    P.dev.xv = xv;
-  }
-  if (P.nsub > 0) {
-    if (in_smem) {
-      CUDA_TRY(cudaFuncSetAttribute(implicit_apply_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vbytes));
-      implicit_apply_kernel<true><<<P.nsub, kThreads, vbytes, stream>>>(P.dev, lambda);
-    } else {
-      implicit_apply_kernel<false><<<P.nsub, kThreads, 0, stream>>>(P.dev, lambda);
-    }
-    CUDA_TRY(cudaGetLastError());
-  }
+  sc_status st = launch_implicit_solve(P, lambda, stream_v, err);
+  if (st != SC_OK) return st;
   if (P.n_lambda > 0) {
     const int64_t nb = (P.n_lambda + kThreads - 1) / kThreads;
     implicit_scatter_kernel<<<(unsigned)nb, kThreads, 0, stream>>>(P.dev, q, P.n_lambda);

@@ -202,10 +202,12 @@ constexpr int kFW = 32;         // factor panel width cap = frame rows = frame c
 // (nR x kw, column-major, ld nR) and inv(L_pp) at inv_off (kw8 x kw8, column-major, zero padded).
 struct FPanel {
   int32_t a, kw, nR, R_off;
-  int32_t upd_begin, upd_end;      // descendant updates of this panel (global indices into fupd)
+  int32_t upd_begin, upd_end;      // descendant updates of this panel (class-local indices into FactorClass::upd)
   int32_t frame_begin, nframe;     // 1 diagonal frame + ceil(nR / 32) row frames (global indices)
   int64_t w_off, inv_off;
   int32_t level, kw8;              // level: 0 = no descendants, else 1 + max over its descendants
+  int32_t anc_begin, anc_end;      // implicit apply (backward): the ancestor panels this panel updates
+                                   //   (global indices into fanc: {a, s0, s1} = R_p[s0, s1) in a's columns)
 };
 // Descendant panel d updates panel p: rows R_d[s0, s1) lie in [a_p, a_p + kw_p) (the columns of p),
 // rows R_d[s1, nR_d) below it (a subset of R_p by the closure of the fill pattern).
@@ -214,16 +216,26 @@ struct FUpd {
 };
 // Frame = one warp task: the diagonal block (r0 = -1, rows = the panel's columns) or 32 consecutive
 // rows R_p[r0, r0 + nrow) of a panel.  K / L entries of the frame: (value index within the subdomain's
-// CSC array, frame position row * 32 + col).
+// CSC array, frame position row * 32 + col).  Frame updates [u_begin, u_end): the descendant panels
+// that touch this frame (global indices into fupd).
 struct FFrame {
   int32_t panel, r0, nrow, pad;
   int32_t k_begin, k_end, l_begin, l_end;
+  int32_t u_begin, u_end;
+};
+// Descendant panel d updates one frame of p: the frame's columns get d's rows R_d[s0, s1) (values in
+// [a_p, a_p + kw_p)); its rows get R_d[k0, k1) (diagonal frame: k0 = s0, k1 = s1; row frame: the rows of
+// R_d below p's columns whose values fall in the frame's row range -- contiguous in R_d; a row of a
+// relaxed panel that is not in R_p contributes exact zeros and is skipped by the kernel).
+struct FFUpd {
+  int32_t d, s0, s1, k0, k1, pad;
 };
 struct FEnt {
   int32_t q, pos;
 };
 struct FTask {
   int32_t sub, frame;              // frame: global index
+  int32_t nf, pad;                 // frames [frame, frame + nf) of one panel, processed in order by one warp
 };
 
 // Host symbolic data of the device factorization, per pattern class.
@@ -232,7 +244,11 @@ struct FactorClass {
   std::vector<int32_t> Rrows;
   std::vector<FUpd> upd;
   std::vector<FFrame> frames;
+  std::vector<FFUpd> fupd;
   std::vector<FEnt> kent, lent;
+  std::vector<FUpd> anc;           // per panel (FPanel::anc_*): {ancestor a, s0, s1}
+  std::vector<int32_t> bt_rp, bt_a; // B~^T by permuted row (CSR, n+1 / entries): stepped column, value
+  std::vector<double> bt_v;
   int64_t nnzK = 0, w_doubles = 0;
   int32_t max_level = 0;
   double flops = 0;                // executed factorization flops per subdomain (updates + diag + TRSM)
@@ -243,7 +259,7 @@ struct FactorClass {
 struct DevFactor {
   const FPanel* panels;
   const int32_t* Rrows;            // concatenated per class; FPanel::R_off globalised
-  const FUpd* upd;
+  const FFUpd* fupd;
   const FFrame* frames;            // FFrame::k_* / l_* global indices into kent / lent
   const FEnt* kent;
   const FEnt* lent;
@@ -259,6 +275,18 @@ struct DevFactor {
   int32_t* queue;                  // task counters (one per launch slot)
   unsigned long long* err;
   int32_t fp32, pad;
+  // implicit apply on the factor workspace
+  const FUpd* anc;
+  const I2* ptasks;                // (sub, global panel) in forward (level) order; backward = reversed
+  const int32_t* bt_rp;            // per class (offset cls_bt0) CSR of B~^T by permuted row
+  const int32_t* bt_a;
+  const double* bt_v;
+  const int64_t* cls_bt0;          // per class: offset into bt_rp (n+1 entries); bt_rp values are global
+  const int64_t* sub_x_base;       // per subdomain: offset of its work vector in xv (n doubles)
+  double* xv;
+  const void* const* Lin;          // stage mode: the plan's L table (DevPlan::Lptr)
+  const int64_t* slm;              // = DevPlan::slm / sub_slm_off (stepped lambda map)
+  const int64_t* sub_slm_off;
 };
 
 struct FactorPlan {
@@ -266,10 +294,17 @@ struct FactorPlan {
   std::vector<FactorClass> classes;
   std::vector<FPanel> panels;      // global
   std::vector<int32_t> Rrows;
-  std::vector<FUpd> upd;
+  std::vector<FFUpd> fupd;
   std::vector<FFrame> frames;
   std::vector<FEnt> kent, lent;
   std::vector<FTask> tasks;
+  std::vector<FUpd> anc;
+  std::vector<I2> ptasks;
+  std::vector<int32_t> bt_rp, bt_a;
+  std::vector<double> bt_v;
+  std::vector<int64_t> cls_bt0, sub_x_base;
+  bool has_K = false;              // built with a K pattern (factorize), else staging from L only
+  bool w_ready = false;            // W holds the factor (last factorize or stage)
   std::vector<int64_t> task_chunk; // chunk c = tasks [task_chunk[c], task_chunk[c+1]) of subdomains
   std::vector<int32_t> chunk_sub;  //   [chunk_sub[c], chunk_sub[c+1]) (host-fed pipeline granularity)
   std::vector<int64_t> sub_W_base, sub_flag_base, sub_nnzK;
@@ -282,6 +317,8 @@ struct FactorPlan {
   void** d_ptrs = nullptr;
   void* ptr_event = nullptr;
   void* d_Kstage = nullptr;        // host-fed path: K values staging
+  void* fstream = nullptr;         // host-fed path: factorization stream (overlaps the assembly)
+  std::vector<void*> fev;          // per chunk: factorization done
   std::vector<int64_t> Kstage_off;
 };
 
@@ -337,7 +374,6 @@ struct DevPlan {
   unsigned long long* err;         // sticky device error: [0] = ((sub+1) << 32) | col, [1+sub] = col+1
   const int32_t* gidx;             // warp TRSM gather maps (all classes; Panel::gx_off is global)
   int32_t nsub, max_n, T, G;
-  int32_t factor_ready;            // (host-side bookkeeping mirrors Plan::factor_ready)
   int32_t wmode;                         // 1: chunks hold W_p = L[R_p,p] inv(L_pp) (W mode), 0: L (Y mode)
   int32_t fp32;                          // precision 32: L, X and F' stored in FP32 (FP64 arithmetic)
 };
@@ -347,7 +383,6 @@ struct Plan {
   int32_t T = 32, G = 64, PW = 64, ring_bytes = 0;
   bool gstrip = false;             // X strips solved in place in the group strips (global memory)
   int32_t gs2 = 0;                 // global strips at T = 16 with this many CTAs per SM (2; 3 via SC_GS2=3)
-  bool factor_ready = false;       // panel buffers hold the factor of the last prepare / assemble
   bool wmode = true;               // TRSM update operand W_p = L[R_p,p] inv(L_pp) (wide panels) or L (Y mode)
   bool warp_trsm = false;          // fused warp-per-tile TRSM straight from the CSC values (no prep)
   int32_t warp_ctas = 4;           // warps (tiles) per CTA of the warp TRSM
@@ -426,6 +461,9 @@ sc_status upload_factor_plan(Plan& P, std::string& err);
 void free_factor_device(Plan& P);
 sc_status launch_factorize(Plan& P, const void* const* Kptr, void* const* Lout, void* stream, std::string& err);
 sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* stream, std::string& err);
+sc_status launch_stage(Plan& P, void* stream, std::string& err);
+sc_status launch_implicit_solve(Plan& P, const double* lambda, void* stream, std::string& err);
+sc_status ensure_factor_plan(Plan& P, std::string& err);  // K-less factor plan for the implicit apply
 
 // pcpg.cu
 sc_status pcpg_solve(Plan& P, const double* d, const double* e_host, double* lambda, const sc_coarse* cs,
