@@ -139,6 +139,7 @@ typedef struct {
   int64_t factor_panels;        /* factor panels (<= 32 columns), summed over subdomains              */
   int32_t factor_max_level;     /* longest elimination-tree chain of factor panels (critical path)     */
   int32_t pad1;
+  double bytes_factor_W;        /* factor workspace: rows below each panel + inverted diagonal blocks  */
 } sc_stats;
 
 /* Fill `opt` with defaults: precision 64, skip EXACT, tile/panel auto, device 0. */

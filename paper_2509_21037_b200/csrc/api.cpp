@@ -132,6 +132,7 @@ sc_status sc_factor_attach(sc_plan_t p, const sc_K_pattern* K, int32_t nsub) {
   S.flops_factor_executed = F.flops;
   S.bytes_K_values = F.bytes_K;
   S.factor_tasks = F.task_chunk.empty() ? 0 : F.task_chunk[0];
+  S.bytes_factor_W = 8.0 * (double)F.W_doubles;
   S.factor_panels = 0;
   S.factor_max_level = 0;
   for (int32_t i = 0; i < p->P.nsub; i++) {

@@ -57,7 +57,7 @@ class Stats(ctypes.Structure):
                 ("bytes_X_reach", ctypes.c_double), ("flops_factor_useful", ctypes.c_double),
                 ("flops_factor_executed", ctypes.c_double), ("bytes_K_values", ctypes.c_double),
                 ("factor_tasks", ctypes.c_int64), ("factor_panels", ctypes.c_int64),
-                ("factor_max_level", ctypes.c_int32), ("pad1", ctypes.c_int32)]
+                ("factor_max_level", ctypes.c_int32), ("pad1", ctypes.c_int32), ("bytes_factor_W", ctypes.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
