@@ -69,6 +69,13 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// 16-byte global -> shared copy, zero-filled when src_bytes == 0 (L2 only: .cg)
+__device__ __forceinline__ void cp_async16z(void* dst, const void* src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_f() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all_f() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFactor F, int64_t t0, int64_t t1, int slot,
                                                                  int stage) {
   extern __shared__ double fsm[];
@@ -106,13 +113,13 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
     for (int u0 = fr.u_begin; u0 < (stage ? fr.u_begin : fr.u_end); u0 += 32) {
       const int nu = min(32, fr.u_end - u0);
       FFUpd U{};
-      int dkw = 0, dnR = 0, dR = 0;
+      int dkw = 0, dkw8 = 0, dR = 0;
       int64_t dw = 0;
       if (lane < nu) {
         U = F.fupd[u0 + lane];
         const FPanel dn = F.panels[U.d];
         dkw = dn.kw;
-        dnR = dn.nR;
+        dkw8 = dn.kw8;
         dR = dn.R_off;
         dw = dn.w_off;
         const int* fl = flags + U.d;
@@ -124,7 +131,7 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
       for (int j = 0; j < nu; j++) {
         const int s0 = __shfl_sync(~0u, U.s0, j), s1 = __shfl_sync(~0u, U.s1, j);
         const int k0 = __shfl_sync(~0u, U.k0, j), k1 = __shfl_sync(~0u, U.k1, j);
-        const int ukw = __shfl_sync(~0u, dkw, j), ldd = __shfl_sync(~0u, dnR, j), uR = __shfl_sync(~0u, dR, j);
+        const int ukw = __shfl_sync(~0u, dkw, j), ukw8 = __shfl_sync(~0u, dkw8, j), uR = __shfl_sync(~0u, dR, j);
         const int64_t uw = __shfl_sync(~0u, dw, j);
         const int32_t* Rd = F.Rrows + uR;
         // columns: R_d[s0, s1) are columns of this panel (value - a); rows: R_d[k0, k1) -> frame rows
@@ -150,54 +157,37 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
         const int ridx = rmap[lane], cidx = cmap[lane];
         const unsigned rm = __ballot_sync(~0u, ridx >= 0), cm = __ballot_sync(~0u, cidx >= 0);
         if (!rm || !cm) continue;
-        const double* Wd = W + uw;
-        int ri[4], ci[4];
+        // DMMA fragments gathered straight from the workspace rows of d (row-major, kw8 wide; L2):
+        // A = L[frame rows, d] (row ridx), B = L[frame columns, d] (row cidx)
+        const double* Wd = W + uw + t;
+        int oa[4], ob[4];  // row offsets of the fragments' rows in d's workspace, -1 = zero / inactive block
 #pragma unroll
-        for (int I = 0; I < 4; I++) ri[I] = __shfl_sync(~0u, ridx, 8 * I + g);
+        for (int I = 0; I < 4; I++) {
+          const int r = __shfl_sync(~0u, ridx, 8 * I + g);
+          oa[I] = (I < nI && ((rm >> (8 * I)) & 0xFFu) && r >= 0) ? r * ukw8 : -1;
+        }
 #pragma unroll
-        for (int J = 0; J < 4; J++) ci[J] = __shfl_sync(~0u, cidx, 8 * J + g);
-        bool ra[4], ca[4];
+        for (int J = 0; J < 4; J++) {
+          const int c = __shfl_sync(~0u, cidx, 8 * J + g);
+          ob[J] = (J < nJ && ((cm >> (8 * J)) & 0xFFu) && c >= 0) ? c * ukw8 : -1;
+        }
+        bool ra[4], ca[4];  // warp-uniform block activity
 #pragma unroll
         for (int I = 0; I < 4; I++) ra[I] = I < nI && ((rm >> (8 * I)) & 0xFFu);
 #pragma unroll
         for (int J = 0; J < 4; J++) ca[J] = J < nJ && ((cm >> (8 * J)) & 0xFFu);
-        // k loop software-pipelined: the fragments of step kb + 4 are in flight during the DMMAs of kb
-        auto load = [&](int kb, double (&a)[4], double (&b)[4]) {
-          const int kk = kb + t;
-          const bool kv = kk < ukw;
-          const double* col = Wd + (int64_t)kk * ldd;
-#pragma unroll
-          for (int I = 0; I < 4; I++) a[I] = (ra[I] && kv && ri[I] >= 0) ? __ldcg(col + ri[I]) : 0.0;
-#pragma unroll
-          for (int J = 0; J < 4; J++) b[J] = (ca[J] && kv && ci[J] >= 0) ? __ldcg(col + ci[J]) : 0.0;
-        };
-#if SC_FPREFETCH
-        double a[4], b[4], an[4], bn[4];
-        load(0, a, b);
-        for (int kb = 0; kb < ukw; kb += 4) {
-          if (kb + 4 < ukw) load(kb + 4, an, bn);
-#pragma unroll
-          for (int I = 0; I < 4; I++)
-#pragma unroll
-            for (int J = 0; J < 4; J++)
-              if (ra[I] && ca[J] && (!diag || J <= I)) fdmma(acc[I][J][0], acc[I][J][1], a[I], b[J]);
-#pragma unroll
-          for (int q = 0; q < 4; q++) {
-            a[q] = an[q];
-            b[q] = bn[q];
-          }
-        }
-#else
-        for (int kb = 0; kb < ukw; kb += 4) {
+        for (int kb = 0; kb < ukw; kb += 4) {  // kb + t < ukw8: the padding columns of a row are zeros
           double a[4], b[4];
-          load(kb, a, b);
+#pragma unroll
+          for (int I = 0; I < 4; I++) a[I] = oa[I] >= 0 ? __ldcg(Wd + oa[I] + kb) : 0.0;
+#pragma unroll
+          for (int J = 0; J < 4; J++) b[J] = ob[J] >= 0 ? __ldcg(Wd + ob[J] + kb) : 0.0;
 #pragma unroll
           for (int I = 0; I < 4; I++)
 #pragma unroll
             for (int J = 0; J < 4; J++)
               if (ra[I] && ca[J] && (!diag || J <= I)) fdmma(acc[I][J][0], acc[I][J][1], a[I], b[J]);
         }
-#endif
       }
     }
 
@@ -285,10 +275,12 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
         for (int i = 0; i < kFW; i++)
           if (i < pn.kw8) Winv[lane * pn.kw8 + i] = x[i];
       }
-    } else if (stage) {  // the rows of the given L go to the workspace as they are
+    } else if (stage) {  // the rows of the given L go to the workspace as they are (row-major, kw8 wide)
       double* Wp = W + pn.w_off;
-      for (int c = 0; c < kw; c++)
-        if (lane < fr.nrow) Wp[(int64_t)c * pn.nR + fr.r0 + lane] = S[lane * kSLd + c];
+      if (lane < fr.nrow)
+        for (int c = 0; c < pn.kw8; c += 2)
+          *reinterpret_cast<double2*>(Wp + (int64_t)(fr.r0 + lane) * pn.kw8 + c) =
+              make_double2(S[lane * kSLd + c], S[lane * kSLd + c + 1]);
     } else {
       // ---- wait for the panel's own diagonal frame, then X = S inv(L_pp)^T
       if (lane == 0) {
@@ -325,10 +317,8 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
             const int r = 8 * I + g, c = 8 * J + 2 * t;
             S[r * kSLd + c] = acc[I][J][0];
             S[r * kSLd + c + 1] = acc[I][J][1];
-            if (r < fr.nrow) {
-              if (c < kw) Wp[(int64_t)c * pn.nR + fr.r0 + r] = acc[I][J][0];
-              if (c + 1 < kw) Wp[(int64_t)(c + 1) * pn.nR + fr.r0 + r] = acc[I][J][1];
-            }
+            if (r < fr.nrow)  // row-major, kw8 wide (the padding columns are exact zeros)
+              *reinterpret_cast<double2*>(Wp + (int64_t)(fr.r0 + r) * pn.kw8 + c) = make_double2(acc[I][J][0], acc[I][J][1]);
           }
     }
     __syncwarp();
@@ -407,7 +397,7 @@ __global__ void __launch_bounds__(32 * kFWarps) implicit_fwd_kernel(DevFactor F,
         U = F.fupd[u0 + lane];
         const FPanel dn = F.panels[U.d];
         dkw = dn.kw;
-        dnR = dn.nR;
+        dnR = dn.kw8;  // row stride of the workspace rows
         dR = dn.R_off;
         da = dn.a;
         dw = dn.w_off;
@@ -418,20 +408,23 @@ __global__ void __launch_bounds__(32 * kFWarps) implicit_fwd_kernel(DevFactor F,
       __syncwarp();
       for (int j = 0; j < nu; j++) {
         const int s0 = __shfl_sync(~0u, U.s0, j), s1 = __shfl_sync(~0u, U.s1, j);
-        const int ukw = __shfl_sync(~0u, dkw, j), ldd = __shfl_sync(~0u, dnR, j), uR = __shfl_sync(~0u, dR, j);
+        const int ukw = __shfl_sync(~0u, dkw, j), ukw8 = __shfl_sync(~0u, dnR, j), uR = __shfl_sync(~0u, dR, j);
         const int ua = __shfl_sync(~0u, da, j);
         const int64_t uw = __shfl_sync(~0u, dw, j);
         if (lane < s1 - s0) {
-          const double* col = W + uw + s0 + lane;
+          const double* row = W + uw + (int64_t)(s0 + lane) * ukw8;  // row-major, kw8 wide
           double v = 0.0;
 #pragma unroll
           for (int h = 0; h < kFW; h += 16) {  // 16 loads in flight, then the fixed-order sum
             double w[16], xk[16];
 #pragma unroll
-            for (int k = 0; k < 16; k++) {
-              w[k] = h + k < ukw ? __ldcg(col + (int64_t)(h + k) * ldd) : 0.0;
-              xk[k] = h + k < ukw ? __ldcg(x + ua + h + k) : 0.0;
+            for (int k = 0; k < 16; k += 2) {
+              const double2 w2 = h + k < ukw ? __ldcg(reinterpret_cast<const double2*>(row + h + k)) : make_double2(0.0, 0.0);
+              w[k] = w2.x;
+              w[k + 1] = w2.y;
             }
+#pragma unroll
+            for (int k = 0; k < 16; k++) xk[k] = h + k < ukw ? __ldcg(x + ua + h + k) : 0.0;
 #pragma unroll
             for (int k = 0; k < 16; k++) v = fma(w[k], xk[k], v);
           }
@@ -485,9 +478,14 @@ __global__ void __launch_bounds__(32 * kFWarps) implicit_bwd_kernel(DevFactor F,
     for (int r0 = 0; r0 < pn.nR; r0 += 32) {
       const int r = r0 + lane;
       const double z = r < pn.nR ? __ldcg(x + __ldg(F.Rrows + pn.R_off + r)) : 0.0;
+      const double* row = Wp + (int64_t)r * pn.kw8;  // row-major, kw8 wide
 #pragma unroll
-      for (int k = 0; k < kFW; k++)
-        if (k < kw && r < pn.nR) part[k] = fma(__ldcg(Wp + (int64_t)k * pn.nR + r), z, part[k]);
+      for (int k = 0; k < kFW; k += 2)
+        if (k < kw && r < pn.nR) {
+          const double2 w2 = __ldcg(reinterpret_cast<const double2*>(row + k));
+          part[k] = fma(w2.x, z, part[k]);
+          part[k + 1] = fma(w2.y, z, part[k + 1]);
+        }
     }
     double s = 0.0;
 #pragma unroll

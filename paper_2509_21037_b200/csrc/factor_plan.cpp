@@ -42,7 +42,11 @@ sc_status analyse_factor_class(const ClassPlan& C, const sc_K_pattern* Kp, Facto
   for (int32_t c = 0; c < n; c++)
     if (cp[c + 1] - cp[c] > 1) parent[(size_t)c] = ri[cp[c] + 1];
   std::vector<PanelPart> parts;
-  partition_panels(n, cp, ri, parent, kFW, parts);
+  // relaxation of the factor panels (explicit zeros cost workspace bytes and update flops here, and
+  // panels cost tasks): SC_FACTOR_ZMAX / SC_FACTOR_WSMALL, default the TRSM's rule
+  const char* ez = std::getenv("SC_FACTOR_ZMAX");
+  const char* ew = std::getenv("SC_FACTOR_WSMALL");
+  partition_panels(n, cp, ri, parent, kFW, parts, ez ? std::atof(ez) : -1.0, ew ? std::atoi(ew) : -1);
   std::vector<int32_t> poc((size_t)n, -1);
   for (size_t k = 0; k < parts.size(); k++) {
     FPanel p{};
@@ -96,7 +100,7 @@ sc_status analyse_factor_class(const ClassPlan& C, const sc_K_pattern* Kp, Facto
       F.frames.push_back(fr);
     }
     pn.w_off = w;
-    w += (int64_t)pn.nR * pn.kw;
+    w += (int64_t)pn.nR * pn.kw8;  // row-major rows, kw8 wide (16-byte aligned rows for cp.async)
     pn.inv_off = w;
     w += (int64_t)pn.kw8 * pn.kw8;
     F.flops += (double)pn.kw * pn.kw * pn.kw / 3.0 * 2.0 + 2.0 * pn.nR * (double)pn.kw * pn.kw;

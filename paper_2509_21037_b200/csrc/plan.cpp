@@ -134,7 +134,7 @@ int relax_wsmall() {
 // (<= SC_RELAX_WSMALL columns) -- relaxed amalgamation.  R = the panel's pruned below-diagonal rows
 // (P:494), the union of its columns' rows below the panel.  Returns the number of supernodes.
 int32_t partition_panels(int32_t n, const int64_t* cp, const int32_t* ri, const std::vector<int32_t>& parent, int PW,
-                         std::vector<PanelPart>& out) {
+                         std::vector<PanelPart>& out, double zmax, int wsmall) {
   auto cc = [&](int32_t c) { return (int32_t)(cp[c + 1] - cp[c]); };
   std::vector<int32_t> sn_c0, sn_c1;
   for (int32_t c = 0; c < n;) {
@@ -145,8 +145,8 @@ int32_t partition_panels(int32_t n, const int64_t* cp, const int32_t* ri, const 
     sn_c1.push_back(c);
   }
   const int32_t nsup = (int32_t)sn_c0.size();
-  const double zmax = relax_zmax();
-  const int wsmall = relax_wsmall();
+  if (zmax < 0) zmax = relax_zmax();
+  if (wsmall < 0) wsmall = relax_wsmall();
   PanelPart open;
   double open_nnz = 0;
   auto close_open = [&]() {

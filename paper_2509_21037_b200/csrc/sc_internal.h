@@ -199,7 +199,8 @@ struct ClassPlan {
 constexpr int kFW = 32;         // factor panel width cap = frame rows = frame columns
 // Factor panel: columns [a, a+kw), below-diagonal rows R = fRrows[R_off .. R_off+nR) (ascending).
 // Workspace per subdomain (doubles from the subdomain's base): the finished L[R, panel] at w_off
-// (nR x kw, column-major, ld nR) and inv(L_pp) at inv_off (kw8 x kw8, column-major, zero padded).
+// (nR x kw8, row-major: row r at w_off + r kw8, padding columns zero) and inv(L_pp) at inv_off
+// (kw8 x kw8, column-major, zero padded).
 struct FPanel {
   int32_t a, kw, nR, R_off;
   int32_t upd_begin, upd_end;      // descendant updates of this panel (class-local indices into FactorClass::upd)
@@ -437,8 +438,9 @@ struct PanelPart {
   int32_t a = -1, b = -1, merged = 0;  // columns [a, b); merged: relaxed (several supernodes)
   std::vector<int32_t> R;              // rows below the panel, ascending
 };
+// zmax / wsmall < 0: the TRSM defaults (SC_RELAX_ZMAX / SC_RELAX_WSMALL)
 int32_t partition_panels(int32_t n, const int64_t* cp, const int32_t* ri, const std::vector<int32_t>& parent, int PW,
-                         std::vector<PanelPart>& out);
+                         std::vector<PanelPart>& out, double zmax = -1.0, int wsmall = -1);
 sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options& opt, Plan& P, std::string& err);
 
 // kernels.cu
