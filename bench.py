@@ -189,12 +189,14 @@ def setup_problem(args, cfg, world, rank):
     from synth import config_problem
     from synth.mesh import CONFIGS, make_problem
     if args.weak or world == 1:
+        if args.perturbed:  # one fill-reducing ordering (L pattern) per subdomain: plan-time / memory stress
+            return make_problem(name=cfg, perturbed=True, seed=rank if args.weak else 0, **CONFIGS[cfg]), None
         return config_problem(cfg, seed=rank if args.weak else 0), None
     from paper_2509_21037_b200.shard import imbalance, lpt_partition
-    Pall = config_problem(cfg)
+    Pall = make_problem(name=cfg, perturbed=True, **CONFIGS[cfg]) if args.perturbed else config_problem(cfg)
     costs = SCPlan(Pall.subdomains, n_lambda=Pall.n_lambda, device=-1).subdomain_costs()
     parts = lpt_partition(costs, world)
-    P = make_problem(name=cfg, subdomains=parts[rank], **CONFIGS[cfg])
+    P = make_problem(name=cfg, subdomains=parts[rank], perturbed=args.perturbed, **CONFIGS[cfg])
     info = {"nsub_total": len(Pall.subdomains), "imbalance": imbalance(costs, parts),
             "partition": "LPT on the planner's executed-flop cost", "nsub_per_rank": [len(p) for p in parts]}
     return P, info
@@ -378,6 +380,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-amortization", action="store_true")
     ap.add_argument("--no-factor", action="store_true", help="skip the device factorization (f4) timing / K-fed e2e")
+    ap.add_argument("--perturbed", action="store_true",
+                    help="a distinct fill-reducing ordering (L pattern) per subdomain: every subdomain its own plan "
+                         "class (plan time / plan memory at the scale of a graph-partitioned mesh)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup(args)
@@ -396,13 +401,16 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = load_peaks()
 
-    t_plan0 = time.perf_counter()
     P, shard_info = setup_problem(args, args.config, world, rank)
+    import psutil
+    rss0 = psutil.Process().memory_info().rss
+    t_plan0 = time.perf_counter()
     skip = {"none": 0, "envelope": 1, "exact": 2}[args.skip]
     plan = SCPlan(P.subdomains, n_lambda=P.n_lambda, skip=skip, tile_cols=args.tile, panel_cols=args.panel,
                   device=local, x_strip={"auto": 0, "shared": 1, "global": 2}[args.strip],
                   trsm_kernel={"auto": 0, "cta": 1, "warp": 2}[args.trsm])
     t_plan = time.perf_counter() - t_plan0
+    plan_rss_mb = (psutil.Process().memory_info().rss - rss0) / 1e6
     st = plan.stats()
     Ls = [torch.from_numpy(np.ascontiguousarray(sd.L_values)).cuda() for sd in P.subdomains]
     nsub = len(P.subdomains)
@@ -576,7 +584,9 @@ def main():
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "e2e_from_L": e2e_L, "factor": factor,
         "amortization": amort,
         "gpu_launches": args.steps * plan.launches_per_assemble,
-        "clocks": clocks, "plan_s": t_plan, "per_config": per_config,
+        "clocks": clocks, "plan_s": t_plan, "plan_host_rss_mb": plan_rss_mb, "n_classes": st["n_classes"],
+        "patterns": "perturbed: one ordering per subdomain" if args.perturbed else "one per boundary class",
+        "per_config": per_config,
         "paper_context": {"a100_sep_opt_ms_per_subdomain": PAPER_A100_MS.get(args.config),
                           "note": "PAPER.md Fig. 8, A100, triangles/tets; context only"},
     }

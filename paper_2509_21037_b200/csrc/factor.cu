@@ -363,29 +363,51 @@ __device__ __forceinline__ void wait_flag(const int* f, int target) {
   while (ld_relaxed(f) < target) __nanosleep(32);
 }
 
-__global__ void __launch_bounds__(32 * kFWarps) implicit_fwd_kernel(DevFactor F, const double* __restrict__ lambda,
-                                                                    int64_t ntask) {
+// b = P B~^T lambda_i for every permuted row of every subdomain (by row, fixed order), into the work
+// vectors; the forward tasks then read their b_p with one load
+__global__ void __launch_bounds__(256) implicit_b_kernel(DevFactor F, const double* __restrict__ lambda, int nmax) {
+  const int sub = blockIdx.y, cls = F.sub_cls[sub];
+  const int n = (int)(F.sub_x_base[sub + 1] - F.sub_x_base[sub]);
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int32_t* rp = F.bt_rp + F.cls_bt0[cls];
+  const int64_t* slm = F.slm + F.sub_slm_off[sub];
+  double b = 0.0;
+  for (int e = rp[r]; e < rp[r + 1]; e++) b = fma(F.bt_v[e], __ldg(lambda + slm[F.bt_a[e]]), b);
+  F.xv[F.sub_x_base[sub] + r] = b;
+  (void)nmax;
+}
+
+__global__ void __launch_bounds__(32 * kFWarps) implicit_fwd_kernel(DevFactor F, int64_t ntask) {
   __shared__ double acc_s[kFWarps][kFW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double* acc = acc_s[warp];
-  for (;;) {
-    int64_t task = 0;
-    if (lane == 0) task = atomicAdd(F.queue + 2, 1);
-    task = __shfl_sync(~0u, task, 0);
-    if (task >= ntask) break;
-    const I2 pt = F.ptasks[task];
+  // the next task's index and descriptors are fetched while the current one runs
+  int64_t task = 0;
+  if (lane == 0) task = atomicAdd(F.queue + 2, 1);
+  task = __shfl_sync(~0u, task, 0);
+  I2 pt_n{};
+  FPanel pn_n{};
+  if (task < ntask) {
+    pt_n = F.ptasks[task];
+    pn_n = F.panels[pt_n.y];
+  }
+  while (task < ntask) {
+    const I2 pt = pt_n;
+    const FPanel pn = pn_n;
+    int64_t next = 0;
+    if (lane == 0) next = atomicAdd(F.queue + 2, 1);
+    next = __shfl_sync(~0u, next, 0);
+    if (next < ntask) {
+      pt_n = F.ptasks[next];
+      pn_n = F.panels[pt_n.y];
+    }
     const int sub = pt.x, cls = F.sub_cls[sub];
-    const FPanel pn = F.panels[pt.y];
     int* flags = F.flags + (F.sub_flag_base[sub] - F.cls_panel0[cls]);
     const double* W = F.W + F.sub_W_base[sub];
     double* x = F.xv + F.sub_x_base[sub];
     const int kw = pn.kw;
-    double b = 0.0;
-    if (lane < kw) {
-      const int32_t* rp = F.bt_rp + F.cls_bt0[cls];
-      const int64_t* slm = F.slm + F.sub_slm_off[sub];
-      for (int e = rp[pn.a + lane]; e < rp[pn.a + lane + 1]; e++) b = fma(F.bt_v[e], __ldg(lambda + slm[F.bt_a[e]]), b);
-    }
+    const double b = lane < kw ? x[pn.a + lane] : 0.0;  // P B~^T lambda (implicit_b_kernel)
     acc[lane] = 0.0;
     const FFrame fr = F.frames[pn.frame_begin];
     for (int u0 = fr.u_begin; u0 < fr.u_end; u0 += 32) {
@@ -449,19 +471,32 @@ __global__ void __launch_bounds__(32 * kFWarps) implicit_fwd_kernel(DevFactor F,
       __threadfence();
       atomicAdd(flags + pt.y, 1);
     }
+    task = next;
   }
 }
 
 __global__ void __launch_bounds__(32 * kFWarps) implicit_bwd_kernel(DevFactor F, int64_t ntask) {
   const int lane = threadIdx.x & 31;
-  for (;;) {
-    int64_t task = 0;
-    if (lane == 0) task = atomicAdd(F.queue + 3, 1);
-    task = __shfl_sync(~0u, task, 0);
-    if (task >= ntask) break;
-    const I2 pt = F.ptasks[ntask - 1 - task];
+  int64_t task = 0;
+  if (lane == 0) task = atomicAdd(F.queue + 3, 1);
+  task = __shfl_sync(~0u, task, 0);
+  I2 pt_n{};
+  FPanel pn_n{};
+  if (task < ntask) {
+    pt_n = F.ptasks[ntask - 1 - task];
+    pn_n = F.panels[pt_n.y];
+  }
+  while (task < ntask) {
+    const I2 pt = pt_n;
+    const FPanel pn = pn_n;
+    int64_t next = 0;
+    if (lane == 0) next = atomicAdd(F.queue + 3, 1);
+    next = __shfl_sync(~0u, next, 0);
+    if (next < ntask) {
+      pt_n = F.ptasks[ntask - 1 - next];
+      pn_n = F.panels[pt_n.y];
+    }
     const int sub = pt.x, cls = F.sub_cls[sub];
-    const FPanel pn = F.panels[pt.y];
     int* flags = F.flags + (F.sub_flag_base[sub] - F.cls_panel0[cls]);
     const double* W = F.W + F.sub_W_base[sub];
     double* x = F.xv + F.sub_x_base[sub];
@@ -513,6 +548,7 @@ __global__ void __launch_bounds__(32 * kFWarps) implicit_bwd_kernel(DevFactor F,
       __threadfence();
       atomicAdd(flags + pt.y, 1);
     }
+    task = next;
   }
 }
 
@@ -720,7 +756,11 @@ sc_status launch_implicit_solve(Plan& P, const double* lambda, void* stream_v, s
       cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((nt + kFWarps - 1) / kFWarps, (int64_t)nsm * 8));
-    implicit_fwd_kernel<<<grid, 32 * kFWarps, 0, stream>>>(F.dev, lambda, nt);
+    int nmax = 0;
+    for (int32_t i = 0; i < P.nsub; i++) nmax = std::max(nmax, (int)(F.sub_x_base[(size_t)i + 1] - F.sub_x_base[(size_t)i]));
+    implicit_b_kernel<<<dim3((unsigned)((nmax + 255) / 256), (unsigned)P.nsub), 256, 0, stream>>>(F.dev, lambda, nmax);
+    FCUDA(cudaGetLastError());
+    implicit_fwd_kernel<<<grid, 32 * kFWarps, 0, stream>>>(F.dev, nt);
     FCUDA(cudaGetLastError());
     implicit_bwd_kernel<<<grid, 32 * kFWarps, 0, stream>>>(F.dev, nt);
     FCUDA(cudaGetLastError());

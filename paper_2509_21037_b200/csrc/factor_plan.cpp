@@ -17,6 +17,8 @@
 //   5. the task order: chunks of subdomains, inside a chunk by (level, subdomain, panel, frame), so
 //      every dependency precedes its dependants in the queue (the kernel's deadlock-freedom argument).
 #include <algorithm>
+#include <atomic>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -281,13 +283,27 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
     }
   }
   F.classes.assign((size_t)ncls, FactorClass());
-  for (int32_t c = 0; c < ncls; c++) {
-    if (rep[(size_t)c] < 0) continue;
-    sc_status st = analyse_factor_class(P.classes[(size_t)c], kp ? &kp[rep[(size_t)c]] : nullptr, F.classes[(size_t)c], err);
-    if (st != SC_OK) {
-      err = "subdomain " + std::to_string(rep[(size_t)c]) + ": " + err;
-      return st;
-    }
+  {  // classes are independent: analysed on all host threads (first error wins, by class order)
+    std::vector<sc_status> cst((size_t)ncls, SC_OK);
+    std::vector<std::string> cerr((size_t)ncls);
+    std::atomic<int32_t> next{0};
+    auto work = [&]() {
+      for (int32_t c = next++; c < ncls; c = next++) {
+        if (rep[(size_t)c] < 0) continue;
+        cst[(size_t)c] = analyse_factor_class(P.classes[(size_t)c], kp ? &kp[rep[(size_t)c]] : nullptr,
+                                              F.classes[(size_t)c], cerr[(size_t)c]);
+      }
+    };
+    const int32_t nthr = std::min<int32_t>(ncls, (int32_t)std::max(1u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (int32_t k = 1; k < nthr; k++) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+    for (int32_t c = 0; c < ncls; c++)
+      if (cst[(size_t)c] != SC_OK) {
+        err = "subdomain " + std::to_string(rep[(size_t)c]) + ": " + cerr[(size_t)c];
+        return cst[(size_t)c];
+      }
   }
   // globalise
   F.panels.clear();

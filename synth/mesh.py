@@ -192,9 +192,11 @@ def regularize(K: sp.csr_matrix, fix: np.ndarray) -> sp.csr_matrix:
 # geometric nested dissection (SURVEY §8.3 reading 6)
 # ----------------------------------------------------------------------------------------------
 
-def nested_dissection_nodes(d: int, N: int) -> np.ndarray:
+def nested_dissection_nodes(d: int, N: int, rng: Optional[np.random.Generator] = None) -> np.ndarray:
     """new->old node order on an N^d lexicographic grid: split the longest axis at its middle plane,
-    order (left, right, separator); boxes with <= 2 nodes per axis stay in natural order."""
+    order (left, right, separator); boxes with <= 2 nodes per axis stay in natural order.  With `rng`
+    (perturbed patterns, one ordering per subdomain like a graph partitioner's): the split plane is
+    jittered by -1/0/+1 and ties between equally long axes are broken at random."""
     out: List[np.ndarray] = []
 
     def natural(lo, hi):
@@ -214,8 +216,13 @@ def nested_dissection_nodes(d: int, N: int) -> np.ndarray:
         if max(ext) <= 2:
             out.append(natural(lo, hi))
             return
-        ax = max(range(d), key=lambda k: (ext[k], k))
-        mid = lo[ax] + ext[ax] // 2
+        if rng is None:
+            ax = max(range(d), key=lambda k: (ext[k], k))
+            mid = lo[ax] + ext[ax] // 2
+        else:
+            longest = [k for k in range(d) if ext[k] == max(ext)]
+            ax = int(longest[rng.integers(len(longest))])
+            mid = lo[ax] + ext[ax] // 2 + (int(rng.integers(-1, 2)) if ext[ax] >= 5 else 0)
         lhi = list(hi)
         lhi[ax] = mid
         rlo = list(lo)
@@ -396,7 +403,7 @@ def _glue(d: int, S: int, E: int, dpn: int, redundant: bool, dirichlet: bool):
 
 def make_problem(dim: int, physics: str, S: int, E: int, *, seed: int = 0, coef: str = "subdomain",
                  redundant: bool = False, dirichlet: bool = True, subdomains: Optional[List[int]] = None,
-                 name: str = "") -> Problem:
+                 name: str = "", perturbed: bool = False) -> Problem:
     """Build a structured FETI problem (see module docstring).  `subdomains` restricts which
     subdomains get materialised (the gluing is always that of the full decomposition)."""
     assert physics in ("heat", "elasticity")
@@ -414,12 +421,14 @@ def make_problem(dim: int, physics: str, S: int, E: int, *, seed: int = 0, coef:
     n = N ** dim * dpn
 
     K_ref = L_ref = None
-    if coef == "subdomain":
+    if coef == "subdomain" and not perturbed:
         K_ref = regularize(assemble_subdomain(dim, E, physics, None, h), fix)
         C = K_ref[perm][:, perm]
         Lp, Li, Lx_ref = sparse_cholesky(C)
-    subs: List[Subdomain] = []
-    for i in ids:
+    if perturbed and K_ref is None:
+        K_ref = regularize(assemble_subdomain(dim, E, physics, None, h), fix)
+
+    def one(i):
         rng = np.random.default_rng([seed, i])
         kappa = float(rng.uniform(1.0, 10.0))
         a, b = starts[i], starts[i + 1]
@@ -428,9 +437,17 @@ def make_problem(dim: int, physics: str, S: int, E: int, *, seed: int = 0, coef:
         Bt_rowidx = l_all[a:b].astype(np.int32)
         Bt_values = v_all[a:b].astype(np.float64)
         lam = g_all[a:b].astype(np.int64)
-        if coef == "subdomain":
+        if coef == "subdomain" and not perturbed:
             sd = Subdomain(i, n, kappa, perm, Lp, Li, Bt_colptr, Bt_rowidx, Bt_values, lam,
                            _K_ref=K_ref, _L_ref_values=Lx_ref)
+        elif perturbed:
+            # a distinct fill-reducing ordering (hence L pattern) per subdomain, same K
+            no = nested_dissection_nodes(dim, N, np.random.default_rng([seed, i, 7]))
+            perm_i = (no[:, None] * dpn + np.arange(dpn)[None, :]).ravel().astype(np.int32)
+            K = (K_ref * kappa).tocsr()
+            Lp_i, Li_i, Lx_i = sparse_cholesky(K[perm_i][:, perm_i])
+            sd = Subdomain(i, n, 1.0, perm_i, Lp_i, Li_i, Bt_colptr, Bt_rowidx, Bt_values, lam,
+                           _K_own=K, _L_own=Lx_i)
         elif coef == "element":
             ec = rng.uniform(1.0, 10.0, size=E ** dim)
             K = regularize(assemble_subdomain(dim, E, physics, ec, h), fix)
@@ -440,7 +457,13 @@ def make_problem(dim: int, physics: str, S: int, E: int, *, seed: int = 0, coef:
                            _K_own=K, _L_own=Lx_i)
         else:
             raise ValueError(coef)
-        subs.append(sd)
+        return sd
+    if perturbed or coef == "element":  # one host factorization per subdomain: in parallel
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(max_workers=max(1, min(32, len(os.sched_getaffinity(0))))) as ex:
+            subs: List[Subdomain] = list(ex.map(one, ids))
+    else:
+        subs = [one(i) for i in ids]
     return Problem(name or f"{dim}d-{physics}-S{S}-E{E}", dim, physics, S, E, subs, n_lambda)
 
 

@@ -99,7 +99,7 @@ def _worker_apply_global(rank, world, port, out):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import oracle
     import bench
-    P, info = bench.setup_problem(argparse.Namespace(weak=False), "cfg1", world, rank)
+    P, info = bench.setup_problem(argparse.Namespace(weak=False, perturbed=False), "cfg1", world, rank)
     plan = SCPlan(P.subdomains, n_lambda=P.n_lambda, device=-1)
     lam = np.random.default_rng(9).standard_normal(P.n_lambda)
 
