@@ -51,8 +51,16 @@ constexpr int kFWarps = 4;              // warps per CTA (independent workers)
 #ifndef SC_FMINB
 #define SC_FMINB 4                      // CTAs per SM the factor kernel's registers are sized for
 #endif
+#ifndef SC_FSTAGE
+#define SC_FSTAGE 0                     // 1: an update's rows staged in shared memory by one cp.async round
+#endif
+#if SC_FSTAGE
+constexpr int kSLd = kFW + 2;           // 16-byte aligned rows (cp.async staging)
+constexpr int kFSmem = 2 * kFWarps * kFW * kSLd * 8;  // frame buffer S (= the rows operand while updating) + SB
+#else
 constexpr int kSLd = kFW + 1;           // per-warp frame buffer: 32 x 33 doubles (column 32: 1 / l_jj)
 constexpr int kFSmem = kFWarps * kFW * kSLd * 8;
+#endif
 
 __device__ __forceinline__ void fdmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -81,7 +89,12 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
   extern __shared__ double fsm[];
   __shared__ int frow_s[kFWarps][kFW], rmap_s[kFWarps][kFW], cmap_s[kFWarps][kFW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+#if SC_FSTAGE
+  double* S = fsm + warp * 2 * kFW * kSLd;
+  double* SB = S + kFW * kSLd;
+#else
   double* S = fsm + warp * kFW * kSLd;
+#endif
   int* frow = frow_s[warp];
   int* rmap = rmap_s[warp];
   int* cmap = cmap_s[warp];
@@ -176,6 +189,37 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
         for (int I = 0; I < 4; I++) ra[I] = I < nI && ((rm >> (8 * I)) & 0xFFu);
 #pragma unroll
         for (int J = 0; J < 4; J++) ca[J] = J < nJ && ((cm >> (8 * J)) & 0xFFu);
+#if SC_FSTAGE
+        {  // stage the active rows: (row, 16-byte chunk) pairs flattened over the lanes
+          const int nch = ukw8 >> 1;
+          for (int e = lane; e < 2 * kFW * nch; e += 32) {
+            const int side = e >= kFW * nch, q = side ? e - kFW * nch : e;
+            const int r = q / nch, ch = q - r * nch;
+            if (!(side ? ca[r >> 3] : ra[r >> 3])) continue;  // block not read by any DMMA
+            const int src = side ? cmap[r] : rmap[r];
+            double* dst = (side ? SB : S) + r * kSLd + 2 * ch;
+            cp_async16z(dst, W + uw + (int64_t)(src >= 0 ? src : 0) * ukw8 + 2 * ch, src >= 0 ? 16 : 0);
+          }
+          cp_async_commit_f();
+          cp_async_wait_all_f();
+          __syncwarp();
+        }
+        for (int kb = 0; kb < ukw; kb += 4) {
+          double a[4], b[4];
+#pragma unroll
+          for (int I = 0; I < 4; I++) a[I] = ra[I] ? S[(8 * I + g) * kSLd + kb + t] : 0.0;
+#pragma unroll
+          for (int J = 0; J < 4; J++) b[J] = ca[J] ? SB[(8 * J + g) * kSLd + kb + t] : 0.0;
+#pragma unroll
+          for (int I = 0; I < 4; I++)
+#pragma unroll
+            for (int J = 0; J < 4; J++)
+              if (ra[I] && ca[J] && (!diag || J <= I)) fdmma(acc[I][J][0], acc[I][J][1], a[I], b[J]);
+        }
+        __syncwarp();
+      }
+    }
+#else
         for (int kb = 0; kb < ukw; kb += 4) {  // kb + t < ukw8: the padding columns of a row are zeros
           double a[4], b[4];
 #pragma unroll
@@ -190,6 +234,8 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
         }
       }
     }
+
+#endif
 
     // ---- S = K entries - updates (frame layout, row-major in the warp's shared buffer); stage mode:
     // S = the frame's entries of the given L (zeros elsewhere)
@@ -636,10 +682,7 @@ void free_factor_device(Plan& P) {
   F.ptr_event = nullptr;
   if (F.d_Kstage) cudaFree(F.d_Kstage);
   F.d_Kstage = nullptr;
-  if (F.fstream) cudaStreamDestroy(static_cast<cudaStream_t>(F.fstream));
-  F.fstream = nullptr;
-  for (void* e : F.fev) cudaEventDestroy(static_cast<cudaEvent_t>(e));
-  F.fev.clear();
+
   F.d_ptrs = nullptr;
   F.ready = false;
 }
@@ -772,9 +815,10 @@ sc_status launch_implicit_solve(Plan& P, const double* lambda, void* stream_v, s
   return SC_OK;
 }
 
-// Host-fed pipeline: per chunk of subdomains, H2D of its K values on the copy stream, its
-// factorization (into the plan's L staging buffer) on the factorization stream, its assembly on
-// `stream`; chunk k's factorization overlaps chunk k-1's assembly and chunk k+1's copies.
+// Host-fed path: H2D of every subdomain's K values (per chunk of subdomains on the plan's copy stream),
+// then one factorization of the whole batch (level order over all subdomains: its critical path is
+// one panel chain, where per-chunk factorizations would serialise one chain per chunk) into the plan's
+// L staging buffer, then the assembly, both on `stream`.
 sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* stream_v, std::string& err) {
   cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
   FactorPlan& F = P.fac;
@@ -791,13 +835,6 @@ sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* strea
     FCUDA(cudaMalloc(&d, std::max<size_t>(8 * (size_t)F.Kstage_off.back(), 16)));
     F.d_Kstage = d;
   }
-  const int32_t nchunk = (int32_t)F.chunk_sub.size() - 1;
-  if (!F.fstream) FCUDA(cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&F.fstream), cudaStreamNonBlocking));
-  while ((int32_t)F.fev.size() < nchunk) {
-    cudaEvent_t e;
-    FCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    F.fev.push_back(e);
-  }
   std::vector<void*> Lst;
   FTRY(assemble_stage_begin(P, Lst, stream_v, err));  // L staging + pointer table + error reset
   std::vector<const void*> Kd((size_t)P.nsub);
@@ -806,44 +843,37 @@ sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* strea
   F.w_ready = true;
   FCUDA(cudaMemsetAsync(F.dev.flags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nflags, 1), stream));
   FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
-  cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream), fs = static_cast<cudaStream_t>(F.fstream);
-  // everything before this call on `stream` (previous users of the staging buffers, the resets above)
+  cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream);
+  // the K staging buffer is reused: the copies wait for everything enqueued on `stream` before this call
   FCUDA(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_start), stream));
   FCUDA(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(P.ev_start), 0));
-  FCUDA(cudaStreamWaitEvent(fs, static_cast<cudaEvent_t>(P.ev_start), 0));
-  while ((int32_t)P.ev_chunk.size() < nchunk) {
+  int32_t i = 0;
+  while (i < P.nsub) {  // one copy per run of host-contiguous subdomains
+    if (F.sub_nnzK[(size_t)i] == 0) {
+      i++;
+      continue;
+    }
+    const char* src = static_cast<const char*>(Khost[i]);
+    size_t bytes = 8 * (size_t)F.sub_nnzK[(size_t)i];
+    int32_t j = i + 1;
+    while (j < P.nsub && F.sub_nnzK[(size_t)j] > 0 && static_cast<const char*>(Khost[j]) == src + bytes) {
+      bytes += 8 * (size_t)F.sub_nnzK[(size_t)j];
+      j++;
+    }
+    FCUDA(cudaMemcpyAsync(static_cast<char*>(F.d_Kstage) + 8 * F.Kstage_off[(size_t)i], src, bytes,
+                          cudaMemcpyHostToDevice, cs));
+    i = j;
+  }
+  if (P.ev_chunk.empty()) {
     cudaEvent_t e;
     FCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     P.ev_chunk.push_back(e);
   }
-  for (int32_t k = 0; k < nchunk; k++) {
-    const int32_t s0 = F.chunk_sub[(size_t)k], s1 = F.chunk_sub[(size_t)k + 1];
-    int32_t i = s0;
-    while (i < s1) {  // one copy per run of host-contiguous subdomains
-      if (F.sub_nnzK[(size_t)i] == 0) {
-        i++;
-        continue;
-      }
-      const char* src = static_cast<const char*>(Khost[i]);
-      size_t bytes = 8 * (size_t)F.sub_nnzK[(size_t)i];
-      int32_t j = i + 1;
-      while (j < s1 && F.sub_nnzK[(size_t)j] > 0 && static_cast<const char*>(Khost[j]) == src + bytes) {
-        bytes += 8 * (size_t)F.sub_nnzK[(size_t)j];
-        j++;
-      }
-      FCUDA(cudaMemcpyAsync(static_cast<char*>(F.d_Kstage) + 8 * F.Kstage_off[(size_t)i], src, bytes,
-                            cudaMemcpyHostToDevice, cs));
-      i = j;
-    }
-    cudaEvent_t ec = static_cast<cudaEvent_t>(P.ev_chunk[(size_t)k]), ef = static_cast<cudaEvent_t>(F.fev[(size_t)k]);
-    FCUDA(cudaEventRecord(ec, cs));
-    FCUDA(cudaStreamWaitEvent(fs, ec, 0));
-    FTRY(factor_range(P, F.task_chunk[(size_t)k], F.task_chunk[(size_t)k + 1], 1 + k % (kQueueSlots - 1), fs, err));
-    FCUDA(cudaEventRecord(ef, fs));
-    FCUDA(cudaStreamWaitEvent(stream, ef, 0));
-    FTRY(assemble_range(P, s0, s1, stream_v, err));
-  }
-  return SC_OK;
+  cudaEvent_t ec = static_cast<cudaEvent_t>(P.ev_chunk[0]);
+  FCUDA(cudaEventRecord(ec, cs));
+  FCUDA(cudaStreamWaitEvent(stream, ec, 0));
+  FTRY(factor_range(P, 0, F.task_chunk[0], 0, stream, err));
+  return assemble_range(P, 0, P.nsub, stream_v, err);
 }
 
 }  // namespace sc

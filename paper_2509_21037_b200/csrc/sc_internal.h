@@ -306,8 +306,7 @@ struct FactorPlan {
   std::vector<int64_t> cls_bt0, sub_x_base;
   bool has_K = false;              // built with a K pattern (factorize), else staging from L only
   bool w_ready = false;            // W holds the factor (last factorize or stage)
-  std::vector<int64_t> task_chunk; // chunk c = tasks [task_chunk[c], task_chunk[c+1]) of subdomains
-  std::vector<int32_t> chunk_sub;  //   [chunk_sub[c], chunk_sub[c+1]) (host-fed pipeline granularity)
+  std::vector<int64_t> task_chunk; // {number of tasks of the whole-batch order}
   std::vector<int64_t> sub_W_base, sub_flag_base, sub_nnzK;
   std::vector<int32_t> cls_panel0;
   int64_t W_doubles = 0, nflags = 0;
@@ -318,8 +317,6 @@ struct FactorPlan {
   void** d_ptrs = nullptr;
   void* ptr_event = nullptr;
   void* d_Kstage = nullptr;        // host-fed path: K values staging
-  void* fstream = nullptr;         // host-fed path: factorization stream (overlaps the assembly)
-  std::vector<void*> fev;          // per chunk: factorization done
   std::vector<int64_t> Kstage_off;
 };
 
