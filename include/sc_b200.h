@@ -276,6 +276,11 @@ sc_status sc_check(sc_plan_t p);
    (F(a,b) at F[b*ld + a], column-major), into HOST memory.  Synchronises. */
 sc_status sc_get_F(sc_plan_t p, int32_t i, double* F, int64_t ld);
 
+/* Same as sc_get_F into DEVICE memory (F: m_i x m_i doubles, column-major, leading dimension ld, full
+   symmetric, original local multiplier order), enqueued on `stream` without synchronisation; device
+   errors of the assembly are reported by sc_check, not here. */
+sc_status sc_get_F_device(sc_plan_t p, int32_t i, double* F, int64_t ld, void* stream);
+
 /* Debug hook for the X-phase pins: X_i = L_i^{-1} P B~_i^T(:, sigma) as a dense n_i x m_i HOST
    matrix (column-major, ld = n_i; rows in the permuted order, columns in stepped order); entries
    outside the plan's strips are written as exact zeros.  Valid after sc_assemble_batch.  Also

@@ -210,6 +210,18 @@ sc_status sc_get_F(sc_plan_t p, int32_t i, double* F, int64_t ld) {
   return SC_OK;
 }
 
+sc_status sc_get_F_device(sc_plan_t p, int32_t i, double* F, int64_t ld, void* stream) {
+  if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
+  if (!p->P.on_device) return fail(SC_ERR_STATE, "host-only plan (device < 0)");
+  if (i < 0 || i >= p->P.nsub) return fail(SC_ERR_INVALID_ARG, "subdomain index out of range");
+  const int64_t m = p->P.sub_m[(size_t)i];
+  if (m == 0) return SC_OK;
+  if (!F || ld < m) return fail(SC_ERR_INVALID_ARG, "NULL F or ld < m");
+  std::string err;
+  sc_status st = sc::export_F_device(p->P, i, F, ld, stream, err);
+  return st == SC_OK ? SC_OK : fail(st, err);
+}
+
 sc_status sc_get_X(sc_plan_t p, int32_t i, double* X, int32_t* sigma) {
   if (!p) return fail(SC_ERR_INVALID_ARG, "NULL plan");
   if (i < 0 || i >= p->P.nsub) return fail(SC_ERR_INVALID_ARG, "subdomain index out of range");

@@ -51,16 +51,8 @@ constexpr int kFWarps = 4;              // warps per CTA (independent workers)
 #ifndef SC_FMINB
 #define SC_FMINB 4                      // CTAs per SM the factor kernel's registers are sized for
 #endif
-#ifndef SC_FSTAGE
-#define SC_FSTAGE 0                     // 1: an update's rows staged in shared memory by one cp.async round
-#endif
-#if SC_FSTAGE
-constexpr int kSLd = kFW + 2;           // 16-byte aligned rows (cp.async staging)
-constexpr int kFSmem = 2 * kFWarps * kFW * kSLd * 8;  // frame buffer S (= the rows operand while updating) + SB
-#else
 constexpr int kSLd = kFW + 1;           // per-warp frame buffer: 32 x 33 doubles (column 32: 1 / l_jj)
 constexpr int kFSmem = kFWarps * kFW * kSLd * 8;
-#endif
 
 __device__ __forceinline__ void fdmma(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -77,24 +69,13 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-// 16-byte global -> shared copy, zero-filled when src_bytes == 0 (L2 only: .cg)
-__device__ __forceinline__ void cp_async16z(void* dst, const void* src, int src_bytes) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit_f() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all_f() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFactor F, int64_t t0, int64_t t1, int slot,
                                                                  int stage) {
   extern __shared__ double fsm[];
   __shared__ int frow_s[kFWarps][kFW], rmap_s[kFWarps][kFW], cmap_s[kFWarps][kFW];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-#if SC_FSTAGE
-  double* S = fsm + warp * 2 * kFW * kSLd;
-  double* SB = S + kFW * kSLd;
-#else
   double* S = fsm + warp * kFW * kSLd;
-#endif
   int* frow = frow_s[warp];
   int* rmap = rmap_s[warp];
   int* cmap = cmap_s[warp];
@@ -189,37 +170,6 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
         for (int I = 0; I < 4; I++) ra[I] = I < nI && ((rm >> (8 * I)) & 0xFFu);
 #pragma unroll
         for (int J = 0; J < 4; J++) ca[J] = J < nJ && ((cm >> (8 * J)) & 0xFFu);
-#if SC_FSTAGE
-        {  // stage the active rows: (row, 16-byte chunk) pairs flattened over the lanes
-          const int nch = ukw8 >> 1;
-          for (int e = lane; e < 2 * kFW * nch; e += 32) {
-            const int side = e >= kFW * nch, q = side ? e - kFW * nch : e;
-            const int r = q / nch, ch = q - r * nch;
-            if (!(side ? ca[r >> 3] : ra[r >> 3])) continue;  // block not read by any DMMA
-            const int src = side ? cmap[r] : rmap[r];
-            double* dst = (side ? SB : S) + r * kSLd + 2 * ch;
-            cp_async16z(dst, W + uw + (int64_t)(src >= 0 ? src : 0) * ukw8 + 2 * ch, src >= 0 ? 16 : 0);
-          }
-          cp_async_commit_f();
-          cp_async_wait_all_f();
-          __syncwarp();
-        }
-        for (int kb = 0; kb < ukw; kb += 4) {
-          double a[4], b[4];
-#pragma unroll
-          for (int I = 0; I < 4; I++) a[I] = ra[I] ? S[(8 * I + g) * kSLd + kb + t] : 0.0;
-#pragma unroll
-          for (int J = 0; J < 4; J++) b[J] = ca[J] ? SB[(8 * J + g) * kSLd + kb + t] : 0.0;
-#pragma unroll
-          for (int I = 0; I < 4; I++)
-#pragma unroll
-            for (int J = 0; J < 4; J++)
-              if (ra[I] && ca[J] && (!diag || J <= I)) fdmma(acc[I][J][0], acc[I][J][1], a[I], b[J]);
-        }
-        __syncwarp();
-      }
-    }
-#else
         for (int kb = 0; kb < ukw; kb += 4) {  // kb + t < ukw8: the padding columns of a row are zeros
           double a[4], b[4];
 #pragma unroll
@@ -235,7 +185,6 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
       }
     }
 
-#endif
 
     // ---- S = K entries - updates (frame layout, row-major in the warp's shared buffer); stage mode:
     // S = the frame's entries of the given L (zeros elsewhere)
@@ -613,6 +562,31 @@ __global__ void __launch_bounds__(256) implicit_gather_kernel(DevPlan P, const d
   }
 }
 
+// ------------------------------------------------------------------------------------------------
+// Host -> device gather of many small pinned host arrays in one launch: the kernel reads mapped
+// (pinned, UVA) host memory over PCIe directly, one block per array, so a batch of a thousand
+// 160-KB K arrays costs one launch instead of a thousand cudaMemcpyAsync calls.
+// ------------------------------------------------------------------------------------------------
+template <typename E>
+__global__ void __launch_bounds__(256) gather_host_kernel(const E* const* __restrict__ src,
+                                                          const int64_t* __restrict__ off, E* __restrict__ dst,
+                                                          int s0, int s1) {
+  for (int sgi = s0 + blockIdx.x; sgi < s1; sgi += gridDim.x) {
+    const E* a = src[sgi];
+    const int64_t o = off[sgi], n = off[sgi + 1] - o;
+    E* d = dst + o;
+    constexpr int V = 16 / sizeof(E);  // elements per 16-byte vector
+    if ((((uintptr_t)a | (uintptr_t)d) & 15) == 0) {
+      const int64_t nv = n / V;
+      for (int64_t i = threadIdx.x; i < nv; i += blockDim.x)
+        reinterpret_cast<uint4*>(d)[i] = reinterpret_cast<const uint4*>(a)[i];
+      for (int64_t i = nv * V + threadIdx.x; i < n; i += blockDim.x) d[i] = a[i];
+    } else {
+      for (int64_t i = threadIdx.x; i < n; i += blockDim.x) d[i] = a[i];
+    }
+  }
+}
+
 template <typename V>
 sc_status fupload(FactorPlan& F, const std::vector<V>& v, const V** dst, std::string& err) {
   void* d = nullptr;
@@ -682,6 +656,14 @@ void free_factor_device(Plan& P) {
   F.ptr_event = nullptr;
   if (F.d_Kstage) cudaFree(F.d_Kstage);
   F.d_Kstage = nullptr;
+  if (F.d_hptrs) cudaFree(F.d_hptrs);
+  if (F.d_Kstage_off) cudaFree(F.d_Kstage_off);
+  if (F.h_hptrs) cudaFreeHost((void*)F.h_hptrs);
+  F.d_hptrs = nullptr;
+  F.d_Kstage_off = nullptr;
+  F.h_hptrs = nullptr;
+  if (F.hptr_event) cudaEventDestroy(static_cast<cudaEvent_t>(F.hptr_event));
+  F.hptr_event = nullptr;
 
   F.d_ptrs = nullptr;
   F.ready = false;
@@ -733,6 +715,22 @@ sc_status upload_factor_plan(Plan& P, std::string& err) {
   D.fp32 = P.esz == 4 ? 1 : 0;
   F.dev = D;
   F.ready = true;
+  return SC_OK;
+}
+
+// Mapped-host gather of arrays [s0, s1) (element size esz) into dst at the offsets `off` (device).
+sc_status gather_host_range(const void* const* d_src, const int64_t* d_off, void* d_dst, int32_t s0, int32_t s1,
+                            int esz, void* stream_v, std::string& err) {
+  if (s1 <= s0) return SC_OK;
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  const int grid = std::max(1, std::min(s1 - s0, 256));
+  if (esz == 8)
+    gather_host_kernel<double><<<grid, 256, 0, stream>>>(reinterpret_cast<const double* const*>(d_src), d_off,
+                                                          static_cast<double*>(d_dst), s0, s1);
+  else
+    gather_host_kernel<float><<<grid, 256, 0, stream>>>(reinterpret_cast<const float* const*>(d_src), d_off,
+                                                         static_cast<float*>(d_dst), s0, s1);
+  FCUDA(cudaGetLastError());
   return SC_OK;
 }
 
@@ -843,35 +841,75 @@ sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* strea
   F.w_ready = true;
   FCUDA(cudaMemsetAsync(F.dev.flags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nflags, 1), stream));
   FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
-  cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream);
-  // the K staging buffer is reused: the copies wait for everything enqueued on `stream` before this call
-  FCUDA(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_start), stream));
-  FCUDA(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(P.ev_start), 0));
-  int32_t i = 0;
-  while (i < P.nsub) {  // one copy per run of host-contiguous subdomains
-    if (F.sub_nnzK[(size_t)i] == 0) {
-      i++;
-      continue;
+  // pinned (device-mapped) host arrays: one gather kernel on `stream`; otherwise cudaMemcpyAsync per
+  // host-contiguous run on the copy stream
+  bool mapped = true;
+  std::vector<const void*> hdev((size_t)P.nsub, nullptr);
+  for (int32_t i = 0; i < P.nsub && mapped; i++) {
+    if (F.sub_nnzK[(size_t)i] == 0) continue;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, Khost[i]) != cudaSuccess || at.type != cudaMemoryTypeHost || !at.devicePointer) {
+      cudaGetLastError();
+      mapped = false;
+    } else {
+      hdev[(size_t)i] = at.devicePointer;
     }
-    const char* src = static_cast<const char*>(Khost[i]);
-    size_t bytes = 8 * (size_t)F.sub_nnzK[(size_t)i];
-    int32_t j = i + 1;
-    while (j < P.nsub && F.sub_nnzK[(size_t)j] > 0 && static_cast<const char*>(Khost[j]) == src + bytes) {
-      bytes += 8 * (size_t)F.sub_nnzK[(size_t)j];
-      j++;
+  }
+  if (mapped) {
+    if (!F.d_hptrs) {
+      void* d = nullptr;
+      FCUDA(cudaMalloc(&d, sizeof(void*) * (size_t)std::max(P.nsub, 1)));
+      F.d_hptrs = d;
+      int64_t* o = nullptr;
+      FCUDA(cudaMalloc(&o, sizeof(int64_t) * ((size_t)P.nsub + 1)));
+      FCUDA(cudaMemcpy(o, F.Kstage_off.data(), sizeof(int64_t) * ((size_t)P.nsub + 1), cudaMemcpyHostToDevice));
+      F.d_Kstage_off = o;
+      void* hp = nullptr;
+      FCUDA(cudaMallocHost(&hp, sizeof(void*) * (size_t)std::max(P.nsub, 1)));
+      F.h_hptrs = static_cast<const void**>(hp);
+      cudaEvent_t ev;
+      FCUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      FCUDA(cudaEventRecord(ev, stream));
+      F.hptr_event = ev;
     }
-    FCUDA(cudaMemcpyAsync(static_cast<char*>(F.d_Kstage) + 8 * F.Kstage_off[(size_t)i], src, bytes,
-                          cudaMemcpyHostToDevice, cs));
-    i = j;
+    FCUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(F.hptr_event)));  // the last upload consumed the pinned table
+    for (int32_t i = 0; i < P.nsub; i++) F.h_hptrs[i] = hdev[(size_t)i] ? hdev[(size_t)i] : Khost[0];
+    FCUDA(cudaMemcpyAsync(F.d_hptrs, F.h_hptrs, sizeof(void*) * (size_t)P.nsub, cudaMemcpyHostToDevice, stream));
+    FCUDA(cudaEventRecord(static_cast<cudaEvent_t>(F.hptr_event), stream));
+    gather_host_kernel<double><<<std::max(1, std::min(P.nsub, 1024)), 256, 0, stream>>>(
+        static_cast<const double* const*>(F.d_hptrs), F.d_Kstage_off, static_cast<double*>(F.d_Kstage), 0, P.nsub);
+    FCUDA(cudaGetLastError());
+  } else {
+    cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream);
+    // the K staging buffer is reused: the copies wait for everything enqueued on `stream` before this call
+    FCUDA(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_start), stream));
+    FCUDA(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(P.ev_start), 0));
+    int32_t i = 0;
+    while (i < P.nsub) {  // one copy per run of host-contiguous subdomains
+      if (F.sub_nnzK[(size_t)i] == 0) {
+        i++;
+        continue;
+      }
+      const char* src = static_cast<const char*>(Khost[i]);
+      size_t bytes = 8 * (size_t)F.sub_nnzK[(size_t)i];
+      int32_t j = i + 1;
+      while (j < P.nsub && F.sub_nnzK[(size_t)j] > 0 && static_cast<const char*>(Khost[j]) == src + bytes) {
+        bytes += 8 * (size_t)F.sub_nnzK[(size_t)j];
+        j++;
+      }
+      FCUDA(cudaMemcpyAsync(static_cast<char*>(F.d_Kstage) + 8 * F.Kstage_off[(size_t)i], src, bytes,
+                            cudaMemcpyHostToDevice, cs));
+      i = j;
+    }
+    if (P.ev_chunk.empty()) {
+      cudaEvent_t e;
+      FCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      P.ev_chunk.push_back(e);
+    }
+    cudaEvent_t ec = static_cast<cudaEvent_t>(P.ev_chunk[0]);
+    FCUDA(cudaEventRecord(ec, cs));
+    FCUDA(cudaStreamWaitEvent(stream, ec, 0));
   }
-  if (P.ev_chunk.empty()) {
-    cudaEvent_t e;
-    FCUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    P.ev_chunk.push_back(e);
-  }
-  cudaEvent_t ec = static_cast<cudaEvent_t>(P.ev_chunk[0]);
-  FCUDA(cudaEventRecord(ec, cs));
-  FCUDA(cudaStreamWaitEvent(stream, ec, 0));
   FTRY(factor_range(P, 0, F.task_chunk[0], 0, stream, err));
   return assemble_range(P, 0, P.nsub, stream_v, err);
 }

@@ -20,6 +20,7 @@
 #include <atomic>
 #include <thread>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -163,6 +164,16 @@ sc_status analyse_factor_class(const ClassPlan& C, const sc_K_pattern* Kp, Facto
         if (k < dn.nR) ip = (int32_t)(std::lower_bound(Rp + fend, Rp + pn.nR, Rd[k]) - Rp);
       }
     }
+  }
+  if (std::getenv("SC_DEBUG_FACTOR")) {
+    size_t nu = 0, rows = 0, maxu = 0;
+    for (auto& v : fl) {
+      nu += v.size();
+      maxu = std::max(maxu, v.size());
+      for (auto& u : v) rows += (size_t)(u.k1 - u.k0);
+    }
+    fprintf(stderr, "factor class: n %d panels %d frames %zu frame-updates %zu (max %zu per frame) update rows %zu levels %d\n",
+            n, np, F.frames.size(), nu, maxu, rows, F.max_level);
   }
   for (size_t f = 0; f < F.frames.size(); f++) {
     F.frames[f].u_begin = (int32_t)F.fupd.size();

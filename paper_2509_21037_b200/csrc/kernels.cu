@@ -1450,6 +1450,21 @@ __global__ void __launch_bounds__(kThreads) apply_scatter_kernel(DevPlan P, doub
 //   backward, descending:       z_p = inv(L_pp)^T (y_p - L[R_p,p]^T z[R_p])   (W mode:
 //                               z_p = inv(L_pp)^T y_p - W_p^T z[R_p])
 // ------------------------------------------------------------------------------------------------
+// sc_get_F_device: F(sigma(a), sigma(b)) = F'(max(a,b), min(a,b)) for one subdomain, full symmetric,
+// original multiplier order, column-major with leading dimension ld
+template <typename ST>
+__global__ void __launch_bounds__(256) export_F_kernel(DevPlan P, int sub, double* __restrict__ out, int64_t ld) {
+  const int m = P.sub_m[sub];
+  const int r = blockIdx.y * 16 + (threadIdx.x >> 4), c = blockIdx.x * 16 + (threadIdx.x & 15);
+  if (r >= m || c > r) return;
+  const ST* F = static_cast<const ST*>(P.F) + P.sub_F_base[sub];
+  const int32_t* sg = P.ssig + P.sub_slm_off[sub];
+  const double v = (double)F[f_index(r, c)];
+  const int64_t sr = sg[r], sc = sg[c];
+  out[sc * ld + sr] = v;
+  out[sr * ld + sc] = v;
+}
+
 __global__ void __launch_bounds__(kThreads) implicit_scatter_kernel(DevPlan P, double* __restrict__ q, int64_t nl) {
   const int64_t gidx = (int64_t)blockIdx.x * kThreads + threadIdx.x;
   if (gidx >= nl) return;
@@ -1731,6 +1746,14 @@ void free_plan_device(Plan& P) {
   P.copy_stream = P.ev_start = nullptr;
   if (P.d_Lstage) cudaFree(P.d_Lstage);
   P.d_Lstage = nullptr;
+  if (P.d_hsrc) cudaFree(P.d_hsrc);
+  if (P.d_Lstage_off) cudaFree(P.d_Lstage_off);
+  if (P.h_hsrc) cudaFreeHost((void*)P.h_hsrc);
+  if (P.ev_hsrc) cudaEventDestroy(static_cast<cudaEvent_t>(P.ev_hsrc));
+  P.d_hsrc = nullptr;
+  P.d_Lstage_off = nullptr;
+  P.h_hsrc = nullptr;
+  P.ev_hsrc = nullptr;
   P.on_device = false;
 }
 
@@ -1995,23 +2018,66 @@ sc_status assemble_host_pipelined(Plan& P, const void* const* Lhost, void* strea
   // the staging buffer is reused: copies wait for everything enqueued on `stream` before this call
   CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_start), stream));
   CUDA_TRY(cudaStreamWaitEvent(cs, static_cast<cudaEvent_t>(P.ev_start), 0));
+  // pinned (device-mapped) host arrays: one gather kernel per chunk on the copy stream (reads host
+  // memory over PCIe; no per-array copy calls); otherwise cudaMemcpyAsync per host-contiguous run
+  bool mapped = true;
+  std::vector<const void*> hdev((size_t)P.nsub, nullptr);
+  for (int32_t i = 0; i < P.nsub && mapped; i++) {
+    if (P.sub_nnz[(size_t)i] == 0) continue;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, Lhost[i]) != cudaSuccess || at.type != cudaMemoryTypeHost || !at.devicePointer) {
+      cudaGetLastError();
+      mapped = false;
+    } else {
+      hdev[(size_t)i] = at.devicePointer;
+    }
+  }
+  if (mapped) {
+    if (!P.d_hsrc) {
+      void* d = nullptr;
+      CUDA_TRY(cudaMalloc(&d, sizeof(void*) * (size_t)std::max(P.nsub, 1)));
+      P.d_hsrc = d;
+      int64_t* o = nullptr;
+      CUDA_TRY(cudaMalloc(&o, sizeof(int64_t) * ((size_t)P.nsub + 1)));
+      CUDA_TRY(cudaMemcpy(o, P.Lstage_off.data(), sizeof(int64_t) * ((size_t)P.nsub + 1), cudaMemcpyHostToDevice));
+      P.d_Lstage_off = o;
+      void* hp = nullptr;
+      CUDA_TRY(cudaMallocHost(&hp, sizeof(void*) * (size_t)std::max(P.nsub, 1)));
+      P.h_hsrc = static_cast<const void**>(hp);
+      cudaEvent_t ev;
+      CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(ev, cs));
+      P.ev_hsrc = ev;
+    }
+    CUDA_TRY(cudaEventSynchronize(static_cast<cudaEvent_t>(P.ev_hsrc)));
+    for (int32_t i = 0; i < P.nsub; i++) P.h_hsrc[i] = hdev[(size_t)i] ? hdev[(size_t)i] : Lhost[0];
+    CUDA_TRY(cudaMemcpyAsync(P.d_hsrc, P.h_hsrc, sizeof(void*) * (size_t)P.nsub, cudaMemcpyHostToDevice, cs));
+    CUDA_TRY(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_hsrc), cs));
+  }
   for (int32_t k = 0; k < nchunk; k++) {
     const int32_t s0 = (int32_t)((int64_t)P.nsub * k / nchunk), s1 = (int32_t)((int64_t)P.nsub * (k + 1) / nchunk);
-    // one cudaMemcpyAsync per run of host-contiguous subdomains (the staging side is contiguous)
-    int32_t i = s0;
-    while (i < s1) {
-      if (P.sub_nnz[(size_t)i] == 0) { i++; continue; }
-      const char* src = static_cast<const char*>(Lhost[i]);
-      size_t bytes = (size_t)P.esz * (size_t)P.sub_nnz[(size_t)i];
-      int32_t j = i + 1;
-      while (j < s1 && P.sub_nnz[(size_t)j] > 0 && static_cast<const char*>(Lhost[j]) == src + bytes &&
-             P.Lstage_off[(size_t)j] == P.Lstage_off[(size_t)i] + (int64_t)(bytes / P.esz)) {
-        bytes += (size_t)P.esz * (size_t)P.sub_nnz[(size_t)j];
-        j++;
+    if (mapped) {
+      st = gather_host_range(reinterpret_cast<const void* const*>(P.d_hsrc), P.d_Lstage_off, P.d_Lstage, s0, s1, P.esz,
+                             cs, err);
+      if (st != SC_OK) return st;
+    } else {
+      int32_t i = s0;
+      while (i < s1) {  // one cudaMemcpyAsync per run of host-contiguous subdomains
+        if (P.sub_nnz[(size_t)i] == 0) {
+          i++;
+          continue;
+        }
+        const char* src = static_cast<const char*>(Lhost[i]);
+        size_t bytes = (size_t)P.esz * (size_t)P.sub_nnz[(size_t)i];
+        int32_t j = i + 1;
+        while (j < s1 && P.sub_nnz[(size_t)j] > 0 && static_cast<const char*>(Lhost[j]) == src + bytes) {
+          bytes += (size_t)P.esz * (size_t)P.sub_nnz[(size_t)j];
+          j++;
+        }
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(P.d_Lstage) + P.esz * P.Lstage_off[(size_t)i], src, bytes,
+                                 cudaMemcpyHostToDevice, cs));
+        i = j;
       }
-      CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(P.d_Lstage) + P.esz * P.Lstage_off[(size_t)i], src, bytes,
-                               cudaMemcpyHostToDevice, cs));
-      i = j;
     }
     cudaEvent_t e = static_cast<cudaEvent_t>(P.ev_chunk[(size_t)k]);
     CUDA_TRY(cudaEventRecord(e, cs));
@@ -2114,6 +2180,19 @@ sc_status copy_F_lower(Plan& P, int32_t i, std::vector<double>& out, std::string
   const int64_t m = P.sub_m[(size_t)i], len = f_tiles((int)m) * kApplyTile * kApplyTile;
   out.resize((size_t)len);
   if (m > 0) TRY(copy_elements(P, P.dev.F, P.sub_F_base[(size_t)i], len, out.data(), err));
+  return SC_OK;
+}
+
+sc_status export_F_device(Plan& P, int32_t i, double* F, int64_t ld, void* stream_v, std::string& err) {
+  cudaStream_t stream = static_cast<cudaStream_t>(stream_v);
+  CUDA_TRY(cudaSetDevice(P.opt.device));
+  const int m = P.sub_m[(size_t)i];
+  if (m == 0) return SC_OK;
+  P.last_stream = stream_v;
+  const dim3 grid((unsigned)((m + 15) / 16), (unsigned)((m + 15) / 16));
+  if (P.esz == 4) export_F_kernel<float><<<grid, 256, 0, stream>>>(P.dev, i, F, ld);
+  else export_F_kernel<double><<<grid, 256, 0, stream>>>(P.dev, i, F, ld);
+  CUDA_TRY(cudaGetLastError());
   return SC_OK;
 }
 

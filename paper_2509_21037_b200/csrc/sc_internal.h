@@ -317,6 +317,10 @@ struct FactorPlan {
   void** d_ptrs = nullptr;
   void* ptr_event = nullptr;
   void* d_Kstage = nullptr;        // host-fed path: K values staging
+  void* d_hptrs = nullptr;         // host-fed path: device table of the mapped host K pointers
+  int64_t* d_Kstage_off = nullptr; //   and the staging offsets (gather_host_kernel)
+  const void** h_hptrs = nullptr;  //   pinned upload buffer of that table (guarded by hptr_event)
+  void* hptr_event = nullptr;
   std::vector<int64_t> Kstage_off;
 };
 
@@ -425,6 +429,10 @@ struct Plan {
   void* ov_stream[2] = {nullptr, nullptr};
   std::vector<void*> ev_ov;
   void* copy_stream = nullptr;   // host-fed pipeline (sc_assemble_batch_host): H2D copies
+  void* d_hsrc = nullptr;        // host-fed pipeline: device table of the mapped host L pointers
+  int64_t* d_Lstage_off = nullptr;
+  const void** h_hsrc = nullptr; //   its pinned upload buffer (guarded by ev_hsrc)
+  void* ev_hsrc = nullptr;
   void* ev_start = nullptr;
   std::vector<void*> ev_chunk;
   FactorPlan fac;                // device numeric factorization (sc_factor_attach)
@@ -450,6 +458,7 @@ sc_status launch_apply_implicit(Plan& P, const double* lambda, double* q, void* 
 sc_status device_check(Plan& P, std::string& err);
 sc_status copy_F_lower(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
 sc_status copy_X_strips(Plan& P, int32_t i, std::vector<double>& out, std::string& err);
+sc_status export_F_device(Plan& P, int32_t i, double* F, int64_t ld, void* stream, std::string& err);
 sc_status assemble_host_pipelined(Plan& P, const void* const* Lhost, void* stream, std::string& err);
 sc_status assemble_stage_begin(Plan& P, std::vector<void*>& dptrs, void* stream, std::string& err);
 sc_status assemble_range(Plan& P, int32_t s0, int32_t s1, void* stream, std::string& err);
@@ -463,6 +472,8 @@ sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* strea
 sc_status launch_stage(Plan& P, void* stream, std::string& err);
 sc_status launch_implicit_solve(Plan& P, const double* lambda, void* stream, std::string& err);
 sc_status ensure_factor_plan(Plan& P, std::string& err);  // K-less factor plan for the implicit apply
+sc_status gather_host_range(const void* const* d_src, const int64_t* d_off, void* d_dst, int32_t s0, int32_t s1,
+                            int esz, void* stream, std::string& err);
 
 // pcpg.cu
 sc_status pcpg_solve(Plan& P, const double* d, const double* e_host, double* lambda, const sc_coarse* cs,

@@ -96,7 +96,8 @@ EXPORTS = ["sc_pcpg", "sc_options_default", "sc_plan_create", "sc_assemble_batch
            "sc_check", "sc_get_F", "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_plan_subdomain_costs",
            "sc_set_timing_events", "sc_launches_per_assemble",
            "sc_launches_per_apply", "sc_plan_destroy", "sc_last_error", "sc_prepare_factor", "sc_apply_implicit",
-           "sc_launches_per_apply_implicit", "sc_factor_attach", "sc_factorize_batch", "sc_factorize_assemble_host"]
+           "sc_launches_per_apply_implicit", "sc_factor_attach", "sc_factorize_batch", "sc_factorize_assemble_host",
+           "sc_get_F_device"]
 
 
 def lib():
@@ -120,6 +121,7 @@ def lib():
     L.sc_launches_per_apply_implicit.restype = ctypes.c_int32
     L.sc_get_F.argtypes = [_P, ctypes.c_int32, _P, ctypes.c_int64]
     L.sc_get_X.argtypes = [_P, ctypes.c_int32, _P, _P]
+    L.sc_get_F_device.argtypes = [_P, ctypes.c_int32, _P, ctypes.c_int64, _P]
     L.sc_plan_strip_rows.argtypes = [_P, ctypes.c_int32, ctypes.c_int32, _P, _P]
     L.sc_plan_stats.argtypes = [_P, ctypes.POINTER(Stats)]
     L.sc_set_timing_events.argtypes = [_P, _P, ctypes.c_int32]
@@ -140,7 +142,7 @@ def lib():
     L.sc_last_error.restype = ctypes.c_char_p
     for f in ("sc_plan_create", "sc_assemble_batch", "sc_assemble_batch_host", "sc_apply", "sc_check", "sc_get_F",
               "sc_prepare_factor", "sc_apply_implicit", "sc_factor_attach", "sc_factorize_batch",
-              "sc_factorize_assemble_host",
+              "sc_factorize_assemble_host", "sc_get_F_device",
               "sc_get_X", "sc_plan_strip_rows", "sc_plan_stats", "sc_set_timing_events", "sc_plan_subdomain_costs"):
         getattr(L, f).restype = ctypes.c_int
     _lib = L
@@ -333,6 +335,16 @@ class SCPlan:
         F = np.zeros((m, m), dtype=np.float64, order="F")
         _check(lib().sc_get_F(self._h, i, F.ctypes.data, m))
         return np.asfortranarray(F)
+
+    def get_F_device(self, i: int, out=None, stream=None):
+        """F_i (full symmetric, original multiplier order) into a CUDA float64 tensor (m x m, column-major:
+        out[b, a] = F(a, b), i.e. the transpose view of a row-major tensor; F is symmetric anyway)."""
+        import torch
+        m = self.m[i]
+        if out is None:
+            out = torch.empty((m, m), dtype=torch.float64, device=f"cuda:{self.device}")
+        _check(lib().sc_get_F_device(self._h, i, out.data_ptr(), m, _stream_handle(stream)))
+        return out
 
     def get_X(self, i: int):
         n, m = self.n[i], self.m[i]
