@@ -24,6 +24,12 @@
 //                         with the staged factor panels, no F.
 #include <cuda_runtime.h>
 
+// X init of the global-strip TRSM paths: zero only the rows of the tile's own reach (1) or every
+// group-strip row (0)
+#ifndef SC_CTA_ZERO_REACH
+#define SC_CTA_ZERO_REACH 0  // 1 measured slower for 3D (one panel per thread: cfg3 TRSM 13.9 vs 12.8 ms)
+#endif
+
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -710,11 +716,23 @@ __global__ void __launch_bounds__(TileCfg<T, MINB>::CT + 32, MINB) trsm_smem_ker
   // ---- consumers.  X init (row a2): zero the strip (+4 pad rows), scatter B~^T
   const int g = lane >> 2, t4 = lane & 3;
   const int br0 = (warp / NWC) * WM, bc0 = (warp % NWC) * WN;
-  if constexpr (GS) {  // the tile's T columns of every group-strip row
-    for (int q = tid; q < tile.strip_rows * (T / 2); q += CT) {
+  if constexpr (GS) {
+#if SC_CTA_ZERO_REACH
+    // the tile's T columns of the group-strip rows of its own reach (one step's panel per thread);
+    // the group's other rows are never written in these columns and stay zero from the allocation
+    for (int s = tile.step_begin + tid; s < tile.step_end; s += CT) {
+      const Step st = P.steps[s];
+      const int nr = P.panels[st.panel].kw;
+      for (int r = 0; r < nr; r++)
+#pragma unroll
+        for (int j = 0; j < T; j += 2) xst2((st.strip_row + r) * LDX + j, make_double2(0.0, 0.0));
+    }
+#else
+    for (int q = tid; q < tile.strip_rows * (T / 2); q += CT) {  // the tile's T columns of every group-strip row
       const int r = q / (T / 2), j = 2 * (q - r * (T / 2));
       xst2(r * LDX + j, make_double2(0.0, 0.0));
     }
+#endif
   } else {
     double2* X2 = reinterpret_cast<double2*>(Xs);
     const int nvec = (tile.strip_rows + 4) * LDX / 2;
@@ -994,6 +1012,9 @@ __device__ __forceinline__ double gather_l(const ST* __restrict__ Lv, int32_t q)
   return q >= 0 ? (double)__ldg(Lv + q) : 0.0;
 }
 
+#ifndef SC_WARP_ZERO_REACH
+#define SC_WARP_ZERO_REACH 1
+#endif
 #ifndef SC_WARP_MINB
 #define SC_WARP_MINB 3  // 3 CTAs (12 warps) per SM: no spills at 168 registers (measured: cfg2 TRSM 1.15 vs 1.24 ms at 4, 1.54 at 5)
 #endif
@@ -1117,8 +1138,26 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
     warp_tri_idx(P.gidx + pn_n.gx_off, k8 * (k8 + 1) / 2, lane, qt);
     warp_tri_gather(Lv, qt, k8 * (k8 + 1) / 2, Ts, lane);
   }
-  // X init (row a2): zero the tile's columns of every group-strip row, scatter B~^T
+  // X init (row a2): zero the tile's columns of the group-strip rows of its own reach (the panels it
+  // visits; the group's other rows are never written in these columns and stay zero from the
+  // allocation), scatter B~^T
+#if SC_WARP_ZERO_REACH
+  for (int s0 = tile.step_begin; s0 < tile.step_end; s0 += 32) {
+    int r0 = 0, nr = 0;
+    if (s0 + lane < tile.step_end) {
+      const Step st = P.steps[s0 + lane];
+      r0 = st.strip_row;
+      nr = P.panels[st.panel].kw;
+    }
+    const int ns = min(32, tile.step_end - s0);
+    for (int j = 0; j < ns; j++) {
+      const int rj = __shfl_sync(0xffffffffu, r0, j), nj = __shfl_sync(0xffffffffu, nr, j);
+      for (int r = vr0; r < nj; r += RPI) st2(Xs + (int64_t)(rj + r) * G + vc2, make_double2(0.0, 0.0));
+    }
+  }
+#else
   for (int r = vr0; r < tile.strip_rows; r += RPI) st2(Xs + (int64_t)r * G + vc2, make_double2(0.0, 0.0));
+#endif
   __syncwarp();
   for (int q = tile.binit_begin + lane; q < tile.binit_end; q += 32) {
     const BInit bi = P.binit[q];
@@ -1225,13 +1264,20 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
 #endif
 constexpr int kKC = SC_SYRK_KC;  // k rows staged per chunk
 
+#ifndef SC_SYRK_KSPLIT
+#define SC_SYRK_KSPLIT 0  // 1: k-split G = 32 SYRK (measured 2x slower on cfg2: short k ranges, reduction cost)
+#endif
 template <int G>
 struct SyrkCfg {              // (G/8)^2 output blocks of 8x8 over 8 warps
+  // G = 32 (2D): every warp holds all 4 x 4 output blocks and takes every 8th k step of a chunk
+  // (16 DMMAs per 8 fragment loads instead of 2 per 3), partial tiles summed over the warps in a
+  // fixed tree order at the end
+  static constexpr bool KSPLIT = (G == 32) && SC_SYRK_KSPLIT;
   static constexpr int NB = G / 8;
-  static constexpr int WN = (G == 64) ? 4 : (G == 32 ? 2 : 1);
-  static constexpr int WM = (G == 64) ? 2 : 1;
+  static constexpr int WN = KSPLIT ? NB : (G == 64) ? 4 : (G == 32 ? 2 : 1);
+  static constexpr int WM = KSPLIT ? NB : (G == 64) ? 2 : 1;
   static constexpr int NWC = NB / WN;
-  static constexpr int ACTIVE = (NB / WM) * NWC;   // warps with work (4 for G = 16)
+  static constexpr int ACTIVE = KSPLIT ? 8 : (NB / WM) * NWC;   // warps with work (4 for G = 16)
 };
 
 // smem row stride (elements) of a staged X chunk: conflict-free fragment loads for 8- and 4-byte
@@ -1242,7 +1288,11 @@ __host__ __device__ constexpr int syrk_ld() {
 }
 template <int G, typename ST = double>
 __host__ __device__ constexpr size_t syrk_smem_bytes() {
-  return sizeof(ST) * 4 * kKC * syrk_ld<G, ST>();  // 2 stages x (X_I chunk, X_J chunk)
+  // 2 stages x (X_I chunk, X_J chunk); the k-split G = 32 kernel reuses it for its warp reduction
+  // (4 partial 32 x 32 tiles of doubles)
+  return (G == 32 && SC_SYRK_KSPLIT && sizeof(ST) * 4 * kKC * syrk_ld<G, ST>() < 4 * 16 * 64 * sizeof(double))
+             ? 4 * 16 * 64 * sizeof(double)
+             : sizeof(ST) * 4 * kKC * syrk_ld<G, ST>();
 }
 
 template <int G, typename ST>
@@ -1260,7 +1310,8 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
   const Group gI = P.groups[pr.I], gJ = P.groups[pr.J];
   const ST* __restrict__ XI = static_cast<const ST*>(P.X) + P.sub_X_base[sub] + gI.x_off;
   const ST* __restrict__ XJ = static_cast<const ST*>(P.X) + P.sub_X_base[sub] + gJ.x_off;
-  const int br0 = (warp / NWC) * WM, bc0 = (warp % NWC) * WN;
+  constexpr bool KSPLIT = SyrkCfg<G>::KSPLIT;
+  const int br0 = KSPLIT ? 0 : (warp / NWC) * WM, bc0 = KSPLIT ? 0 : (warp % NWC) * WN;
   double acc[WM][WN][2];
 #pragma unroll
   for (int i = 0; i < WM; i++)
@@ -1320,7 +1371,9 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
 #pragma unroll
           for (int j = 0; j < WN; j++) dmma(acc[i][j][0], acc[i][j][1], a[i], b[j]);
       };
-      if (kn4 == kKC) {  // full chunk: fixed trip count, fully unrolled
+      if constexpr (KSPLIT) {  // this warp's k steps of the chunk
+        for (int k = 4 * warp; k < kn4; k += 4 * (kThreads / 32)) kstep(k);
+      } else if (kn4 == kKC) {  // full chunk: fixed trip count, fully unrolled
 #pragma unroll
         for (int k = 0; k < kKC; k += 4) kstep(k);
       } else {
@@ -1330,6 +1383,34 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
     __syncthreads();
   }
   cp_async_wait<0>();
+  if constexpr (KSPLIT) {  // sum the warps' partial tiles: 8 -> 4 -> 2 -> 1, fixed order
+    double* R = reinterpret_cast<double*>(syrk_smem);  // >= 4 x (WM x WN x 64) doubles (the stage buffers)
+    static_assert(4 * WM * WN * 64 * sizeof(double) <= syrk_smem_bytes<G, ST>(), "reduction buffer");
+#pragma unroll
+    for (int half = 4; half >= 1; half >>= 1) {
+      if (warp >= half && warp < 2 * half) {
+#pragma unroll
+        for (int i = 0; i < WM; i++)
+#pragma unroll
+          for (int j = 0; j < WN; j++) {
+            R[(((warp - half) * WM + i) * WN + j) * 64 + 2 * lane] = acc[i][j][0];
+            R[(((warp - half) * WM + i) * WN + j) * 64 + 2 * lane + 1] = acc[i][j][1];
+          }
+      }
+      __syncthreads();
+      if (warp < half) {
+#pragma unroll
+        for (int i = 0; i < WM; i++)
+#pragma unroll
+          for (int j = 0; j < WN; j++) {
+            acc[i][j][0] += R[((warp * WM + i) * WN + j) * 64 + 2 * lane];
+            acc[i][j][1] += R[((warp * WM + i) * WN + j) * 64 + 2 * lane + 1];
+          }
+      }
+      __syncthreads();
+    }
+    if (warp != 0) return;
+  }
   if (!active) return;
   ST* __restrict__ F = static_cast<ST*>(P.F) + P.sub_F_base[sub];
   const bool diag = (pr.I == pr.J);

@@ -1,5 +1,6 @@
 #!/bin/bash
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_factor.py tests/test_gpu_parity.py -q -x -k "factor or host or cfg2_class" > gpurun_out/t_host.log 2>&1; echo "rc=$?" >> gpurun_out/t_host.log
-timeout 900 python bench.py --cpu-budget 2 --per-config "" > gpurun_out/bench_cfg2.json 2> gpurun_out/bench_cfg2.err
+timeout 1800 python -m pytest tests -m gpu -q -x -k "global or cfg5 or full_size or classes or perturbed or warp" > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+rm -f gpurun_out/variants.txt
+VARIANTS="zall:" CFGS="cfg2 cfg3 cfg4" STEPS=5 bash tools/variants.sh
