@@ -228,9 +228,13 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
       __syncwarp();
     }
     if (diag) {
-      // ---- Cholesky of the diagonal block (right-looking, lane = row)
+      // ---- Cholesky of the diagonal block, left-looking by columns (lane = row): column j needs the
+      // finished columns k < j only, so every lane runs the same k loop (no divergence) and one
+      // __syncwarp per column suffices
       for (int j = 0; j < (stage ? 0 : kw); j++) {
-        double djj = S[j * kSLd + j];
+        double v = S[lane * kSLd + j];
+        for (int k = 0; k < j; k++) v = fma(-S[lane * kSLd + k], S[j * kSLd + k], v);
+        double djj = __shfl_sync(~0u, v, j);
         if (!(djj > 0.0) || !isfinite(djj)) {
           if (lane == 0) {
             atomicCAS(F.err, 0ull, ((unsigned long long)(sub + 1) << 32) | (unsigned long long)(pn.a + j));
@@ -239,17 +243,11 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
           djj = 1.0;
         }
         const double l = sqrt(djj), rl = 1.0 / l;
-        __syncwarp();
         if (lane == j) {
           S[j * kSLd + j] = l;
           S[j * kSLd + kFW] = rl;
         }
-        if (lane > j && lane < kw) S[lane * kSLd + j] *= rl;
-        __syncwarp();
-        if (lane > j && lane < kw) {
-          const double lij = S[lane * kSLd + j];
-          for (int c = j + 1; c <= lane; c++) S[lane * kSLd + c] -= lij * S[c * kSLd + j];
-        }
+        if (lane > j && lane < kw) S[lane * kSLd + j] = v * rl;
         __syncwarp();
       }
       // ---- inverse of the triangle: lane c computes column c (forward substitution, registers)
@@ -696,6 +694,7 @@ sc_status upload_factor_plan(Plan& P, std::string& err) {
   D.slm = P.dev.slm;
   D.sub_slm_off = P.dev.sub_slm_off;
   FTRY(falloc(F, F.W_doubles, &D.W, err));
+
   FTRY(falloc(F, F.nflags, &D.flags, err));
   FTRY(falloc(F, kQueueSlots, &D.queue, err));
   void** dp = nullptr;

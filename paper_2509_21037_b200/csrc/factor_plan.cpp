@@ -393,28 +393,67 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
   // serialise one chain per chunk: measured 2.6x slower for cfg2 with 16 chunks).
   const char* me = std::getenv("SC_FACTOR_MERGE");
   const int32_t merge = me ? std::atoi(me) : 6;  // panels with <= this many frames form one task
+  const char* mst = std::getenv("SC_FACTOR_SUBTREE");
+  const int32_t subtree = mst ? std::atoi(mst) : 24;  // self-contained panel ranges of <= this many frames
+  // Per class: self-contained panel ranges [lo, hi] (every update of a panel in the range comes from
+  // the range: a whole subtree when the ordering is a postorder, as nested dissection's is) of at
+  // most `subtree` frames become ONE task -- its frames in panel order, processed by one warp with no
+  // waits -- at level 0; the other panels are tasks of their own level.
+  std::vector<std::vector<std::pair<int32_t, int32_t>>> cls_units((size_t)ncls);  // (first local panel, last)
+  for (int32_t c = 0; c < ncls; c++) {
+    const FactorClass& fc = F.classes[(size_t)c];
+    const int32_t np = (int32_t)fc.panels.size();
+    std::vector<int32_t> lo((size_t)np);
+    for (int32_t p = 0; p < np; p++) {  // lowest panel of p's dependency closure
+      int32_t l = p;
+      for (int32_t u = fc.panels[(size_t)p].upd_begin; u < fc.panels[(size_t)p].upd_end; u++)
+        l = std::min(l, lo[(size_t)fc.upd[(size_t)u].d]);
+      lo[(size_t)p] = l;
+    }
+    auto& units = cls_units[(size_t)c];
+    int32_t p = np - 1;
+    while (p >= 0) {
+      const int32_t l = lo[(size_t)p];
+      int32_t frames = 0, minlo = l;
+      for (int32_t q = l; q <= p; q++) {
+        frames += fc.panels[(size_t)q].nframe;
+        minlo = std::min(minlo, lo[(size_t)q]);
+      }
+      if (l < p && minlo >= l && frames <= subtree) {
+        units.push_back({l, p});
+        p = l - 1;
+      } else {
+        units.push_back({p, p});
+        p--;
+      }
+    }
+  }
   auto order = [&](int32_t s0, int32_t s1) {
     int32_t maxlev = 0;
     for (int32_t i = s0; i < s1; i++) maxlev = std::max(maxlev, F.classes[(size_t)P.sub_cls[(size_t)i]].max_level);
     std::vector<std::vector<FTask>> bylev((size_t)maxlev + 1);
+    std::vector<std::vector<I2>> pbylev((size_t)maxlev + 1);
     for (int32_t i = s0; i < s1; i++) {
-      const int32_t c = P.sub_cls[(size_t)i];
-      for (int32_t p = F.cls_panel0[(size_t)c]; p < F.cls_panel0[(size_t)c + 1]; p++) {
-        const FPanel& pn = F.panels[(size_t)p];
-        if (pn.nframe <= merge) {  // small panel: one warp does the diagonal and then its rows (no waits)
-          bylev[(size_t)pn.level].push_back(FTask{i, pn.frame_begin, pn.nframe, 0});
+      const int32_t c = P.sub_cls[(size_t)i], p0 = F.cls_panel0[(size_t)c];
+      for (const auto& un : cls_units[(size_t)c]) {
+        const FPanel& pa = F.panels[(size_t)(p0 + un.first)];
+        if (un.first < un.second) {  // subtree unit: all its frames, panel order, level 0
+          const FPanel& pb = F.panels[(size_t)(p0 + un.second)];
+          bylev[0].push_back(FTask{i, pa.frame_begin, pb.frame_begin + pb.nframe - pa.frame_begin, 0});
+        } else if (pa.nframe <= merge) {  // small panel: one warp does the diagonal and then its rows
+          bylev[(size_t)pa.level].push_back(FTask{i, pa.frame_begin, pa.nframe, 0});
         } else {
-          for (int32_t f = 0; f < pn.nframe; f++) bylev[(size_t)pn.level].push_back(FTask{i, pn.frame_begin + f, 1, 0});
+          for (int32_t f = 0; f < pa.nframe; f++) bylev[(size_t)pa.level].push_back(FTask{i, pa.frame_begin + f, 1, 0});
         }
       }
+      for (int32_t p = p0; p < F.cls_panel0[(size_t)c + 1]; p++) pbylev[(size_t)F.panels[(size_t)p].level].push_back(I2{i, p});
     }
     for (auto& v : bylev) F.tasks.insert(F.tasks.end(), v.begin(), v.end());
+    for (auto& v : pbylev) F.ptasks.insert(F.ptasks.end(), v.begin(), v.end());
   };
   F.tasks.clear();
+  F.ptasks.clear();  // implicit apply: one task per (subdomain, panel) in level order
   order(0, nsub);
-  F.ptasks.clear();  // implicit apply: one task per (subdomain, panel), the diagonal frames in this order
-  for (const FTask& t : F.tasks)
-    if (F.frames[(size_t)t.frame].r0 < 0) F.ptasks.push_back(I2{t.sub, F.frames[(size_t)t.frame].panel});
   F.task_chunk.assign(1, (int64_t)F.tasks.size());  // end of the whole-batch order
   if (F.tasks.size() > (size_t)INT32_MAX) FFAIL(SC_ERR_INVALID_ARG, "too many factorization tasks");
   return SC_OK;
