@@ -298,7 +298,7 @@ def roofline_for(st, phases, ms_step, peaks, cfg):
     warp = st.get("trsm_kernel") == 2
     kernel_names = {"prep": "prep_panel_kernel + prep_small_kernel",
                     "trsm": (f"trsm_warp_kernel<{st['tile_cols'] // 8}>" if warp else f"trsm_smem_kernel<{st['tile_cols']}>"),
-                    "syrk": f"syrk_pair_kernel<{st['group_cols']}>"}
+                    "syrk": ("syrk_warp16_kernel" if st["group_cols"] == 16 else f"syrk_pair_kernel<{st['group_cols']}>")}
     alg = {"prep": (0.0, st["bytes_L_values"]),
            "trsm": (st["flops_trsm_useful"], st["bytes_L_values"] + st["bytes_X_reach"]),
            "syrk": (st["flops_syrk_useful"], st["bytes_X"] + st["bytes_F_lower"])}

@@ -224,10 +224,12 @@ sc_status sc_factor_attach(sc_plan_t p, const sc_K_pattern* K, int32_t nsub);
    SC_ERR_STATE without sc_factor_attach. */
 sc_status sc_factorize_batch(sc_plan_t p, const void* const* K_values, void* const* L_values, void* stream);
 
-/* Host-fed end-to-end preprocessing: K values in HOST memory (ideally pinned) -> H2D copy of K (about
-   nnz(K lower) / nnz(L) of the bytes sc_assemble_batch_host moves; on a plan-owned copy stream) ->
-   one device factorization of the whole batch into a plan-owned L buffer -> assembly of every F_i,
-   both on `stream`.  The host arrays must stay valid until `stream` completes.  Does not
+/* Host-fed end-to-end preprocessing: K values in HOST memory -> device factorization of the whole batch
+   into a plan-owned L buffer -> assembly of every F_i, on `stream`.  Pinned (device-mapped) host
+   arrays are read by the factorization kernel itself over PCIe (each frame's K entries copied
+   asynchronously while its updates run; about nnz(K lower) / nnz(L) of the bytes
+   sc_assemble_batch_host moves); pageable arrays are first copied to a plan-owned staging buffer on
+   a plan-owned copy stream.  The host arrays must stay valid until `stream` completes.  Does not
    synchronise. */
 sc_status sc_factorize_assemble_host(sc_plan_t p, const void* const* K_values_host, void* stream);
 
