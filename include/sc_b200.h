@@ -224,13 +224,13 @@ sc_status sc_factor_attach(sc_plan_t p, const sc_K_pattern* K, int32_t nsub);
    SC_ERR_STATE without sc_factor_attach. */
 sc_status sc_factorize_batch(sc_plan_t p, const void* const* K_values, void* const* L_values, void* stream);
 
-/* Host-fed end-to-end preprocessing: K values in HOST memory -> device factorization of the whole batch
-   into a plan-owned L buffer -> assembly of every F_i, on `stream`.  Pinned (device-mapped) host
-   arrays are read by the factorization kernel itself over PCIe (each frame's K entries copied
-   asynchronously while its updates run; about nnz(K lower) / nnz(L) of the bytes
-   sc_assemble_batch_host moves); pageable arrays are first copied to a plan-owned staging buffer on
-   a plan-owned copy stream.  The host arrays must stay valid until `stream` completes.  Does not
-   synchronise. */
+/* Host-fed end-to-end preprocessing: K values in HOST memory -> device staging (pinned, device-mapped
+   arrays: one gather kernel reading host memory over PCIe; pageable arrays: cudaMemcpyAsync per
+   host-contiguous run on a plan-owned copy stream; about nnz(K lower) / nnz(L) of the bytes
+   sc_assemble_batch_host moves) -> one device factorization of the whole batch into a plan-owned L
+   buffer -> assembly of every F_i, both on `stream`.  (Reading K straight from host memory inside
+   the factorization measured slower: scattered small PCIe reads.)  The host arrays must stay valid
+   until `stream` completes.  Does not synchronise. */
 sc_status sc_factorize_assemble_host(sc_plan_t p, const void* const* K_values_host, void* stream);
 
 /* ---- Solution stage: PCPG on the FETI dual problem -------------------------------

@@ -69,13 +69,7 @@ __device__ __forceinline__ int ld_relaxed(const int* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-// 8-byte global -> shared asynchronous copy (the source may be mapped pinned host memory)
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit_f() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void cp_async_wait_all_f() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
 
 __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFactor F, int64_t t0, int64_t t1, int slot,
                                                                  int stage) {
@@ -102,17 +96,6 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
     const int kw = pn.kw, nI = (fr.nrow + 7) >> 3, nJ = pn.kw8 >> 3;
     // the frame's row values (ascending), for the row lookups of the descendants' rows
     frow[lane] = lane < fr.nrow ? (diag ? pn.a + lane : __ldg(F.Rrows + pn.R_off + fr.r0 + lane)) : INT32_MAX;
-    if (!stage) {  // S = the frame's K entries (zeros elsewhere): asynchronous copies that travel while the
-                   // updates run (K may be pinned host memory read over PCIe: sc_factorize_assemble_host)
-      for (int e = lane; e < kFW * kSLd; e += 32) S[e] = 0.0;
-      __syncwarp();
-      const double* Kv = static_cast<const double*>(F.Kptr[sub]);
-      for (int e = fr.k_begin + lane; e < fr.k_end; e += 32) {
-        const FEnt en = F.kent[e];
-        cp_async8(S + (en.pos >> 5) * kSLd + (en.pos & 31), Kv + en.q);
-      }
-      cp_async_commit_f();
-    }
     double acc[4][4][2];
 #pragma unroll
     for (int I = 0; I < 4; I++)
@@ -217,16 +200,20 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
                    : __ldg(static_cast<const double*>(F.Lin[sub]) + en.q);
       }
     } else {
-      cp_async_wait_all_f();  // the K entries
-      __syncwarp();
 #pragma unroll
       for (int I = 0; I < 4; I++)
 #pragma unroll
         for (int J = 0; J < 4; J++)
           if (I < nI && J < nJ) {
-            S[(8 * I + g) * kSLd + 8 * J + 2 * t] -= acc[I][J][0];
-            S[(8 * I + g) * kSLd + 8 * J + 2 * t + 1] -= acc[I][J][1];
+            S[(8 * I + g) * kSLd + 8 * J + 2 * t] = -acc[I][J][0];
+            S[(8 * I + g) * kSLd + 8 * J + 2 * t + 1] = -acc[I][J][1];
           }
+      __syncwarp();
+      const double* Kv = static_cast<const double*>(F.Kptr[sub]);
+      for (int e = fr.k_begin + lane; e < fr.k_end; e += 32) {
+        const FEnt en = F.kent[e];
+        S[(en.pos >> 5) * kSLd + (en.pos & 31)] += __ldg(Kv + en.q);
+      }
     }
     __syncwarp();
 
@@ -668,6 +655,14 @@ void free_factor_device(Plan& P) {
   F.ptr_event = nullptr;
   if (F.d_Kstage) cudaFree(F.d_Kstage);
   F.d_Kstage = nullptr;
+  if (F.d_hptrs) cudaFree(F.d_hptrs);
+  if (F.d_Kstage_off) cudaFree(F.d_Kstage_off);
+  if (F.h_hptrs) cudaFreeHost((void*)F.h_hptrs);
+  F.d_hptrs = nullptr;
+  F.d_Kstage_off = nullptr;
+  F.h_hptrs = nullptr;
+  if (F.hptr_event) cudaEventDestroy(static_cast<cudaEvent_t>(F.hptr_event));
+  F.hptr_event = nullptr;
 
 
   F.d_ptrs = nullptr;
@@ -832,13 +827,25 @@ sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* strea
       err = "K_values_host[" + std::to_string(i) + "] is NULL";
       return SC_ERR_INVALID_ARG;
     }
+  if (!F.d_Kstage) {
+    F.Kstage_off.assign((size_t)P.nsub + 1, 0);
+    for (int32_t i = 0; i < P.nsub; i++) F.Kstage_off[(size_t)i + 1] = F.Kstage_off[(size_t)i] + F.sub_nnzK[(size_t)i];
+    void* d = nullptr;
+    FCUDA(cudaMalloc(&d, std::max<size_t>(8 * (size_t)F.Kstage_off.back(), 16)));
+    F.d_Kstage = d;
+  }
   std::vector<void*> Lst;
   FTRY(assemble_stage_begin(P, Lst, stream_v, err));  // L staging + pointer table + error reset
-  // pinned (device-mapped) host arrays: the factorization reads K straight from host memory over PCIe
-  // (its per-frame K copies are asynchronous and overlap the updates): no staging, no transfer step.
-  // Pageable arrays: cudaMemcpyAsync per host-contiguous run into a device staging buffer first.
+  std::vector<const void*> Kd((size_t)P.nsub);
+  for (int32_t i = 0; i < P.nsub; i++) Kd[(size_t)i] = static_cast<char*>(F.d_Kstage) + 8 * F.Kstage_off[(size_t)i];
+  FTRY(set_ptrs(P, Kd.data(), Lst.data(), stream, err));
+  F.w_ready = true;
+  FCUDA(cudaMemsetAsync(F.dev.flags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nflags, 1), stream));
+  FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
+  // pinned (device-mapped) host arrays: one gather kernel on `stream`; otherwise cudaMemcpyAsync per
+  // host-contiguous run on the copy stream
   bool mapped = true;
-  std::vector<const void*> Kp((size_t)P.nsub, nullptr);
+  std::vector<const void*> hdev((size_t)P.nsub, nullptr);
   for (int32_t i = 0; i < P.nsub && mapped; i++) {
     if (F.sub_nnzK[(size_t)i] == 0) continue;
     cudaPointerAttributes at{};
@@ -846,18 +853,34 @@ sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* strea
       cudaGetLastError();
       mapped = false;
     } else {
-      Kp[(size_t)i] = at.devicePointer;
+      hdev[(size_t)i] = at.devicePointer;
     }
   }
-  if (!mapped) {
-    if (!F.d_Kstage) {
-      F.Kstage_off.assign((size_t)P.nsub + 1, 0);
-      for (int32_t i = 0; i < P.nsub; i++) F.Kstage_off[(size_t)i + 1] = F.Kstage_off[(size_t)i] + F.sub_nnzK[(size_t)i];
+  if (mapped) {
+    if (!F.d_hptrs) {
       void* d = nullptr;
-      FCUDA(cudaMalloc(&d, std::max<size_t>(8 * (size_t)F.Kstage_off.back(), 16)));
-      F.d_Kstage = d;
+      FCUDA(cudaMalloc(&d, sizeof(void*) * (size_t)std::max(P.nsub, 1)));
+      F.d_hptrs = d;
+      int64_t* o = nullptr;
+      FCUDA(cudaMalloc(&o, sizeof(int64_t) * ((size_t)P.nsub + 1)));
+      FCUDA(cudaMemcpy(o, F.Kstage_off.data(), sizeof(int64_t) * ((size_t)P.nsub + 1), cudaMemcpyHostToDevice));
+      F.d_Kstage_off = o;
+      void* hp = nullptr;
+      FCUDA(cudaMallocHost(&hp, sizeof(void*) * (size_t)std::max(P.nsub, 1)));
+      F.h_hptrs = static_cast<const void**>(hp);
+      cudaEvent_t ev;
+      FCUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      FCUDA(cudaEventRecord(ev, stream));
+      F.hptr_event = ev;
     }
-    for (int32_t i = 0; i < P.nsub; i++) Kp[(size_t)i] = static_cast<char*>(F.d_Kstage) + 8 * F.Kstage_off[(size_t)i];
+    FCUDA(cudaEventSynchronize(static_cast<cudaEvent_t>(F.hptr_event)));  // the last upload consumed the pinned table
+    for (int32_t i = 0; i < P.nsub; i++) F.h_hptrs[i] = hdev[(size_t)i] ? hdev[(size_t)i] : Khost[0];
+    FCUDA(cudaMemcpyAsync(F.d_hptrs, F.h_hptrs, sizeof(void*) * (size_t)P.nsub, cudaMemcpyHostToDevice, stream));
+    FCUDA(cudaEventRecord(static_cast<cudaEvent_t>(F.hptr_event), stream));
+    gather_host_kernel<double><<<std::max(1, std::min(P.nsub, 1024)), 256, 0, stream>>>(
+        static_cast<const double* const*>(F.d_hptrs), F.d_Kstage_off, static_cast<double*>(F.d_Kstage), 0, P.nsub);
+    FCUDA(cudaGetLastError());
+  } else {
     cudaStream_t cs = static_cast<cudaStream_t>(P.copy_stream);
     // the K staging buffer is reused: the copies wait for everything enqueued on `stream` before this call
     FCUDA(cudaEventRecord(static_cast<cudaEvent_t>(P.ev_start), stream));
@@ -888,10 +911,6 @@ sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* strea
     FCUDA(cudaEventRecord(ec, cs));
     FCUDA(cudaStreamWaitEvent(stream, ec, 0));
   }
-  FTRY(set_ptrs(P, Kp.data(), Lst.data(), stream, err));
-  F.w_ready = true;
-  FCUDA(cudaMemsetAsync(F.dev.flags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nflags, 1), stream));
-  FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
   FTRY(factor_range(P, 0, F.task_chunk[0], 0, stream, err));
   return assemble_range(P, 0, P.nsub, stream_v, err);
 }

@@ -317,6 +317,10 @@ struct FactorPlan {
   void** d_ptrs = nullptr;
   void* ptr_event = nullptr;
   void* d_Kstage = nullptr;        // host-fed path: K values staging
+  void* d_hptrs = nullptr;         // host-fed path: device table of the mapped host K pointers
+  int64_t* d_Kstage_off = nullptr; //   and the staging offsets (gather_host_kernel)
+  const void** h_hptrs = nullptr;  //   pinned upload buffer of that table (guarded by hptr_event)
+  void* hptr_event = nullptr;
   std::vector<int64_t> Kstage_off;
 };
 

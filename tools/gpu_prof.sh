@@ -21,7 +21,7 @@ done
 mkdir -p gpurun_out/profiles
 python tools/make_profiles.py ${TAG:-r01} /tmp/prof gpurun_out/profiles > gpurun_out/make_profiles.log 2>&1
 for CFG in ${CFGS:-cfg2 cfg3 cfg4}; do  # per-line stall tables of the TRSM / SYRK captures
-  for K in trsm_smem_kernel trsm_warp_kernel syrk_pair_kernel factor_kernel implicit_fwd_kernel; do
+  for K in trsm_smem_kernel trsm_warp_kernel syrk_pair_kernel syrk_warp16_kernel factor_kernel implicit_fwd_kernel; do
     [ -f /tmp/prof/prof_${CFG}_$K.ncu-rep ] && python tools/ncu_lines.py /tmp/prof/prof_${CFG}_$K.ncu-rep 25 > gpurun_out/profiles/lines_${CFG}_${K}_${TAG:-r01}.txt 2>&1
   done
 done

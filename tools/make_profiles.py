@@ -24,7 +24,7 @@ os.makedirs(dst, exist_ok=True)
 
 PHASE = {"prep_panel_kernel": "prep", "prep_small_kernel": "prep", "trsm_smem_kernel": "trsm", "trsm_warp_kernel": "trsm",
          "factor_kernel": "factor", "implicit_fwd_kernel": "implicit_fwd", "implicit_bwd_kernel": "implicit_bwd",
-         "syrk_pair_kernel": "syrk"}
+         "syrk_pair_kernel": "syrk", "syrk_warp16_kernel": "syrk"}
 
 
 def to_bytes(s):
