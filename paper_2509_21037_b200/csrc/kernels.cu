@@ -1463,16 +1463,27 @@ __global__ void __launch_bounds__(256) syrk_warp16_kernel(DevPlan P, int t0, int
     const int len = __shfl_sync(0xffffffffu, my.len, sj);
     const ST* ai = XI + (int64_t)(offI + t) * 16 + g;  // A[i][k] = X_I[k][i], lane (g, t): row k = t
     const ST* bj = XJ + (int64_t)(offJ + t) * 16 + g;  // B[k][j] = X_J[k][j]
-#pragma unroll 8
-    for (int k = 0; k < len; k += 4) {
-      const bool ok = k + t < len;
-      const int64_t o = (int64_t)k * 16;
-      const double a0 = ok ? (double)ai[o] : 0.0, a1 = ok ? (double)ai[o + 8] : 0.0;
-      const double b0 = ok ? (double)bj[o] : 0.0, b1 = ok ? (double)bj[o + 8] : 0.0;
-      dmma(acc[0][0][0], acc[0][0][1], a0, b0);
-      dmma(acc[0][1][0], acc[0][1][1], a0, b1);
-      dmma(acc[1][0][0], acc[1][0][1], a1, b0);
-      dmma(acc[1][1][0], acc[1][1][1], a1, b1);
+    // 4 k steps (16 rows) per batch: all 16 fragment loads issued before the batch's 16 DMMAs (the
+    // compiler otherwise reuses the fragment registers and serialises one load latency per k step)
+    for (int k0 = 0; k0 < len; k0 += 16) {
+      double a0[4], a1[4], b0[4], b1[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const int k = k0 + 4 * u;
+        const bool ok = k + t < len;
+        const int64_t o = (int64_t)k * 16;
+        a0[u] = ok ? (double)ai[o] : 0.0;
+        a1[u] = ok ? (double)ai[o + 8] : 0.0;
+        b0[u] = ok ? (double)bj[o] : 0.0;
+        b1[u] = ok ? (double)bj[o + 8] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        dmma(acc[0][0][0], acc[0][0][1], a0[u], b0[u]);
+        dmma(acc[0][1][0], acc[0][1][1], a0[u], b1[u]);
+        dmma(acc[1][0][0], acc[1][0][1], a1[u], b0[u]);
+        dmma(acc[1][1][0], acc[1][1][1], a1[u], b1[u]);
+      }
     }
     }
   }
