@@ -1437,6 +1437,9 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
 // tile's k range to the rows both 16-column strips hold: 1.35x the useful flops instead of 1.94x with
 // 32-column groups (cfg2), and the strips themselves shrink to the tile-exact reach.
 // ------------------------------------------------------------------------------------------------
+#ifndef SC_SYRK16_BATCH
+#define SC_SYRK16_BATCH 4  // k steps whose fragment loads are issued together
+#endif
 template <typename ST>
 __global__ void __launch_bounds__(256) syrk_warp16_kernel(DevPlan P, int t0, int ntask) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1465,10 +1468,10 @@ __global__ void __launch_bounds__(256) syrk_warp16_kernel(DevPlan P, int t0, int
     const ST* bj = XJ + (int64_t)(offJ + t) * 16 + g;  // B[k][j] = X_J[k][j]
     // 4 k steps (16 rows) per batch: all 16 fragment loads issued before the batch's 16 DMMAs (the
     // compiler otherwise reuses the fragment registers and serialises one load latency per k step)
-    for (int k0 = 0; k0 < len; k0 += 16) {
-      double a0[4], a1[4], b0[4], b1[4];
+    for (int k0 = 0; k0 < len; k0 += 4 * SC_SYRK16_BATCH) {
+      double a0[SC_SYRK16_BATCH], a1[SC_SYRK16_BATCH], b0[SC_SYRK16_BATCH], b1[SC_SYRK16_BATCH];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
+      for (int u = 0; u < SC_SYRK16_BATCH; u++) {
         const int k = k0 + 4 * u;
         const bool ok = k + t < len;
         const int64_t o = (int64_t)k * 16;
@@ -1478,7 +1481,7 @@ __global__ void __launch_bounds__(256) syrk_warp16_kernel(DevPlan P, int t0, int
         b1[u] = ok ? (double)bj[o + 8] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
+      for (int u = 0; u < SC_SYRK16_BATCH; u++) {
         dmma(acc[0][0][0], acc[0][0][1], a0[u], b0[u]);
         dmma(acc[0][1][0], acc[0][1][1], a0[u], b1[u]);
         dmma(acc[1][0][0], acc[1][0][1], a1[u], b0[u]);
