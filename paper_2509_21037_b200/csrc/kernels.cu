@@ -1015,10 +1015,15 @@ __device__ __forceinline__ double gather_l(const ST* __restrict__ Lv, int32_t q)
 #ifndef SC_WARP_ZERO_REACH
 #define SC_WARP_ZERO_REACH 1
 #endif
-#ifndef SC_WARP_MINB
-#define SC_WARP_MINB 3  // 3 CTAs (12 warps) per SM: no spills at 168 registers (measured: cfg2 TRSM 1.15 vs 1.24 ms at 4, 1.54 at 5)
+#ifndef SC_WARP_WPC
+#define SC_WARP_WPC 1  // warps (tiles) per CTA (1: a finished warp frees its slot at once; 4 measured 4 % slower)
+#endif
+#ifndef SC_WARP_PER_SM
+#define SC_WARP_PER_SM 12  // resident warps per SM the registers are sized for: no spills at 168 registers
+                           // (measured, 4-warp CTAs: cfg2 TRSM 1.15 ms at 12 warps vs 1.24 at 16, 1.54 at 20)
 #endif
 constexpr int kWarpTri = 10 * 64;  // staged triangle values per warp: <= 10 8x8 blocks (kw <= 32)
+
 
 template <int BYTES>
 __device__ __forceinline__ void cp_async_el(void* dst, const void* src, int src_bytes) {  // 4 or 8 bytes
@@ -1027,10 +1032,20 @@ __device__ __forceinline__ void cp_async_el(void* dst, const void* src, int src_
                : "memory");
 }
 
-// R-row update (X[R_p] -= L[R_p, p] Y) in batches of NRBB 8-row blocks (KS <= KSMAX k steps).
-// q / row hold the gather map / row map of one batch (q[r * KSMAX/2 + k2]); warp_r_idx loads them
-// (L2), warp_r_run gathers the L values (HBM) and the old X rows (L2) of the batch, issues the next
-// batch's maps, then D = X - L Y by DMMA with Y's B fragments from shared memory, and stores.
+// Warp TRSM staging buffer Ys (32 rows of the tile's T columns): NB = 2 rows are 16 doubles (128 B)
+// with the 16-byte units XOR-swizzled by row (unit ^ (4 (row & 1) | (row & 2))), so the B-fragment
+// reads (rows 4ks + t, column 8j + g), the C-fragment double2 accesses (row 8K + g, columns 8j + 2t),
+// the row-wise cp.async / double2 copies and the column-per-lane triangle reads are all free of bank
+// conflicts; NB = 1 keeps a padded row of 12 doubles.
+template <int NB>
+__device__ __forceinline__ int ysi(int row, int col) {
+  if constexpr (NB == 2) return row * 16 + ((((col >> 1) ^ (((row & 1) << 2) | (row & 2))) << 1) | (col & 1));
+  else return row * 12 + col;
+}
+template <int NB>
+__host__ __device__ constexpr int ys_ld() { return NB == 2 ? 16 : 12; }
+
+// R maps of a batch (lane-contiguous int2 per pair of k steps) and its strip rows
 template <int KSMAX, int NRBB>
 __device__ __forceinline__ void warp_r_idx(const int32_t* __restrict__ gr, const uint16_t* __restrict__ srw, int R0,
                                            int nRB, int KS, int lane, int2 (&q)[8], int (&row)[4]) {
@@ -1039,12 +1054,19 @@ __device__ __forceinline__ void warp_r_idx(const int32_t* __restrict__ gr, const
   for (int r = 0; r < NRBB; r++) {
     const bool on = R0 + r < nRB;
     row[r] = on ? (int)__ldg(srw + 8 * (R0 + r) + g) : 0xFFFF;
-    const int2* gi = reinterpret_cast<const int2*>(gr + ((int64_t)(R0 + r) * 32 + lane) * KS);
+    const int2* gi = reinterpret_cast<const int2*>(gr) + (int64_t)(R0 + r) * (KS / 2) * 32 + lane;
 #pragma unroll
-    for (int k2 = 0; k2 < KSMAX / 2; k2++) q[r * (KSMAX / 2) + k2] = (on && 2 * k2 < KS) ? __ldg(gi + k2) : make_int2(-1, -1);
+    for (int k2 = 0; k2 < KSMAX / 2; k2++) q[r * (KSMAX / 2) + k2] = (on && 2 * k2 < KS) ? __ldg(gi + 32 * k2) : make_int2(-1, -1);
   }
 }
-template <int NB, int KSMAX, int NRBB, int LDY, typename ST>
+// R-row update (X[R_p] -= L[R_p, p] Y) in batches of NRBB 8-row blocks (KS <= KSMAX k steps).
+// q / row hold the batch's gather map / row map (loaded during the previous batch or before the
+// triangle solve); per batch: gather the L values (HBM) and the old X rows (L2), load the next
+// batch's maps, D = X - L Y by DMMA with Y's B fragments from shared memory, store.  (Measured and
+// dropped: the next batch's L values gathered before this batch's DMMAs, the first batch's before the
+// triangle solve, the step's maps staged in shared memory -- the kernel is bound by the L1 data
+// pipe, not by the latency those hide.)
+template <int NB, int KSMAX, int NRBB, typename ST>
 __device__ __forceinline__ void warp_r_run(const ST* __restrict__ Lv, const int32_t* __restrict__ gr,
                                           const uint16_t* __restrict__ srw, ST* __restrict__ Xs, const int G,
                                           const double* __restrict__ Ys, const int nRB, const int KS, const int lane,
@@ -1072,7 +1094,7 @@ __device__ __forceinline__ void warp_r_run(const ST* __restrict__ Lv, const int3
       if (ks >= KS) break;
 #pragma unroll
       for (int j = 0; j < NB; j++) {
-        const double b = Ys[(4 * ks + t) * LDY + 8 * j + g];
+        const double b = Ys[ysi<NB>(4 * ks + t, 8 * j + g)];
 #pragma unroll
         for (int r = 0; r < NRBB; r++) dmma(xo[r][j].x, xo[r][j].y, a[r][ks], b);
       }
@@ -1109,12 +1131,20 @@ __device__ __forceinline__ void warp_tri_idx(const int32_t* __restrict__ gx, int
 // gathered (cp.async) as soon as the current triangle is solved; the first R batch's maps are
 // loaded before the triangle solve.  Per warp shared memory: X_p / Y (32 x LDY), the triangle
 // values (block b, k step s: Ts[64 b + 32 s + lane]) and the reciprocal pivots.
+__device__ __forceinline__ WStep ld_wstep(const WStep* p) {
+  const int4 u = __ldg(reinterpret_cast<const int4*>(p)), v = __ldg(reinterpret_cast<const int4*>(p) + 1);
+  WStep w;
+  w.strip_row = u.x, w.a = u.y, w.kw = u.z, w.nR = u.w;
+  w.gx_off = (int64_t)(((uint64_t)(uint32_t)v.y << 32) | (uint32_t)v.x);
+  w.srow_off = (int64_t)(((uint64_t)(uint32_t)v.w << 32) | (uint32_t)v.z);
+  return w;
+}
 template <int NB, typename ST>
-__global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P, int t0, int ntask) {
-  constexpr int T = 8 * NB, LDY = T + 4;
-  __shared__ __align__(16) double wsm[4][32 * LDY + kWarpTri + 32];
+__global__ void __launch_bounds__(32 * SC_WARP_WPC, SC_WARP_PER_SM / SC_WARP_WPC) trsm_warp_kernel(DevPlan P, int t0, int ntask) {
+  constexpr int T = 8 * NB, LDY = ys_ld<NB>();
+  __shared__ __align__(16) double wsm[SC_WARP_WPC][32 * LDY + kWarpTri + 32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int wt = blockIdx.x * 4 + wid;
+  const int wt = blockIdx.x * SC_WARP_WPC + wid;
   if (wt >= ntask) return;
   double* __restrict__ Ys = wsm[wid];
   ST* __restrict__ Ts = reinterpret_cast<ST*>(Ys + 32 * LDY);  // triangle values as stored (ST)
@@ -1128,14 +1158,13 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
   const int g = lane >> 2, t = lane & 3;
   constexpr int VPR = T / 2, RPI = 32 / VPR;  // double2 per strip row, rows per warp instruction
   const int vr0 = lane / VPR, vc2 = 2 * (lane % VPR);
-  Step st_n{};
-  Panel pn_n{};
+  WStep ws_n{}, ws_nn{};  // descriptors of the next two steps
   int2 qt[10];
   if (tile.step_begin < tile.step_end) {
-    st_n = P.steps[tile.step_begin];
-    pn_n = P.panels[st_n.panel];
-    const int k8 = (pn_n.kw + 7) >> 3;
-    warp_tri_idx(P.gidx + pn_n.gx_off, k8 * (k8 + 1) / 2, lane, qt);
+    ws_n = ld_wstep(P.wsteps + tile.step_begin);
+    if (tile.step_begin + 1 < tile.step_end) ws_nn = ld_wstep(P.wsteps + tile.step_begin + 1);
+    const int k8 = (ws_n.kw + 7) >> 3;
+    warp_tri_idx(P.gidx + ws_n.gx_off, k8 * (k8 + 1) / 2, lane, qt);
     warp_tri_gather(Lv, qt, k8 * (k8 + 1) / 2, Ts, lane);
   }
   // X init (row a2): zero the tile's columns of the group-strip rows of its own reach (the panels it
@@ -1145,9 +1174,9 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
   for (int s0 = tile.step_begin; s0 < tile.step_end; s0 += 32) {
     int r0 = 0, nr = 0;
     if (s0 + lane < tile.step_end) {
-      const Step st = P.steps[s0 + lane];
-      r0 = st.strip_row;
-      nr = P.panels[st.panel].kw;
+      const WStep w = ld_wstep(P.wsteps + s0 + lane);
+      r0 = w.strip_row;
+      nr = w.kw;
     }
     const int ns = min(32, tile.step_end - s0);
     for (int j = 0; j < ns; j++) {
@@ -1165,29 +1194,29 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
   }
   __syncwarp();
   for (int s = tile.step_begin; s < tile.step_end; s++) {
-    const Step st = st_n;
-    const Panel pn = pn_n;
-    const int kw = pn.kw, kw8 = (kw + 7) >> 3, KS = 2 * kw8;
-    const int32_t* __restrict__ gx = P.gidx + pn.gx_off;
+    const WStep st = ws_n;
+    const int kw = st.kw, kw8 = (kw + 7) >> 3, KS = 2 * kw8;
+    const int32_t* __restrict__ gx = P.gidx + st.gx_off;
     ST* __restrict__ xp = Xs + (int64_t)st.strip_row * G;
     // X_p -> Ys (rows kw..8 kw8 zero-filled): cp.async for FP64 strips, converting loads for FP32
     if constexpr (sizeof(ST) == 8) {
       for (int r = vr0; r < 8 * kw8; r += RPI)
-        cp_async16(Ys + r * LDY + vc2, xp + (int64_t)(r < kw ? r : 0) * G + vc2, r < kw ? 16 : 0);
+        cp_async16(Ys + ysi<NB>(r, vc2), xp + (int64_t)(r < kw ? r : 0) * G + vc2, r < kw ? 16 : 0);
     } else {
       for (int r = vr0; r < 8 * kw8; r += RPI)
-        *reinterpret_cast<double2*>(Ys + r * LDY + vc2) = r < kw ? ld2(xp + (int64_t)r * G + vc2) : make_double2(0.0, 0.0);
+        *reinterpret_cast<double2*>(Ys + ysi<NB>(r, vc2)) = r < kw ? ld2(xp + (int64_t)r * G + vc2) : make_double2(0.0, 0.0);
     }
     cp_async_commit();
     const bool more = s + 1 < tile.step_end;
-    if (more) {  // next step's descriptors and triangle gather map
-      st_n = P.steps[s + 1];
-      pn_n = P.panels[st_n.panel];
-      const int k8 = (pn_n.kw + 7) >> 3;
-      warp_tri_idx(P.gidx + pn_n.gx_off, k8 * (k8 + 1) / 2, lane, qt);
+    if (more) {  // next step's triangle gather map (its descriptor was loaded a step earlier), and the
+                 // descriptor of the step after it
+      ws_n = ws_nn;
+      const int k8 = (ws_n.kw + 7) >> 3;
+      warp_tri_idx(P.gidx + ws_n.gx_off, k8 * (k8 + 1) / 2, lane, qt);
+      if (s + 2 < tile.step_end) ws_nn = ld_wstep(P.wsteps + s + 2);
     }
-    // first R batch's maps
-    const int nRB = (pn.nR + 7) >> 3;
+    // first R batch's maps (they travel during the triangle solve)
+    const int nRB = (st.nR + 7) >> 3;
     const int32_t* __restrict__ gr = gx + 64 * (kw8 * (kw8 + 1) / 2);
     const uint16_t* __restrict__ srw = P.srows + st.srow_off;
     int2 qr[8];
@@ -1200,7 +1229,7 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
       const int K = lane >> 3, gg = lane & 7;
       const bool live = lane < kw;
       const double d = live ? (double)Ts[64 * warp_tri_block(K, K, kw8) + 32 * (gg >> 2) + 4 * gg + (gg & 3)] : 1.0;
-      if (live && (!(d > 0.0) || !isfinite(d))) flag_zero_pivot(P, sub, pn.a + lane);
+      if (live && (!(d > 0.0) || !isfinite(d))) flag_zero_pivot(P, sub, st.a + lane);
       Rv[lane] = live ? 1.0 / d : 0.0;
     }
     __syncwarp();
@@ -1210,25 +1239,25 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
       if (K > 0) {
         double2 x[NB];
 #pragma unroll
-        for (int j = 0; j < NB; j++) x[j] = *reinterpret_cast<const double2*>(Ys + (8 * K + g) * LDY + 8 * j + 2 * t);
+        for (int j = 0; j < NB; j++) x[j] = *reinterpret_cast<const double2*>(Ys + ysi<NB>(8 * K + g, 8 * j + 2 * t));
         for (int J = 0; J < K; J++) {
           const ST* tb = Ts + 64 * warp_tri_block(J, K, kw8);
           const double a0 = -(double)tb[lane], a1 = -(double)tb[32 + lane];
 #pragma unroll
           for (int j = 0; j < NB; j++) {
-            dmma(x[j].x, x[j].y, a0, Ys[(8 * J + t) * LDY + 8 * j + g]);
-            dmma(x[j].x, x[j].y, a1, Ys[(8 * J + 4 + t) * LDY + 8 * j + g]);
+            dmma(x[j].x, x[j].y, a0, Ys[ysi<NB>(8 * J + t, 8 * j + g)]);
+            dmma(x[j].x, x[j].y, a1, Ys[ysi<NB>(8 * J + 4 + t, 8 * j + g)]);
           }
         }
 #pragma unroll
-        for (int j = 0; j < NB; j++) *reinterpret_cast<double2*>(Ys + (8 * K + g) * LDY + 8 * j + 2 * t) = x[j];
+        for (int j = 0; j < NB; j++) *reinterpret_cast<double2*>(Ys + ysi<NB>(8 * K + g, 8 * j + 2 * t)) = x[j];
         __syncwarp();
       }
       if (lane < T) {
         const ST* tb = Ts + 64 * warp_tri_block(K, K, kw8);
         double xv[8];
 #pragma unroll
-        for (int i = 0; i < 8; i++) xv[i] = Ys[(8 * K + i) * LDY + lane];
+        for (int i = 0; i < 8; i++) xv[i] = Ys[ysi<NB>(8 * K + i, lane)];
 #pragma unroll
         for (int k = 0; k < 8; k++) {
           xv[k] *= Rv[8 * K + k];
@@ -1236,21 +1265,21 @@ __global__ void __launch_bounds__(128, SC_WARP_MINB) trsm_warp_kernel(DevPlan P,
           for (int i = k + 1; i < 8; i++) xv[i] = fma(-(double)tb[32 * (k >> 2) + 4 * i + (k & 3)], xv[k], xv[i]);
         }
 #pragma unroll
-        for (int i = 0; i < 8; i++) Ys[(8 * K + i) * LDY + lane] = xv[i];
+        for (int i = 0; i < 8; i++) Ys[ysi<NB>(8 * K + i, lane)] = xv[i];
       }
       __syncwarp();
     }
     // Ts is free: gather the next step's triangle while this step's R rows are updated
     if (more) {
-      const int k8 = (pn_n.kw + 7) >> 3;
+      const int k8 = (ws_n.kw + 7) >> 3;
       warp_tri_gather(Lv, qt, k8 * (k8 + 1) / 2, Ts, lane);
     }
     cp_async_commit();
     // the solved rows are final: into the group strip
     for (int r = vr0; r < kw; r += RPI)
-      st2(xp + (int64_t)r * G + vc2, *reinterpret_cast<const double2*>(Ys + r * LDY + vc2));
-    if (KS <= 4) warp_r_run<NB, 4, 4, LDY, ST>(Lv, gr, srw, Xs, G, Ys, nRB, KS, lane, qr, rr);
-    else warp_r_run<NB, 8, 2, LDY, ST>(Lv, gr, srw, Xs, G, Ys, nRB, KS, lane, qr, rr);
+      st2(xp + (int64_t)r * G + vc2, *reinterpret_cast<const double2*>(Ys + ysi<NB>(r, vc2)));
+    if (KS <= 4) warp_r_run<NB, 4, 4, ST>(Lv, gr, srw, Xs, G, Ys, nRB, KS, lane, qr, rr);
+    else warp_r_run<NB, 8, 2, ST>(Lv, gr, srw, Xs, G, Ys, nRB, KS, lane, qr, rr);
     __syncwarp();  // this step's strip writes are visible to every lane of the next step
   }
   cp_async_wait<0>();
@@ -1763,6 +1792,14 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, csc_off, &D.cls_csc_off, err));
   TRY(upload(P, tiles, &D.tiles, err));
   TRY(upload(P, steps, &D.steps, err));
+  if (P.warp_trsm) {
+    std::vector<WStep> ws(steps.size());
+    for (size_t q = 0; q < steps.size(); q++) {
+      const Panel& pn = panels[(size_t)steps[q].panel];
+      ws[q] = WStep{steps[q].strip_row, pn.a, pn.kw, pn.nR, pn.gx_off, steps[q].srow_off};
+    }
+    TRY(upload(P, ws, &D.wsteps, err));
+  }
   TRY(upload(P, srows, &D.srows, err));
   TRY(upload(P, groups, &D.groups, err));
   TRY(upload(P, greach, &D.greach, err));
@@ -1988,13 +2025,14 @@ static sc_status launch_trsm_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
     const int ntr = (int)P.trsm_tasks.size();
     const int a = all ? 0 : task_lb(P.trsm_tasks, 0, ntr, s0), b = all ? ntr : task_lb(P.trsm_tasks, 0, ntr, s1);
     if (b > a) {
-      const int nb = (b - a + 3) / 4;  // 4 warps (tiles) per CTA
+      constexpr int W = SC_WARP_WPC, NT = 32 * SC_WARP_WPC;
+      const int nb = (b - a + W - 1) / W;  // W warps (tiles) per CTA
       if (P.esz == 4) {
-        if (P.T == 8) trsm_warp_kernel<1, float><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
-        else trsm_warp_kernel<2, float><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
+        if (P.T == 8) trsm_warp_kernel<1, float><<<nb, NT, 0, stream>>>(P.dev, a, b - a);
+        else trsm_warp_kernel<2, float><<<nb, NT, 0, stream>>>(P.dev, a, b - a);
       } else {
-        if (P.T == 8) trsm_warp_kernel<1, double><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
-        else trsm_warp_kernel<2, double><<<nb, 128, 0, stream>>>(P.dev, a, b - a);
+        if (P.T == 8) trsm_warp_kernel<1, double><<<nb, NT, 0, stream>>>(P.dev, a, b - a);
+        else trsm_warp_kernel<2, double><<<nb, NT, 0, stream>>>(P.dev, a, b - a);
       }
       CUDA_TRY(cudaGetLastError());
     }

@@ -311,7 +311,8 @@ sc_status analyse_class(const sc_subdomain_desc& d, int T, int kGroup, int PW, i
           } else {
             const int32_t k = (int32_t)(std::lower_bound(R, R + p.nR, r) - R);
             const int lane = 4 * (k & 7) + t;
-            C.gidx[(size_t)(roff + ((int64_t)(k >> 3) * 32 + lane) * KS + (cc >> 2))] = (int32_t)q;
+            const int ks = cc >> 2;  // k step; R maps are [row block][k step pair][lane] int2
+            C.gidx[(size_t)(roff + (((int64_t)(k >> 3) * (KS / 2) + (ks >> 1)) * 32 + lane) * 2 + (ks & 1))] = (int32_t)q;
           }
         }
     }
@@ -869,6 +870,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
       Tw = e ? std::atoi(e) : 16;
     }
     if (!(Tw == 8 || Tw == 16)) FAIL(SC_ERR_INVALID_ARG, "warp TRSM needs tile_cols 8 or 16");
+    G0 = 16;  // 16-column group strips (syrk_warp16_kernel)
     P.wmode = false;
     sc_status st = analyse_all(Tw, true, -1);
     if (st != SC_OK) return st;

@@ -79,7 +79,8 @@ struct Panel {
 // loads its m8n8k4 A fragments straight from the caller's CSC values (L crosses HBM once):
 //   triangle: 8x8 blocks (I >= K) in the order K = 0.., I = K..kw8-1; per block [lane][s] (s = 0,1)
 //             -> L[a + 8I + g][a + 8K + 4s + t]   (lane = 4g + t)
-//   R rows:   per row block RB of R_p, [lane][s] (s < KS = 2 kw8) -> L[R_p[8RB + g]][a + 4s + t]
+//   R rows:   per row block RB of R_p, [s/2][lane][s%2] (s < KS = 2 kw8) -> L[R_p[8RB + g]][a + 4s + t]
+//             (one int2 per lane and pair of k steps: lane-contiguous, bank-conflict free once staged)
 SC_HD inline int64_t warp_tri_block(int K, int I, int kw8) { return (int64_t)(K * kw8 - K * (K - 1) / 2 + (I - K)); }
 SC_HD inline int64_t warp_gx_size(int kw, int nR) {
   const int kw8 = (kw + 7) / 8, nRB = (nR + 7) / 8;
@@ -105,6 +106,13 @@ struct Step {
   int32_t grow, pad;               // row of the panel in the tile's group strip (solved rows go there)
   int64_t srow_off;
 };
+// Warp TRSM step descriptor: the Step and Panel fields one step of trsm_warp_kernel reads, in one
+// 32-byte sector (one dependent load per step instead of Step -> Panel)
+struct WStep {
+  int32_t strip_row, a, kw, nR;    // strip row of the panel, its first column, width, pruned rows
+  int64_t gx_off, srow_off;        // fragment gather map (global), strip rows of R_p (global)
+};
+static_assert(sizeof(WStep) == 32, "WStep is one sector");
 
 
 // SYRK column group (width kGroup, a union of TRSM tiles): its X strip in global memory holds
@@ -338,6 +346,7 @@ struct DevPlan {
   const int64_t* cls_csc_off;
   const Tile* tiles;
   const Step* steps;
+  const WStep* wsteps;             // warp TRSM: per step, Step + Panel fields (empty otherwise)
   const uint16_t* srows;           // concatenated per class (Step.srow_off globalised)
   const Group* groups;
   const Reach* greach;
