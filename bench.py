@@ -372,6 +372,8 @@ def main():
     ap.add_argument("--strip", default="auto", choices=["auto", "shared", "global"],
                     help="where TRSM tiles keep their X strip (sc_options.x_strip)")
     ap.add_argument("--trsm", default="auto", choices=["auto", "cta", "warp"], help="sc_options.trsm_kernel")
+    ap.add_argument("--syrk", default="output", choices=["output", "input"],
+                    help="SYRK splitting (P:523-540): output (default) or input (f3 ablation, SC_SYRK_SPLIT=input)")
     ap.add_argument("--per-config", default="cfg3,cfg4",
                     help="extra configs timed in the same run (N=1 only), reported under per_config")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of oracle work for cpu_baseline")
@@ -402,6 +404,8 @@ def main():
     peaks = load_peaks()
 
     P, shard_info = setup_problem(args, args.config, world, rank)
+    if args.syrk == "input":
+        os.environ["SC_SYRK_SPLIT"] = "input"
     import psutil
     rss0 = psutil.Process().memory_info().rss
     t_plan0 = time.perf_counter()
@@ -569,7 +573,7 @@ def main():
                    "skip": args.skip, "tile_cols": st["tile_cols"], "panel_cols": st["panel_cols"],
                    "trsm_kernel": {1: "cta", 2: "warp"}.get(st["trsm_kernel"]),
                    "x_strip": {1: "shared", 2: "global"}.get(st["x_strip"], "?"),
-                   "trsm_tasks_2cta": st["trsm_tasks_2cta"],
+                   "trsm_tasks_2cta": st["trsm_tasks_2cta"], "syrk_split": args.syrk,
                    "parallelism": (f"replica batch per rank x{world}" if (args.weak and world > 1) else
                                    f"one batch LPT-sharded over {world} rank(s), no collective in assembly"),
                    "shard": shard_info, "nccl_ranks": world, "per_rank_ms": per_rank_ms,

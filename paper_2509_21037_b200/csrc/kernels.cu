@@ -1553,6 +1553,58 @@ __device__ __forceinline__ int64_t apply_tile_index(int rb, int cb) { return (in
 #endif
 constexpr int kApplyTPC = SC_APPLY_TPC;  // tiles per CTA
 
+// ------------------------------------------------------------------------------------------------
+// Input-split SYRK ("Splitting of the input matrix"; SURVEY f3 ablation): the k
+// loop of F = X^T X is cut into block rows -- here the plan's common-row segments of each group pair
+// -- and each block row's small SYRK touches only the output block of the columns that are non-zero
+// in it; the partial results are summed into F' (zeroed first) with FP64 atomics, so the summation
+// order (and the last bits of F) varies from run to run.  The default output-split kernels above
+// write every F' entry once.
+// ------------------------------------------------------------------------------------------------
+template <typename ST>
+__global__ void __launch_bounds__(256) syrk_input_split_kernel(DevPlan P, const SplitTask* __restrict__ tasks,
+                                                               int64_t t0, int64_t ntask) {
+  const int lane = threadIdx.x & 31;
+  const int64_t ti = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (ti >= ntask) return;
+  const SplitTask tk = tasks[t0 + ti];
+  const Pair pr = P.pairs[tk.pair];
+  const Seg sg = P.segs[tk.seg];
+  const Group gI = P.groups[pr.I], gJ = P.groups[pr.J];
+  const int G = P.G, ib = tk.ij >> 2, jb = tk.ij & 3;
+  const ST* __restrict__ XI = static_cast<const ST*>(P.X) + P.sub_X_base[tk.sub] + gI.x_off + 16 * ib;
+  const ST* __restrict__ XJ = static_cast<const ST*>(P.X) + P.sub_X_base[tk.sub] + gJ.x_off + 16 * jb;
+  const int g = lane >> 2, t = lane & 3;
+  const ST* ai = XI + (int64_t)(sg.offI + t) * G + g;
+  const ST* bj = XJ + (int64_t)(sg.offJ + t) * G + g;
+  double acc[2][2][2] = {};
+  for (int k = 0; k < sg.len; k += 4) {
+    const bool ok = k + t < sg.len;
+    const int64_t o = (int64_t)k * G;
+    const double a0 = ok ? (double)ai[o] : 0.0, a1 = ok ? (double)ai[o + 8] : 0.0;
+    const double b0 = ok ? (double)bj[o] : 0.0, b1 = ok ? (double)bj[o + 8] : 0.0;
+    dmma(acc[0][0][0], acc[0][0][1], a0, b0);
+    dmma(acc[0][1][0], acc[0][1][1], a0, b1);
+    dmma(acc[1][0][0], acc[1][0][1], a1, b0);
+    dmma(acc[1][1][0], acc[1][1][1], a1, b1);
+  }
+  ST* __restrict__ F = static_cast<ST*>(P.F) + P.sub_F_base[tk.sub];
+  const bool diag = pr.I == pr.J;
+#pragma unroll
+  for (int i = 0; i < 2; i++) {
+    const int r = 16 * ib + 8 * i + g;
+    if (r >= gI.width) continue;
+#pragma unroll
+    for (int j = 0; j < 2; j++)
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const int c = 16 * jb + 8 * j + 2 * t + h;
+        if (c >= gJ.width || (diag && r < c)) continue;
+        atomicAdd(F + f_index(gI.col0 + r, gJ.col0 + c), (ST)acc[i][j][h]);
+      }
+  }
+}
+
 template <typename ST>
 __global__ void __launch_bounds__(kThreads) apply_tile_kernel(DevPlan P, const double* __restrict__ lambda, int ntask) {
   constexpr int AT = kApplyTile;
@@ -1834,6 +1886,24 @@ sc_status upload_plan(Plan& P, std::string& err) {
   TRY(upload(P, P.prep_small_tasks, &D.prep_small_tasks, err));
   TRY(upload(P, P.trsm_tasks, &D.trsm_tasks, err));
   TRY(upload(P, P.syrk_tasks, &D.syrk_tasks, err));
+  if (P.syrk_input) {  // (sub, pair, segment, 16 x 16 sub-tile) tasks of the input-split SYRK
+    std::vector<SplitTask> st;
+    P.split_sub_begin.assign((size_t)P.nsub + 1, 0);
+    const int nb = P.G / 16;
+    size_t q = 0;
+    for (int32_t i = 0; i < P.nsub; i++) {
+      P.split_sub_begin[(size_t)i] = (int64_t)st.size();
+      for (; q < P.syrk_tasks.size() && P.syrk_tasks[q].x == i; q++) {
+        const Pair& pr = pairs[(size_t)P.syrk_tasks[q].y];
+        for (int32_t sg = pr.seg_begin; sg < pr.seg_end; sg++)
+          for (int ib = 0; ib < nb; ib++)
+            for (int jb = 0; jb < nb; jb++)
+              if (!(pr.I == pr.J && jb > ib)) st.push_back(SplitTask{i, P.syrk_tasks[q].y, sg, ib * 4 + jb});
+      }
+    }
+    P.split_sub_begin[(size_t)P.nsub] = (int64_t)st.size();
+    TRY(upload(P, st, &P.d_split, err));
+  }
   TRY(upload(P, P.apply_tasks, &D.apply_tasks, err));
   TRY(upload(P, P.sub_slm_off, &D.sub_slm_off, err));
   TRY(upload(P, P.slm, &D.slm, err));
@@ -2070,6 +2140,18 @@ static sc_status launch_trsm_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
 
 static sc_status launch_syrk_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t stream, std::string& err) {
   const bool all = s0 == 0 && s1 == P.nsub;
+  if (P.syrk_input) {  // f3 ablation: zero F' of the range, then the input-split kernel's atomics
+    const int64_t f0 = P.sub_F_base[(size_t)s0], f1 = s1 < P.nsub ? P.sub_F_base[(size_t)s1] : P.F_doubles;
+    CUDA_TRY(cudaMemsetAsync(static_cast<char*>(P.dev.F) + (size_t)P.esz * f0, 0, (size_t)P.esz * (f1 - f0), stream));
+    const int64_t a = P.split_sub_begin[(size_t)s0], n = P.split_sub_begin[(size_t)s1] - a;
+    if (n > 0) {
+      const unsigned nb = (unsigned)((n + 7) / 8);
+      if (P.esz == 4) syrk_input_split_kernel<float><<<nb, 256, 0, stream>>>(P.dev, P.d_split, a, n);
+      else syrk_input_split_kernel<double><<<nb, 256, 0, stream>>>(P.dev, P.d_split, a, n);
+      CUDA_TRY(cudaGetLastError());
+    }
+    return SC_OK;
+  }
   {
     const int nsy = (int)P.syrk_tasks.size();
     const int a = all ? 0 : task_lb(P.syrk_tasks, 0, nsy, s0), b = all ? nsy : task_lb(P.syrk_tasks, 0, nsy, s1);

@@ -760,6 +760,7 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
   P.wmode = false;
   if (const char* e = std::getenv("SC_OVERLAP")) P.overlap = std::atoi(e);
   if (const char* e = std::getenv("SC_TRSM_MODE")) P.wmode = e[0] == 'W';
+  if (const char* e = std::getenv("SC_SYRK_SPLIT")) P.syrk_input = e[0] == 'i';
   if (P.esz == 4 && P.wmode) FAIL(SC_ERR_INVALID_ARG, "precision 32 supports the Y-mode TRSM only");
   if (const char* e = std::getenv("SC_GROUP")) G0 = std::atoi(e);
   if (!(G0 == 16 || G0 == 32 || G0 == 64)) FAIL(SC_ERR_INVALID_ARG, "SC_GROUP must be 16, 32 or 64");

@@ -147,6 +147,11 @@ struct Seg {
 struct I2 {
   int32_t x, y;
 };
+// Input-split SYRK (f3 ablation, SC_SYRK_SPLIT=input): one warp per (subdomain, pair, common-row
+// segment, 16 x 16 sub-tile (ib, jb) of the pair's G x G output tile)
+struct SplitTask {
+  int32_t sub, pair, seg, ij;      // ij = ib * 4 + jb
+};
 
 // Apply: one 64 x 64 tile (row block rb >= column block cb) of the lower F' of subdomain sub.
 constexpr int kApplyTile = 64;
@@ -287,6 +292,7 @@ struct DevFactor {
   // implicit apply on the factor workspace
   const FUpd* anc;
   const I2* ptasks;                // (sub, global panel) in forward (level) order; backward = reversed
+  const int32_t* plev;             // per class (offset cls_panel0): its global panels in level order
   const int32_t* bt_rp;            // per class (offset cls_bt0) CSR of B~^T by permuted row
   const int32_t* bt_a;
   const double* bt_v;
@@ -309,6 +315,7 @@ struct FactorPlan {
   std::vector<FTask> tasks;
   std::vector<FUpd> anc;
   std::vector<I2> ptasks;
+  std::vector<int32_t> plev;       // per class: its global panels sorted by level (DevFactor::plev)
   std::vector<int32_t> bt_rp, bt_a;
   std::vector<double> bt_v;
   std::vector<int64_t> cls_bt0, sub_x_base;
@@ -396,6 +403,9 @@ struct Plan {
   int32_t gs2 = 0;                 // global strips at T = 16 with this many CTAs per SM (2; 3 via SC_GS2=3)
   bool wmode = true;               // TRSM update operand W_p = L[R_p,p] inv(L_pp) (wide panels) or L (Y mode)
   bool warp_trsm = false;          // fused warp-per-tile TRSM straight from the CSC values (no prep)
+  bool syrk_input = false;         // SC_SYRK_SPLIT=input: input-split SYRK (f3 ablation) instead of output split
+  const SplitTask* d_split = nullptr;
+  std::vector<int64_t> split_sub_begin;  // first split task of each subdomain (nsub + 1)
   int32_t warp_ctas = 4;           // warps (tiles) per CTA of the warp TRSM
   int32_t nsub = 0;
   std::vector<ClassPlan> classes;
