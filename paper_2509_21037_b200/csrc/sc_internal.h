@@ -292,7 +292,6 @@ struct DevFactor {
   // implicit apply on the factor workspace
   const FUpd* anc;
   const I2* ptasks;                // (sub, global panel) in forward (level) order; backward = reversed
-  const int32_t* plev;             // per class (offset cls_panel0): its global panels in level order
   const int32_t* bt_rp;            // per class (offset cls_bt0) CSR of B~^T by permuted row
   const int32_t* bt_a;
   const double* bt_v;
@@ -315,7 +314,6 @@ struct FactorPlan {
   std::vector<FTask> tasks;
   std::vector<FUpd> anc;
   std::vector<I2> ptasks;
-  std::vector<int32_t> plev;       // per class: its global panels sorted by level (DevFactor::plev)
   std::vector<int32_t> bt_rp, bt_a;
   std::vector<double> bt_v;
   std::vector<int64_t> cls_bt0, sub_x_base;

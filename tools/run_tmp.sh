@@ -1,4 +1,4 @@
 cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 900 python bench.py --config cfg2 --steps 10 --warmup 3 > gpurun_out/bench_cfg2.json 2> gpurun_out/bench_cfg2.err
+CFGS=cfg2 KERNELS="trsm_warp_kernel syrk_warp16_kernel factor_kernel implicit_fwd_kernel" TAG=r02 BENCH_CFGS="cfg2" bash tools/gpu_prof.sh > gpurun_out/prof.log 2>&1
+bash tools/ablation.sh > gpurun_out/abl.log 2>&1
+python tools/ablation_md.py gpurun_out/ablation.jsonl r02 > gpurun_out/ablation_r02.md 2>&1
