@@ -14,6 +14,7 @@ on a bounded sample of the same workload (rank 0 only).  Prints ONE JSON line on
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import sys
@@ -208,8 +209,9 @@ def time_assembly(plan, Ls, steps, warmup, world, clock_index=None):
     import torch
     import torch.distributed as dist
     stream = torch.cuda.current_stream()
+    Lp = plan.pointer_array(Ls)  # the C pointer array, built once (not re-marshalled per call)
     for _ in range(warmup):
-        plan.assemble(Ls)
+        plan.assemble(Lp)
     torch.cuda.synchronize()
     plan.check()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(steps)]
@@ -224,7 +226,7 @@ def time_assembly(plan, Ls, steps, warmup, world, clock_index=None):
         start.record(stream)
         for k in range(steps):
             plan.set_timing_events(evs[k])
-            plan.assemble(Ls)
+            plan.assemble(Lp)
         stop.record(stream)
         torch.cuda.synchronize()
     plan.set_timing_events(None)
@@ -481,12 +483,14 @@ def main():
     e2e = e2e_L = None
     if not args.no_e2e:
         hostL = [torch.from_numpy(np.ascontiguousarray(sd.L_values)).pin_memory() for sd in P.subdomains]
-        e2e_L = e2e_run(lambda: plan.assemble_host(hostL), sum(8 * sd.L_values.size for sd in P.subdomains),
+        hostLp = plan.pointer_array(hostL)
+        e2e_L = e2e_run(lambda: plan.assemble_host(hostLp), sum(8 * sd.L_values.size for sd in P.subdomains),
                         "pinned H2D of this rank's L values + assemble + 1 sc_apply (+NCCL all-reduce) + D2H of q")
         del hostL
         if factor is not None:
             hostK = [torch.from_numpy(sd.K_lower()[2]).pin_memory() for sd in P.subdomains]
-            e2e = e2e_run(lambda: plan.factorize_assemble_host(hostK), sum(8 * k.numel() for k in hostK),
+            hostKp = (ctypes.c_void_p * max(len(hostK), 1))(*[k.data_ptr() for k in hostK])
+            e2e = e2e_run(lambda: plan.factorize_assemble_host(hostKp), sum(8 * k.numel() for k in hostK),
                           "pinned H2D of this rank's K values (lower triangle) + device numeric factorization + "
                           "assemble + 1 sc_apply (+NCCL all-reduce) + D2H of q (sc_factorize_assemble_host)")
             del hostK

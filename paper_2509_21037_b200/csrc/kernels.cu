@@ -1467,12 +1467,15 @@ __global__ void __launch_bounds__(kThreads) syrk_pair_kernel(DevPlan P, int t0) 
 // 32-column groups (cfg2), and the strips themselves shrink to the tile-exact reach.
 // ------------------------------------------------------------------------------------------------
 #ifndef SC_SYRK16_BATCH
-#define SC_SYRK16_BATCH 4  // k steps whose fragment loads are issued together
+#define SC_SYRK16_BATCH 2  // k steps whose fragment loads are issued together
+#endif
+#ifndef SC_SYRK16_WPC
+#define SC_SYRK16_WPC 1    // warps (output tiles) per CTA: 1 (a finished tile frees its slot at once)
 #endif
 template <typename ST>
-__global__ void __launch_bounds__(256) syrk_warp16_kernel(DevPlan P, int t0, int ntask) {
+__global__ void __launch_bounds__(32 * SC_SYRK16_WPC) syrk_warp16_kernel(DevPlan P, int t0, int ntask) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int ti = blockIdx.x * 8 + wid;
+  const int ti = blockIdx.x * SC_SYRK16_WPC + wid;
   if (ti >= ntask) return;
   const I2 task = P.syrk_tasks[t0 + ti];
   const int sub = task.x;
@@ -2157,8 +2160,9 @@ static sc_status launch_syrk_range(Plan& P, int32_t s0, int32_t s1, cudaStream_t
     const int a = all ? 0 : task_lb(P.syrk_tasks, 0, nsy, s0), b = all ? nsy : task_lb(P.syrk_tasks, 0, nsy, s1);
     if (b > a && P.G == 16) {  // warp per 16 x 16 output tile
       const int nt = b - a;
-      if (P.esz == 4) syrk_warp16_kernel<float><<<(nt + 7) / 8, kThreads, 0, stream>>>(P.dev, a, nt);
-      else syrk_warp16_kernel<double><<<(nt + 7) / 8, kThreads, 0, stream>>>(P.dev, a, nt);
+      constexpr int W = SC_SYRK16_WPC;
+      if (P.esz == 4) syrk_warp16_kernel<float><<<(nt + W - 1) / W, 32 * W, 0, stream>>>(P.dev, a, nt);
+      else syrk_warp16_kernel<double><<<(nt + W - 1) / W, 32 * W, 0, stream>>>(P.dev, a, nt);
       CUDA_TRY(cudaGetLastError());
     } else if (b > a) {
       if (P.esz == 4) {

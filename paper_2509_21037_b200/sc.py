@@ -216,9 +216,19 @@ class SCPlan:
         self.nsub = len(subdomains)
 
     # -- preprocessing
+    def pointer_array(self, L_values: Sequence):
+        """The C pointer array (void*[nsub]) of per-subdomain value buffers, for reuse across calls:
+        assemble / assemble_host / prepare_factor accept it in place of the list (no per-call
+        marshalling of nsub Python objects)."""
+        return self._value_ptrs(L_values)
+
     def _value_ptrs(self, L_values: Sequence):
         """Pointer array of the per-subdomain L values; tensors must have the plan's element type
-        (float64, or float32 for precision 32)."""
+        (float64, or float32 for precision 32).  A pointer array from pointer_array() passes through."""
+        if isinstance(L_values, ctypes.Array):
+            if len(L_values) < max(self.nsub, 1):
+                raise ValueError("pointer array shorter than the number of subdomains")
+            return L_values
         ptrs = (_P * max(self.nsub, 1))()
         want = 8 if self.precision == 64 else 4
         for i, t in enumerate(L_values):
@@ -265,9 +275,12 @@ class SCPlan:
     def factorize_assemble_host(self, K_values: Sequence, stream=None):
         """K values in host memory (pinned float64 tensors or numpy arrays): H2D copy of K, device
         factorization, assembly -- all inside the call."""
-        kp = (_P * max(self.nsub, 1))()
-        for i, t in enumerate(K_values):
-            kp[i] = t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
+        if isinstance(K_values, ctypes.Array):  # from pointer_array()
+            kp = K_values
+        else:
+            kp = (_P * max(self.nsub, 1))()
+            for i, t in enumerate(K_values):
+                kp[i] = t.data_ptr() if hasattr(t, "data_ptr") else t.ctypes.data
         _check(lib().sc_factorize_assemble_host(self._h, kp, _stream_handle(stream)))
 
     # -- solution
