@@ -871,7 +871,6 @@ sc_status build_plan(const sc_subdomain_desc* sd, int32_t nsub, const sc_options
       Tw = e ? std::atoi(e) : 16;
     }
     if (!(Tw == 8 || Tw == 16)) FAIL(SC_ERR_INVALID_ARG, "warp TRSM needs tile_cols 8 or 16");
-    G0 = 16;  // 16-column group strips (syrk_warp16_kernel)
     P.wmode = false;
     sc_status st = analyse_all(Tw, true, -1);
     if (st != SC_OK) return st;
