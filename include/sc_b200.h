@@ -196,8 +196,9 @@ sc_status sc_apply_implicit(sc_plan_t p, const double* lambda, double* q, void* 
    L_i L_i^T with the same pattern and CSC order, so its output feeds sc_assemble_batch unchanged, from the
    values of K_reg,i.  Method: left-looking supernodal Cholesky over panels of <= 32 columns (its own
    partition), one warp per 32-row frame of a panel, DMMA updates from the finished descendant panels,
-   the diagonal block factored and inverted in the warp, the rows below it multiplied by the inverse.
-   Deterministic (fixed update order, no atomics on values). */
+   the diagonal block factored and inverted in the warp, the rows below it multiplied by the inverse;
+   frames with many descendant updates hand groups of them to partial-update tasks whose blocks
+   the frame adds in a fixed order.  Deterministic (fixed update order, no atomics on values). */
 typedef struct {
   const int64_t* K_colptr;   /* n+1: CSC of the LOWER triangle (diagonal included) of K_reg,i in the
                                 ORIGINAL DOF numbering (before perm), rows strictly ascending; every

@@ -98,8 +98,11 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
     task = __shfl_sync(~0u, task, 0);
     if (task >= t1) break;
     const FTask tk = F.tasks[task];
-    for (int fi = 0; fi < tk.nf; fi++) {
-    const FFrame fr = F.frames[tk.frame + fi];
+    const bool part = tk.nf < 0;  // partial update task of a split frame (SC_FACTOR_SPLIT)
+    if (part && stage) continue;  // staging has no updates
+    const FPart pt = part ? F.parts[tk.frame] : FPart{};
+    for (int fi = 0; fi < (part ? 1 : tk.nf); fi++) {
+    const FFrame fr = F.frames[part ? pt.frame : tk.frame + fi];
     const FPanel pn = F.panels[fr.panel];
     const int sub = tk.sub;
     int* flags = F.flags + (F.sub_flag_base[sub] - F.cls_panel0[F.sub_cls[sub]]);  // indexed by global panel
@@ -117,8 +120,9 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
     // ---- updates from the finished descendant panels (left-looking), 32 list entries at a time:
     // lane l loads entry l's descriptor and its panel, waits (acquire) for that panel; then the
     // entries are processed in list order (deterministic)
-    for (int u0 = fr.u_begin; u0 < (stage ? fr.u_begin : fr.u_end); u0 += 32) {
-      const int nu = min(32, fr.u_end - u0);
+    const int ub = part ? pt.u_begin : fr.u_begin, ue = part ? pt.u_end : fr.u_end;
+    for (int u0 = ub; u0 < (stage ? ub : ue); u0 += 32) {
+      const int nu = min(32, ue - u0);
       FFUpd U{};
       int dkw = 0, dkw8 = 0, dR = 0;
       int64_t dw = 0;
@@ -198,6 +202,38 @@ __global__ void __launch_bounds__(32 * kFWarps, SC_FMINB) factor_kernel(DevFacto
       }
     }
 
+
+    if (part) {  // partial block -> its slot ([value][lane], coalesced), then release
+      double* pb = F.pbuf + (F.sub_part_base[sub] + pt.slot) * 1024;
+#pragma unroll
+      for (int I = 0; I < 4; I++)
+#pragma unroll
+        for (int J = 0; J < 4; J++) {
+          pb[((I * 4 + J) * 2) * 32 + lane] = acc[I][J][0];
+          pb[((I * 4 + J) * 2 + 1) * 32 + lane] = acc[I][J][1];
+        }
+      __syncwarp();
+      if (lane == 0) red_release_add(F.pflags + F.sub_part_base[sub] + pt.slot, 1);
+      break;
+    }
+    if (!stage && fr.part_end > fr.part_begin) {  // the split-off partial blocks, in slot order
+      for (int q = fr.part_begin; q < fr.part_end; q++) {
+        const int64_t slot = F.sub_part_base[sub] + q;
+        if (lane == 0) {
+          while (ld_relaxed(F.pflags + slot) < 1) __nanosleep(32);
+          fence_acq_rel();
+        }
+        __syncwarp();
+        const double* pb = F.pbuf + slot * 1024;
+#pragma unroll
+        for (int I = 0; I < 4; I++)
+#pragma unroll
+          for (int J = 0; J < 4; J++) {
+            acc[I][J][0] += __ldcg(pb + ((I * 4 + J) * 2) * 32 + lane);
+            acc[I][J][1] += __ldcg(pb + ((I * 4 + J) * 2 + 1) * 32 + lane);
+          }
+      }
+    }
 
     // ---- S = K entries - updates (frame layout, row-major in the warp's shared buffer); stage mode:
     // S = the frame's entries of the given L (zeros elsewhere)
@@ -395,17 +431,21 @@ __global__ void __launch_bounds__(32 * kFWarps) implicit_fwd_kernel(DevFactor F,
     task = __shfl_sync(~0u, task, 0);
     if (task >= ntask) break;
     const I2 pt = F.ptasks[task];
-    const FPanel pn = F.panels[pt.y];
+    const bool part = pt.y < 0;  // partial updates of a split diagonal frame
+    const FPart pp = part ? F.parts[-1 - pt.y] : FPart{};
+    const FFrame fr = F.frames[part ? pp.frame : F.panels[pt.y].frame_begin];
+    const FPanel pn = F.panels[fr.panel];
+    const int pg = fr.panel;
     const int sub = pt.x, cls = F.sub_cls[sub];
     int* flags = F.flags + (F.sub_flag_base[sub] - F.cls_panel0[cls]);
     const double* W = F.W + F.sub_W_base[sub];
     double* x = F.xv + F.sub_x_base[sub];
     const int kw = pn.kw;
-    const double b = lane < kw ? x[pn.a + lane] : 0.0;  // P B~^T lambda (implicit_b_kernel)
+    const double b = !part && lane < kw ? x[pn.a + lane] : 0.0;  // P B~^T lambda (implicit_b_kernel)
     acc[lane] = 0.0;
-    const FFrame fr = F.frames[pn.frame_begin];
-    for (int u0 = fr.u_begin; u0 < fr.u_end; u0 += 32) {
-      const int nu = min(32, fr.u_end - u0);
+    const int ub = part ? pp.u_begin : fr.u_begin, ue = part ? pp.u_end : fr.u_end;
+    for (int u0 = ub; u0 < ue; u0 += 32) {
+      const int nu = min(32, ue - u0);
       FFUpd U{};
       int dkw = 0, dnR = 0, dR = 0, da = 0;
       int64_t dw = 0;
@@ -450,6 +490,23 @@ __global__ void __launch_bounds__(32 * kFWarps) implicit_fwd_kernel(DevFactor F,
       }
     }
     __syncwarp();
+    if (part) {  // partial sums -> the part's slot, then release
+      const int64_t slot = F.sub_part_base[sub] + pp.slot;
+      F.pbuf[slot * 1024 + lane] = acc[lane];
+      __syncwarp();
+      if (lane == 0) red_release_add(F.pflags + slot, 1);
+      continue;
+    }
+    for (int q = fr.part_begin; q < fr.part_end; q++) {  // the split-off partial sums, in slot order
+      const int64_t slot = F.sub_part_base[sub] + q;
+      if (lane == 0) {
+        while (ld_relaxed(F.pflags + slot) < 1) __nanosleep(32);
+        fence_acq_rel();
+      }
+      __syncwarp();
+      acc[lane] += __ldcg(F.pbuf + slot * 1024 + lane);
+      __syncwarp();
+    }
     const double v = lane < kw ? b - acc[lane] : 0.0;
     const double* inv = W + pn.inv_off;  // column-major kw8 x kw8: inv[i][k] at k kw8 + i
     double y = 0.0;
@@ -462,7 +519,7 @@ __global__ void __launch_bounds__(32 * kFWarps) implicit_fwd_kernel(DevFactor F,
     if (lane < kw) x[pn.a + lane] = y;
     __syncwarp();
     if (lane == 0) {
-      red_release_add(flags + pt.y, 1);
+      red_release_add(flags + pg, 1);
     }
   }
 }
@@ -475,6 +532,7 @@ __global__ void __launch_bounds__(32 * kFWarps) implicit_bwd_kernel(DevFactor F,
     task = __shfl_sync(~0u, task, 0);
     if (task >= ntask) break;
     const I2 pt = F.ptasks[ntask - 1 - task];
+    if (pt.y < 0) continue;  // partial forward task: nothing to do backward
     const FPanel pn = F.panels[pt.y];
     const int sub = pt.x, cls = F.sub_cls[sub];
     int* flags = F.flags + (F.sub_flag_base[sub] - F.cls_panel0[cls]);
@@ -670,6 +728,15 @@ sc_status upload_factor_plan(Plan& P, std::string& err) {
   FTRY(fupload(F, F.cls_panel0, &D.cls_panel0, err));
   FTRY(fupload(F, F.anc, &D.anc, err));
   FTRY(fupload(F, F.ptasks, &D.ptasks, err));
+  {  // split frames: partial tasks, their slots and blocks
+    std::vector<FPart> pv(F.parts);
+    if (pv.empty()) pv.push_back(FPart{});
+    FTRY(fupload(F, pv, &D.parts, err));
+    FTRY(fupload(F, F.cls_part0, &D.cls_part0, err));
+    FTRY(fupload(F, F.sub_part_base, &D.sub_part_base, err));
+    FTRY(falloc(F, std::max<int64_t>(F.nparts, 1), &D.pflags, err));
+    FTRY(falloc(F, std::max<int64_t>(F.nparts, 1) * 1024, &D.pbuf, err));
+  }
   FTRY(fupload(F, F.bt_rp, &D.bt_rp, err));
   FTRY(fupload(F, F.bt_a, &D.bt_a, err));
   FTRY(fupload(F, F.bt_v, &D.bt_v, err));
@@ -751,6 +818,7 @@ sc_status launch_factorize(Plan& P, const void* const* Kptr, void* const* Lout, 
   F.w_ready = true;  // the workspace holds this factorization (implicit apply)
   FCUDA(cudaMemsetAsync(P.dev.err, 0, sizeof(unsigned long long) * (1 + (size_t)P.nsub), stream));
   FCUDA(cudaMemsetAsync(F.dev.flags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nflags, 1), stream));
+  FCUDA(cudaMemsetAsync(F.dev.pflags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nparts, 1), stream));
   FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
   return factor_range(P, 0, F.task_chunk[0], 0, stream, err);
 }
@@ -773,6 +841,7 @@ sc_status launch_implicit_solve(Plan& P, const double* lambda, void* stream_v, s
   FactorPlan& F = P.fac;
   const int64_t nt = (int64_t)F.ptasks.size();
   FCUDA(cudaMemsetAsync(F.dev.flags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nflags, 1), stream));
+  FCUDA(cudaMemsetAsync(F.dev.pflags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nparts, 1), stream));
   FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
   if (nt > 0) {
     static int nsm = 0;
@@ -825,6 +894,7 @@ sc_status factorize_assemble_host(Plan& P, const void* const* Khost, void* strea
   FTRY(set_ptrs(P, Kd.data(), Lst.data(), stream, err));
   F.w_ready = true;
   FCUDA(cudaMemsetAsync(F.dev.flags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nflags, 1), stream));
+  FCUDA(cudaMemsetAsync(F.dev.pflags, 0, sizeof(int32_t) * (size_t)std::max<int64_t>(F.nparts, 1), stream));
   FCUDA(cudaMemsetAsync(F.dev.queue, 0, sizeof(int32_t) * kQueueSlots, stream));
   // pinned (device-mapped) host arrays: one gather kernel on `stream`; otherwise cudaMemcpyAsync per
   // host-contiguous run on the copy stream

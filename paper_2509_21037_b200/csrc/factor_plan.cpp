@@ -175,10 +175,23 @@ sc_status analyse_factor_class(const ClassPlan& C, const sc_K_pattern* Kp, Facto
     fprintf(stderr, "factor class: n %d panels %d frames %zu frame-updates %zu (max %zu per frame) update rows %zu levels %d\n",
             n, np, F.frames.size(), nu, maxu, rows, F.max_level);
   }
+  // frames with more than `split` descendant updates keep the first `split` and hand the rest to
+  // partial update tasks of at most `split` updates each (their blocks are summed by the frame)
+  int split = 8;
+  if (const char* e = std::getenv("SC_FACTOR_SPLIT")) split = std::atoi(e);
+  F.parts.clear();
   for (size_t f = 0; f < F.frames.size(); f++) {
     F.frames[f].u_begin = (int32_t)F.fupd.size();
     F.fupd.insert(F.fupd.end(), fl[f].begin(), fl[f].end());
     F.frames[f].u_end = (int32_t)F.fupd.size();
+    F.frames[f].part_begin = F.frames[f].part_end = (int32_t)F.parts.size();
+    const int32_t nu = F.frames[f].u_end - F.frames[f].u_begin;
+    if (split > 0 && nu > split) {
+      for (int32_t u = F.frames[f].u_begin + split; u < F.frames[f].u_end; u += split)
+        F.parts.push_back(FPart{(int32_t)f, u, std::min(u + split, F.frames[f].u_end), (int32_t)F.parts.size()});
+      F.frames[f].u_end = F.frames[f].u_begin + split;
+      F.frames[f].part_end = (int32_t)F.parts.size();
+    }
   }
   // 4. entry maps
   std::vector<int32_t> iperm((size_t)n);
@@ -328,6 +341,8 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
   F.frames.clear();
   F.kent.clear();
   F.lent.clear();
+  F.parts.clear();
+  F.cls_part0.assign((size_t)ncls + 1, 0);
   F.cls_panel0.assign((size_t)ncls + 1, 0);
   for (int32_t c = 0; c < ncls; c++) {
     const FactorClass& fc = F.classes[(size_t)c];
@@ -356,6 +371,13 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
       u.d += p0;
       F.fupd.push_back(u);
     }
+    F.cls_part0[(size_t)c] = (int32_t)F.parts.size();
+    for (FPart pt : fc.parts) {
+      pt.frame += f0;
+      pt.u_begin += u0;
+      pt.u_end += u0;
+      F.parts.push_back(pt);
+    }
     for (FFrame fr : fc.frames) {
       fr.panel += p0;
       fr.u_begin += u0;
@@ -370,6 +392,11 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
     F.lent.insert(F.lent.end(), fc.lent.begin(), fc.lent.end());
   }
   F.cls_panel0[(size_t)ncls] = (int32_t)F.panels.size();
+  F.cls_part0[(size_t)ncls] = (int32_t)F.parts.size();
+  F.sub_part_base.assign((size_t)nsub + 1, 0);
+  for (int32_t i = 0; i < nsub; i++)
+    F.sub_part_base[(size_t)i + 1] = F.sub_part_base[(size_t)i] + (int64_t)F.classes[(size_t)P.sub_cls[(size_t)i]].parts.size();
+  F.nparts = F.sub_part_base[(size_t)nsub];
   // per-subdomain workspace and flags
   F.sub_W_base.assign((size_t)nsub + 1, 0);
   F.sub_flag_base.assign((size_t)nsub + 1, 0);
@@ -428,6 +455,21 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
       }
     }
   }
+  // frames inside multi-panel subtree units are processed in order by the unit's warp: their updates
+  // are not split (a partial task placed before the unit would wait for frames of the unit itself)
+  for (int32_t c = 0; c < ncls; c++)
+    for (const auto& un : cls_units[(size_t)c])
+      if (un.first < un.second)
+        for (int32_t q = un.first; q <= un.second; q++) {
+          const FPanel& pa = F.panels[(size_t)(F.cls_panel0[(size_t)c] + q)];
+          for (int32_t f = 0; f < pa.nframe; f++) {
+            FFrame& fr = F.frames[(size_t)(pa.frame_begin + f)];
+            if (fr.part_end > fr.part_begin) {
+              fr.u_end = F.parts[(size_t)(F.cls_part0[(size_t)c] + fr.part_end - 1)].u_end;
+              fr.part_begin = fr.part_end;
+            }
+          }
+        }
   auto order = [&](int32_t s0, int32_t s1) {
     int32_t maxlev = 0;
     for (int32_t i = s0; i < s1; i++) maxlev = std::max(maxlev, F.classes[(size_t)P.sub_cls[(size_t)i]].max_level);
@@ -440,13 +482,29 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
         if (un.first < un.second) {  // subtree unit: all its frames, panel order, level 0
           const FPanel& pb = F.panels[(size_t)(p0 + un.second)];
           bylev[0].push_back(FTask{i, pa.frame_begin, pb.frame_begin + pb.nframe - pa.frame_begin, 0});
-        } else if (pa.nframe <= merge) {  // small panel: one warp does the diagonal and then its rows
-          bylev[(size_t)pa.level].push_back(FTask{i, pa.frame_begin, pa.nframe, 0});
         } else {
-          for (int32_t f = 0; f < pa.nframe; f++) bylev[(size_t)pa.level].push_back(FTask{i, pa.frame_begin + f, 1, 0});
+          // partial update tasks of the panel's frames first (a frame task waits for its partials,
+          // which only wait for descendants: earlier in the queue), nf = -1 marks them
+          for (int32_t f = 0; f < pa.nframe; f++) {
+            const FFrame& fr = F.frames[(size_t)(pa.frame_begin + f)];
+            for (int32_t q = fr.part_begin; q < fr.part_end; q++)
+              bylev[(size_t)pa.level].push_back(FTask{i, F.cls_part0[(size_t)c] + q, -1, 0});
+          }
+          if (pa.nframe <= merge) {  // small panel: one warp does the diagonal and then its rows
+            bylev[(size_t)pa.level].push_back(FTask{i, pa.frame_begin, pa.nframe, 0});
+          } else {
+            for (int32_t f = 0; f < pa.nframe; f++) bylev[(size_t)pa.level].push_back(FTask{i, pa.frame_begin + f, 1, 0});
+          }
         }
       }
-      for (int32_t p = p0; p < F.cls_panel0[(size_t)c + 1]; p++) pbylev[(size_t)F.panels[(size_t)p].level].push_back(I2{i, p});
+      for (int32_t p = p0; p < F.cls_panel0[(size_t)c + 1]; p++) {
+        // implicit forward: the split-off partial updates of the panel's diagonal frame first
+        // (y = -1 - global part index), then the panel
+        const FFrame& fr = F.frames[(size_t)F.panels[(size_t)p].frame_begin];
+        for (int32_t q = fr.part_begin; q < fr.part_end; q++)
+          pbylev[(size_t)F.panels[(size_t)p].level].push_back(I2{i, -1 - (F.cls_part0[(size_t)c] + q)});
+        pbylev[(size_t)F.panels[(size_t)p].level].push_back(I2{i, p});
+      }
     }
     for (auto& v : bylev) F.tasks.insert(F.tasks.end(), v.begin(), v.end());
     for (auto& v : pbylev) F.ptasks.insert(F.ptasks.end(), v.begin(), v.end());

@@ -235,7 +235,16 @@ struct FUpd {
 struct FFrame {
   int32_t panel, r0, nrow, pad;
   int32_t k_begin, k_end, l_begin, l_end;
-  int32_t u_begin, u_end;
+  int32_t u_begin, u_end;          // the frame task's own updates
+  int32_t part_begin, part_end;    // its split-off partial update tasks (FPart, class-local index
+                                   //   relative to the subdomain's partial slots; global list offset
+                                   //   via cls_part0)
+};
+// Partial update task of a frame with many descendant updates (SC_FACTOR_SPLIT): accumulates the
+// updates [u_begin, u_end) of `frame` into a partial 32 x 32 block (subdomain slot `slot`), summed
+// by the frame task in slot order.
+struct FPart {
+  int32_t frame, u_begin, u_end, slot;
 };
 // Descendant panel d updates one frame of p: the frame's columns get d's rows R_d[s0, s1) (values in
 // [a_p, a_p + kw_p)); its rows get R_d[k0, k1) (diagonal frame: k0 = s0, k1 = s1; row frame: the rows of
@@ -259,6 +268,7 @@ struct FactorClass {
   std::vector<FUpd> upd;
   std::vector<FFrame> frames;
   std::vector<FFUpd> fupd;
+  std::vector<FPart> parts;        // partial update tasks (class-local frame / update indices)
   std::vector<FEnt> kent, lent;
   std::vector<FUpd> anc;           // per panel (FPanel::anc_*): {ancestor a, s0, s1}
   std::vector<int32_t> bt_rp, bt_a; // B~^T by permuted row (CSR, n+1 / entries): stepped column, value
@@ -301,6 +311,12 @@ struct DevFactor {
   const void* const* Lin;          // stage mode: the plan's L table (DevPlan::Lptr)
   const int64_t* slm;              // = DevPlan::slm / sub_slm_off (stepped lambda map)
   const int64_t* sub_slm_off;
+  // split frames (SC_FACTOR_SPLIT): partial update tasks, their per-subdomain slots and flags
+  const FPart* parts;              // global list (FPart::frame / u_* global)
+  const int32_t* cls_part0;        // per class: first entry of its parts in the global list
+  const int64_t* sub_part_base;    // per subdomain: first partial slot
+  int32_t* pflags;                 // per partial slot: 1 once its block is written
+  double* pbuf;                    // per partial slot: 32 lanes x 32 accumulator values ([value][lane])
 };
 
 struct FactorPlan {
@@ -314,6 +330,10 @@ struct FactorPlan {
   std::vector<FTask> tasks;
   std::vector<FUpd> anc;
   std::vector<I2> ptasks;
+  std::vector<FPart> parts;        // global
+  std::vector<int32_t> cls_part0;
+  std::vector<int64_t> sub_part_base;
+  int64_t nparts = 0;              // partial slots over all subdomains
   std::vector<int32_t> bt_rp, bt_a;
   std::vector<double> bt_v;
   std::vector<int64_t> cls_bt0, sub_x_base;
