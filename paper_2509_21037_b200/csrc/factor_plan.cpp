@@ -343,6 +343,7 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
   F.lent.clear();
   F.parts.clear();
   F.cls_part0.assign((size_t)ncls + 1, 0);
+  F.cls_frame0.assign((size_t)ncls + 1, 0);
   F.cls_panel0.assign((size_t)ncls + 1, 0);
   for (int32_t c = 0; c < ncls; c++) {
     const FactorClass& fc = F.classes[(size_t)c];
@@ -372,6 +373,7 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
       F.fupd.push_back(u);
     }
     F.cls_part0[(size_t)c] = (int32_t)F.parts.size();
+    F.cls_frame0[(size_t)c] = f0;
     for (FPart pt : fc.parts) {
       pt.frame += f0;
       pt.u_begin += u0;
@@ -470,6 +472,62 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
             }
           }
         }
+  // partial-update slots cost 8 KB each per subdomain.  Over the budget (SC_FACTOR_SPLIT_MB, default
+  // 8192 MB) consecutive partials of a frame are merged 2, 4, ... at a time (16, 32, ... updates per
+  // partial task); past 64x the frames are not split at all (e.g. cfg5's 64 large subdomains would
+  // need 64 GB at 8 updates per partial)
+  {
+    double mb = 8192.0;
+    if (const char* e = std::getenv("SC_FACTOR_SPLIT_MB")) mb = std::atof(e);
+    std::vector<int64_t> ncls_sub((size_t)ncls, 0);
+    for (int32_t i = 0; i < nsub; i++) ncls_sub[(size_t)P.sub_cls[(size_t)i]]++;
+    auto slots = [&](int k) {  // partial slots over all subdomains when merging k partials
+      double tot = 0;
+      for (int32_t c = 0; c < ncls; c++)
+        for (int32_t g = 0; g < (int32_t)F.classes[(size_t)c].frames.size(); g++) {
+          const FFrame& fr = F.frames[(size_t)(F.cls_frame0[(size_t)c] + g)];
+          tot += (double)ncls_sub[(size_t)c] * (double)((fr.part_end - fr.part_begin + k - 1) / k);
+        }
+      return tot;
+    };
+    int k = 1;
+    while (k <= 64 && 8192.0 * slots(k) > mb * 1e6) k *= 2;
+    if (k > 1) {  // rebuild the partial lists with k partials merged (or none past 64)
+      std::vector<FPart> np;
+      std::vector<int32_t> cp0((size_t)ncls + 1, 0);
+      for (int32_t c = 0; c < ncls; c++) {
+        cp0[(size_t)c] = (int32_t)np.size();
+        int32_t local = 0;
+        for (int32_t g = 0; g < (int32_t)F.classes[(size_t)c].frames.size(); g++) {
+          FFrame& fr = F.frames[(size_t)(F.cls_frame0[(size_t)c] + g)];
+          const int32_t pb = fr.part_begin, pe = fr.part_end;
+          fr.part_begin = fr.part_end = local;
+          if (pe <= pb) continue;
+          if (k > 64) {  // no split
+            fr.u_end = F.parts[(size_t)(F.cls_part0[(size_t)c] + pe - 1)].u_end;
+            continue;
+          }
+          for (int32_t q = pb; q < pe; q += k) {
+            FPart m = F.parts[(size_t)(F.cls_part0[(size_t)c] + q)];
+            m.u_end = F.parts[(size_t)(F.cls_part0[(size_t)c] + std::min(pe, q + k) - 1)].u_end;
+            m.slot = local++;
+            np.push_back(m);
+          }
+          fr.part_end = local;
+        }
+      }
+      cp0[(size_t)ncls] = (int32_t)np.size();
+      F.parts.swap(np);
+      F.cls_part0.swap(cp0);
+      F.sub_part_base.assign((size_t)nsub + 1, 0);
+      for (int32_t i = 0; i < nsub; i++) {
+        const int32_t c = P.sub_cls[(size_t)i];
+        F.sub_part_base[(size_t)i + 1] = F.sub_part_base[(size_t)i] + (F.cls_part0[(size_t)c + 1] - F.cls_part0[(size_t)c]);
+      }
+      F.nparts = F.sub_part_base[(size_t)nsub];
+    }
+    F.part_merge = k;
+  }
   auto order = [&](int32_t s0, int32_t s1) {
     int32_t maxlev = 0;
     for (int32_t i = s0; i < s1; i++) maxlev = std::max(maxlev, F.classes[(size_t)P.sub_cls[(size_t)i]].max_level);

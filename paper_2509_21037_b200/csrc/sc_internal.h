@@ -331,9 +331,10 @@ struct FactorPlan {
   std::vector<FUpd> anc;
   std::vector<I2> ptasks;
   std::vector<FPart> parts;        // global
-  std::vector<int32_t> cls_part0;
+  std::vector<int32_t> cls_part0, cls_frame0;
   std::vector<int64_t> sub_part_base;
   int64_t nparts = 0;              // partial slots over all subdomains
+  int32_t part_merge = 1;          // partials merged per slot to fit the budget (> 64: no split)
   std::vector<int32_t> bt_rp, bt_a;
   std::vector<double> bt_v;
   std::vector<int64_t> cls_bt0, sub_x_base;
