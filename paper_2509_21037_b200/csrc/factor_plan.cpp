@@ -473,26 +473,35 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
           }
         }
   // partial-update slots cost 8 KB each per subdomain.  Over the budget (SC_FACTOR_SPLIT_MB, default
-  // 8192 MB) consecutive partials of a frame are merged 2, 4, ... at a time (16, 32, ... updates per
-  // partial task); past 64x the frames are not split at all (e.g. cfg5's 64 large subdomains would
-  // need 64 GB at 8 updates per partial)
+  // 8192 MB) only the frames with more than t = 16, 32, ... updates stay split (the heaviest frames
+  // are the ones on the critical path), then, if still over, consecutive partials of a frame are
+  // merged 2, 4, ... at a time; past that nothing is split
   {
     double mb = 8192.0;
     if (const char* e = std::getenv("SC_FACTOR_SPLIT_MB")) mb = std::atof(e);
     std::vector<int64_t> ncls_sub((size_t)ncls, 0);
     for (int32_t i = 0; i < nsub; i++) ncls_sub[(size_t)P.sub_cls[(size_t)i]]++;
-    auto slots = [&](int k) {  // partial slots over all subdomains when merging k partials
+    auto nupd = [&](int32_t c, const FFrame& fr) {  // all updates of a (possibly split) frame
+      return fr.part_end > fr.part_begin ? F.parts[(size_t)(F.cls_part0[(size_t)c] + fr.part_end - 1)].u_end - fr.u_begin
+                                         : fr.u_end - fr.u_begin;
+    };
+    auto slots = [&](int t, int k) {  // slots over all subdomains: frames with > t updates, k merged
       double tot = 0;
       for (int32_t c = 0; c < ncls; c++)
         for (int32_t g = 0; g < (int32_t)F.classes[(size_t)c].frames.size(); g++) {
           const FFrame& fr = F.frames[(size_t)(F.cls_frame0[(size_t)c] + g)];
-          tot += (double)ncls_sub[(size_t)c] * (double)((fr.part_end - fr.part_begin + k - 1) / k);
+          if (fr.part_end > fr.part_begin && nupd(c, fr) > t)
+            tot += (double)ncls_sub[(size_t)c] * (double)((fr.part_end - fr.part_begin + k - 1) / k);
         }
       return tot;
     };
-    int k = 1;
-    while (k <= 64 && 8192.0 * slots(k) > mb * 1e6) k *= 2;
-    if (k > 1) {  // rebuild the partial lists with k partials merged (or none past 64)
+    int t = 0, k = 1;
+    while (t < 256 && 8192.0 * slots(t, 1) > mb * 1e6) t = t ? 2 * t : 16;
+    if (t >= 256) {
+      t = 128;
+      while (k <= 64 && 8192.0 * slots(t, k) > mb * 1e6) k *= 2;
+    }
+    if (t > 0 || k > 1) {  // rebuild the partial lists
       std::vector<FPart> np;
       std::vector<int32_t> cp0((size_t)ncls + 1, 0);
       for (int32_t c = 0; c < ncls; c++) {
@@ -500,10 +509,10 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
         int32_t local = 0;
         for (int32_t g = 0; g < (int32_t)F.classes[(size_t)c].frames.size(); g++) {
           FFrame& fr = F.frames[(size_t)(F.cls_frame0[(size_t)c] + g)];
-          const int32_t pb = fr.part_begin, pe = fr.part_end;
+          const int32_t pb = fr.part_begin, pe = fr.part_end, nu = nupd(c, fr);
           fr.part_begin = fr.part_end = local;
           if (pe <= pb) continue;
-          if (k > 64) {  // no split
+          if (nu <= t || k > 64) {  // not split
             fr.u_end = F.parts[(size_t)(F.cls_part0[(size_t)c] + pe - 1)].u_end;
             continue;
           }
@@ -527,6 +536,10 @@ sc_status build_factor_plan(Plan& P, const sc_K_pattern* kp, int32_t nsub, std::
       F.nparts = F.sub_part_base[(size_t)nsub];
     }
     F.part_merge = k;
+    F.part_min_updates = t;
+    if (std::getenv("SC_DEBUG_FACTOR"))
+      fprintf(stderr, "factor split: frames with > %d updates, %d partials per slot, %lld slots (%.1f MB)\n", std::max(t, 8), k,
+              (long long)F.nparts, 8192.0 * (double)F.nparts / 1e6);
   }
   auto order = [&](int32_t s0, int32_t s1) {
     int32_t maxlev = 0;

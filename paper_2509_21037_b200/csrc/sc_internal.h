@@ -335,6 +335,7 @@ struct FactorPlan {
   std::vector<int64_t> sub_part_base;
   int64_t nparts = 0;              // partial slots over all subdomains
   int32_t part_merge = 1;          // partials merged per slot to fit the budget (> 64: no split)
+  int32_t part_min_updates = 0;    // only frames with more updates than this are split (budget)
   std::vector<int32_t> bt_rp, bt_a;
   std::vector<double> bt_v;
   std::vector<int64_t> cls_bt0, sub_x_base;
